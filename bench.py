@@ -1,0 +1,329 @@
+"""Benchmark of the B200 HYDRO step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (N=1): BASELINE config 1 -- 2048x2048 fp64 Sod shock along x,
+transmissive boundaries, gamma 1.4, CFL 0.8, MUSCL-Hancock + minmod + HLLC
+(the reference's hot-path flux), 200 time steps.  One bench "step" is one
+such 200-time-step run from the initial condition.  For N>1 the grid grows
+along i by N (weak scaling: each rank holds a 2048x2048 row slab, halo swap
++ dt min-allreduce over NCCL every time step).
+
+Metric: cell-updates/s = interior cells x time steps / seconds (both sweeps +
+the dt reduction per time step).  ``value`` is device-resident (state in HBM
+before the timed region, CUDA events on the launch stream, max over ranks);
+``e2e`` goes through the C-ABI with pinned host buffers: upload, run, download
+every bench step.  ``--impl reference`` times the reference's own CPU
+implementation (oracle/_ref, coarse_grain over all host threads) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NX = NY = 2048
+TSTEPS = 200
+CASE, BC = "sod_x", "transmit"
+METRIC = "cell-updates/s (both sweeps, fp64)"
+UNIT = "cell-updates/s"
+ALG_BYTES_PER_CELL_SWEEP = 64  # 32 B read + 32 B write of 4 fp64 fields
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, ValueError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_reference_sample(steps_per_sample: int, threads: int):
+    """Times the reference's own CPU path (oracle/_ref coarse_grain) -- or the C
+    port if the compiled reference is absent -- on `steps_per_sample` time
+    steps of the workload.  Returns (cell-steps/s, kind, seconds)."""
+    from oracle import oracle as O
+    g = O.make_case(CASE, NX, NY)
+    if O.ref_available():
+        warm = g.copy()
+        O.ref_run(warm, 1, BC, "coarse_grain", threads)
+        secs = O.ref_run(g, steps_per_sample, BC, "coarse_grain", threads)
+        kind = "reference"
+    else:
+        t0 = time.perf_counter()
+        O.run_sequential(g, steps_per_sample, BC)
+        secs = time.perf_counter() - t0
+        kind, threads = "port", 1
+    return NX * NY * steps_per_sample / secs, kind, secs, threads
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    sample_steps = 5
+    vals, kind = [], None
+    for k in range(args.warmup + args.steps):
+        v, kind, secs, used = cpu_reference_sample(sample_steps, threads)
+        if k >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": NX * NY * sample_steps / value * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (analytic Sod initial condition)",
+        "config": {"workload": f"BASELINE config 1 sample: {NX}x{NY} {CASE} {BC}, "
+                               f"{sample_steps} time steps per bench step",
+                   "global_batch": NX * NY, "parallelism": f"cpu coarse_grain x{used}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": kind,
+                         "sample": f"{sample_steps} time steps of the {NX}x{NY} config-1 grid, "
+                                   "reference coarse_grain (bench.cpp:53-90 dispatch)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2106_13465_b200 as P
+    from paper_2106_13465_b200 import slab as S
+
+    assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    model = P.GasModel()
+    global_nx = NX * world
+    dx, dy = 1.0 / global_nx, 1.0 / NY
+    stream = torch.cuda.current_stream()
+
+    geo = S.SlabGeometry(global_nx, NY, rank, world)
+    if world == 1:
+        grid = P.GpuGrid(NX, NY, dx, dy, model, BC, device=local)
+        grid.set_stream(stream.cuda_stream)
+        slab = None
+    else:
+        slab = S.GpuSlab(geo, dx, dy, model, BC, local)
+        slab.bind_stream(stream)
+        grid = slab.grid
+        comm = S.TorchComm()
+
+    def one_step():
+        grid.init_case(CASE, 0)
+        if world == 1:
+            grid.run_async(TSTEPS)
+        else:
+            S.run_slab(slab, comm, TSTEPS)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        one_step()
+    if world == 1:
+        grid.sync()
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region -----------------------------------
+    clocks = ClockSampler(local)
+    grid.reset_counters()
+    grid.set_timing(True)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clock_info = clocks.stop()
+    if world == 1:
+        grid.sync()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    kt = grid.kernel_times()
+    grid.set_timing(False)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    cells = global_nx * NY
+    value = cells * TSTEPS * args.steps / (ms / 1e3)
+    launches = kt["n_x"] + kt["n_y"] + kt["n_other"] + args.steps  # + init kernels
+
+    # ---- end-to-end through the C-ABI with pinned host buffers --------------
+    host0 = torch.zeros((4, geo.nx + 4, NY + 4), dtype=torch.float64).pin_memory()
+    host = torch.zeros_like(host0).pin_memory()
+    init = P.make_case(CASE, global_nx, NY, model) if world == 1 else None
+    if init is not None:
+        host0.copy_(torch.from_numpy(init.planes))
+    else:
+        full = P.make_case(CASE, global_nx, NY, model)
+        host0.copy_(torch.from_numpy(S.slab_planes(full.planes, global_nx, world, rank)))
+        del full
+    ptrs0 = [host0[v].data_ptr() for v in range(4)]
+    ptrs = [host[v].data_ptr() for v in range(4)]
+
+    def e2e_step():
+        grid.upload_ptr(ptrs0, NY + 4)
+        if world == 1:
+            grid.run(TSTEPS)
+        else:
+            S.run_slab(slab, comm, TSTEPS)
+        grid.download_ptr(ptrs, NY + 4)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = cells * TSTEPS * args.steps / e2e_s
+    plane_bytes = 4 * (geo.nx + 4) * (NY + 4) * 8
+
+    # result check of the e2e leg against the digest of the first run
+    digest = P.grid_digest(P.Grid2D(geo.nx, NY, dx, dy, host.numpy())) if world == 1 else None
+
+    # ---- roofline of the dominant sweep kernel ------------------------------
+    peak, peak_src = peaks()
+    which = "x" if kt["ms_x"] >= kt["ms_y"] else "y"
+    n_launch = max(1, kt[f"n_{which}"])
+    avg_ms = kt[f"ms_{which}"] / n_launch
+    alg_bytes = geo.nx * NY * ALG_BYTES_PER_CELL_SWEEP
+    achieved = alg_bytes / (avg_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        traffic = json.load(open(prof)).get(f"sweep_{which}_bytes_per_launch")
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v, kind, secs, used = cpu_reference_sample(10, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": used, "kind": kind,
+               "sample": f"10 time steps of the {NX}x{NY} config-1 grid ({secs:.1f}s), "
+                         f"reference coarse_grain over {used} host threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (analytic Sod initial condition, no dataset)",
+            "config": {"workload": f"BASELINE config 1: {global_nx}x{NY} {CASE} {BC}, HLLC, "
+                                   f"{TSTEPS} time steps per bench step",
+                       "global_batch": cells, "seq_len": TSTEPS,
+                       "parallelism": f"row slabs x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (2 x 134 MB state per GPU)",
+                       "flux": "hllc"},
+            "roofline": {"bound": "hbm", "kernel": f"sweep_{which}", "achieved": achieved,
+                         "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": plane_bytes,
+                    "d2h_bytes_per_step": plane_bytes},
+            "gpu_launches": launches,
+            "kernel_ms": {"sweep_x": kt["ms_x"], "sweep_y": kt["ms_y"], "other": kt["ms_other"]},
+            "clocks": clock_info,
+            "cpu_baseline": cpu,
+            "result_digest": f"{digest:016x}" if digest is not None else None,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,192 @@
+/*
+ * hydro_gpu.h -- C-ABI of the B200-native HYDRO time step (libhydro_b200.so).
+ *
+ * This is the drop-in boundary for the reference hydro2d's stepping entry
+ * points (all paths relative to /root/reference/):
+ *
+ *   reference (proj/include/hydro/schedulers.hpp)       replaced by
+ *   -------------------------------------------------  ---------------------
+ *   run_sequential(Grid2D&, const GasModel&, int)   :24  hydro_gpu_run
+ *   advance_sequential(Grid2D&, const GasModel&, dt):21  hydro_gpu_advance
+ *   run_until(Grid2D&, const GasModel&, double)     :28  hydro_gpu_run_until
+ *   compute_dt(const Grid2D&, const GasModel&)  euler_kernel.hpp:75
+ *                                                        hydro_gpu_compute_dt
+ *   grid_checksum(...).digest          audit.hpp:34      hydro_grid_digest
+ *   Grid2D storage (4 planes, grid.hpp:26-64)            hydro_gpu_upload /
+ *                                                        hydro_gpu_download
+ *   run_strategy dispatch (proj/src/bench.cpp:53-90)     a "gpu" strategy
+ *
+ *
+ * Conventions: plain C types only, no exceptions cross the boundary, every
+ * call returns an int status: 0 = OK, 1..7 = hydro::ErrorCategory + 1
+ * (proj/include/hydro/errors.hpp:10-18), 8 = CUDA / device failure.  A
+ * positivity failure carries the same step / sweep / strip / cell context the
+ * reference prints (proj/src/schedulers.cpp:23-26,80-91): fetch it with
+ * hydro_gpu_last_error.  A context is single-caller and its calls are
+ * synchronous unless stated otherwise (the reference's callers are
+ * single-threaded).
+ *
+ * Host plane layout accepted by upload/download: the reference Grid2D plane
+ * layout -- (nx+4) rows of `row_stride` doubles, interior cell (i,j) at
+ * row i+1, column j+1 (grid.hpp:54-57).  Pass the address of cell (-1,-1) of
+ * each plane (&grid.at(Var(v), -1, -1)) and row_stride = ny+4.
+ */
+#ifndef HYDRO_GPU_H
+#define HYDRO_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HYDRO_GPU_ABI_VERSION 1
+
+enum hydro_gpu_status {
+  HYDRO_GPU_OK = 0,
+  HYDRO_GPU_ERR_CONFIG = 1,      /* ErrorCategory::Config */
+  HYDRO_GPU_ERR_POSITIVITY = 2,  /* ErrorCategory::Positivity */
+  HYDRO_GPU_ERR_PROTOCOL = 3,
+  HYDRO_GPU_ERR_TASKGRAPH = 4,
+  HYDRO_GPU_ERR_EQUIVALENCE = 5,
+  HYDRO_GPU_ERR_IO = 6,
+  HYDRO_GPU_ERR_VALIDATION = 7,
+  HYDRO_GPU_ERR_CUDA = 8         /* no reference equivalent: device failure */
+};
+
+/* Boundary kind: REFLECT is the reference's apply_boundary
+ * (proj/src/grid.cpp:23-60); TRANSMIT is zero-gradient (both ghost layers
+ * copy the adjacent interior cell), needed by BASELINE configs 1, 2, 4. */
+enum hydro_gpu_bc { HYDRO_GPU_BC_REFLECT = 0, HYDRO_GPU_BC_TRANSMIT = 1 };
+
+/* Riemann flux: HLLC is the reference hot path (euler_kernel.cpp:59-109). */
+enum hydro_gpu_flux { HYDRO_GPU_FLUX_HLLC = 0 };
+
+/* Case ids for the initialisers (cases.cpp:11-69 + BASELINE configs). */
+enum hydro_gpu_case {
+  HYDRO_GPU_CASE_UNIFORM = 0,
+  HYDRO_GPU_CASE_BLAST = 1,
+  HYDRO_GPU_CASE_SOD_J = 2,
+  HYDRO_GPU_CASE_CORNER_BLAST = 3,
+  HYDRO_GPU_CASE_SOD_X = 4,
+  HYDRO_GPU_CASE_RANDOM = 5
+};
+
+typedef struct hydro_gpu_cfg {
+  int nx, ny;          /* interior extent held by this context (a slab for P>1) */
+  double dx, dy;       /* cell sizes (Grid2D::dx/dy) */
+  double gamma, cfl;   /* GasModel (types.hpp:38-41) */
+  int bc;              /* enum hydro_gpu_bc */
+  int flux;            /* enum hydro_gpu_flux */
+  int device;          /* CUDA device ordinal; -1 = the calling thread's current */
+  /* Row-slab decomposition along i.  A full grid is
+   * row0 = 0, global_nx = nx, wall_lo = wall_hi = 1. */
+  int row0;            /* global row index of this slab's first interior row, minus 1 */
+  int global_nx;       /* interior rows of the whole grid */
+  int wall_lo;         /* 1: rows 0,-1 are a physical wall; 0: filled by a halo exchange */
+  int wall_hi;         /* 1: rows nx+1,nx+2 are a physical wall */
+} hydro_gpu_cfg;
+
+typedef struct hydro_gpu_error {
+  int category;        /* enum hydro_gpu_status */
+  int step;            /* step index within the failing call */
+  int phase;           /* 0 = compute_dt, 1 = column sweep, 2 = row sweep */
+  int strip;           /* 1-based strip (column j or row i); grid row for phase 0 */
+  int loop;            /* 0 = primitive conversion, 1 = conservative update */
+  int cell;            /* strip-local index k - kGhost as printed by the reference */
+  int field;           /* 0 = rho, 1 = pres, 2 = internal energy */
+  char message[256];   /* the reference's what() text, context included */
+} hydro_gpu_error;
+
+typedef struct hydro_gpu_ctx hydro_gpu_ctx;
+
+/* ---- lifetime ---------------------------------------------------------- */
+int hydro_gpu_abi_version(void);
+int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out);
+int hydro_gpu_destroy(hydro_gpu_ctx* ctx);
+const char* hydro_gpu_status_string(int status);
+int hydro_gpu_last_error(const hydro_gpu_ctx* ctx, hydro_gpu_error* out);
+
+/* ---- state transfer (host <-> HBM) ------------------------------------- */
+int hydro_gpu_upload(hydro_gpu_ctx* ctx, const double* const planes[4],
+                     size_t row_stride);
+int hydro_gpu_download(hydro_gpu_ctx* ctx, double* const planes[4],
+                       size_t row_stride);
+/* Device-side initialiser, bitwise equal to hydro_init_case_host. */
+int hydro_gpu_init_case(hydro_gpu_ctx* ctx, int case_id, uint64_t seed);
+
+/* ---- the reference's stepping entry points ----------------------------- */
+/* run_sequential: `steps` steps of BC -> dt -> column sweep -> BC -> row
+ * sweep.  *last_dt (may be NULL) receives the dt of the final step. */
+int hydro_gpu_run(hydro_gpu_ctx* ctx, int steps, double* last_dt);
+/* advance_sequential: one step with a caller-chosen dt. */
+int hydro_gpu_advance(hydro_gpu_ctx* ctx, double dt);
+/* run_until: advance to t_end, clamping the last dt; *steps = steps taken. */
+int hydro_gpu_run_until(hydro_gpu_ctx* ctx, double t_end, int* steps);
+/* compute_dt after apply_boundary: cfl * min cell_dt_limit. */
+int hydro_gpu_compute_dt(hydro_gpu_ctx* ctx, double* dt);
+
+/* ---- asynchronous, device-resident interface --------------------------- */
+/* Stream all work of this context is issued on (a cudaStream_t); NULL =
+ * the context's own stream. */
+int hydro_gpu_set_stream(hydro_gpu_ctx* ctx, void* cuda_stream);
+/* Enqueues `steps` steps without synchronising; errors are latched on the
+ * device and reported by the next hydro_gpu_sync. */
+int hydro_gpu_run_async(hydro_gpu_ctx* ctx, int steps);
+int hydro_gpu_sync(hydro_gpu_ctx* ctx);
+
+/* ---- slab phases for multi-GPU drivers (one context per GPU) ----------- */
+/* Physical-wall BC on the current state + local dt limit into the slot
+ * step `step` reads.  Enqueued, not synchronised. */
+int hydro_gpu_slab_prologue(hydro_gpu_ctx* ctx, int step);
+/* Device address of the (pre-cfl) dt limit consumed by `step`: a driver
+ * min-allreduces it across slabs between the previous row sweep and the
+ * column sweep of `step`. */
+int hydro_gpu_limit_slot(hydro_gpu_ctx* ctx, int step, double** dev_ptr);
+/* Device address of the latched error key (uint64, min-combinable). */
+int hydro_gpu_error_slot(hydro_gpu_ctx* ctx, uint64_t** dev_ptr);
+/* Halo rows in the current state: send_lo = interior rows 1..2,
+ * send_hi = rows nx-1..nx, recv_lo = ghost rows -1..0, recv_hi = ghost rows
+ * nx+1..nx+2.  Each is one contiguous block of `count` doubles (2 rows x 4
+ * variables x pitch), so a halo swap is one send/recv per neighbour. */
+int hydro_gpu_halo(hydro_gpu_ctx* ctx, double** send_lo, double** send_hi,
+                   double** recv_lo, double** recv_hi, size_t* count);
+int hydro_gpu_slab_sweep_x(hydro_gpu_ctx* ctx, int step);
+int hydro_gpu_slab_sweep_y(hydro_gpu_ctx* ctx, int step);
+/* Writes the reference's end-of-run ghost state (mirrors of the last
+ * column-sweep output, grid.cpp:23-60 as applied before the last row sweep). */
+int hydro_gpu_slab_finish(hydro_gpu_ctx* ctx);
+/* Synchronises and decodes a (possibly all-reduced) error key. */
+int hydro_gpu_decode_error(hydro_gpu_ctx* ctx, uint64_t key, hydro_gpu_error* out);
+
+/* ---- instrumentation ---------------------------------------------------- */
+/* When on, every sweep launch is bracketed by CUDA events on the launch
+ * stream; hydro_gpu_kernel_times returns the summed device milliseconds and
+ * launch counts since the last reset. */
+int hydro_gpu_set_timing(hydro_gpu_ctx* ctx, int on);
+int hydro_gpu_kernel_times(hydro_gpu_ctx* ctx, double* ms_x, double* ms_y,
+                           double* ms_other, long long* n_x, long long* n_y,
+                           long long* n_other);
+int hydro_gpu_reset_counters(hydro_gpu_ctx* ctx);
+/* Launch-geometry override (0 = default): strip segment length along the
+ * sweep and threads per block. */
+int hydro_gpu_tune(hydro_gpu_ctx* ctx, int seg_x, int seg_y, int block);
+/* Device pointer to plane-interleaved storage and its pitch (doubles). */
+int hydro_gpu_state(hydro_gpu_ctx* ctx, double** dev_ptr, size_t* pitch);
+
+/* ---- host utilities (no device needed) --------------------------------- */
+/* FNV-1a digest of the interior bytes (proj/src/audit.cpp:53-76). */
+uint64_t hydro_grid_digest(const double* const planes[4], size_t row_stride,
+                           int nx, int ny);
+/* Host initialiser for the case ids above; fills 4 planes (zeroing first,
+ * like Grid2D's constructor) and the spacings. */
+int hydro_init_case_host(int case_id, int nx, int ny, double gamma,
+                         uint64_t seed, double* const planes[4],
+                         size_t row_stride, double* dx, double* dy);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HYDRO_GPU_H */

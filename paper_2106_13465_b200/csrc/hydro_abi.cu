@@ -1,0 +1,672 @@
+// hydro_abi.cu -- the extern "C" boundary of libhydro_b200.so (include/hydro_gpu.h).
+//
+// Owns the device state of one grid (or one row slab of a multi-GPU grid):
+// two row-interleaved state buffers used ping-pong (U_a -> column sweep ->
+// U_b -> row sweep -> U_a), four 64-bit device slots (two dt limits, the
+// latched error key, a pending compute_dt error), a stream and optional
+// per-launch CUDA events.  Errors never cross the boundary as exceptions:
+// each call returns a status mirroring hydro::ErrorCategory
+// (proj/include/hydro/errors.hpp:10-18) and records a hydro_gpu_error whose
+// message reproduces the reference's text, context included
+// (proj/src/schedulers.cpp:23-26,80-91).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/hydro_gpu.h"
+#include "hydro_kernels.cuh"
+
+using hb::cell_index;
+
+struct hydro_gpu_ctx {
+  hydro_gpu_cfg cfg;
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  double* A = nullptr;  // current state
+  double* B = nullptr;  // column-sweep output
+  size_t pitch = 0;
+  size_t count = 0;     // doubles per state buffer
+  unsigned long long* slots = nullptr;  // [0],[1] dt limits, [2] error, [3] dt error
+  hydro_gpu_error last{};
+  int seg_x = 0, seg_y = 0, block = 128;
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  struct Pending { cudaEvent_t a, b; int kind; };
+  std::vector<Pending> pending;
+  size_t ev_next = 0;
+  double ms[3] = {0, 0, 0};
+  long long n[3] = {0, 0, 0};
+};
+
+namespace {
+
+constexpr int kSlotErr = 2;
+constexpr int kSlotDtErr = 3;
+
+const char* kFieldName[3] = {"rho", "pres", "internal energy"};
+
+int set_err(hydro_gpu_ctx* c, int cat, const char* fmt, ...) {
+  if (!c) return cat;
+  c->last = hydro_gpu_error{};
+  c->last.category = cat;
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(c->last.message, sizeof(c->last.message), fmt, ap);
+  va_end(ap);
+  return cat;
+}
+
+#define CUDA_TRY(ctx, call)                                                        \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return set_err((ctx), HYDRO_GPU_ERR_CUDA, "cuda: %s (%s:%d)", cudaGetErrorString(e_), \
+                     __FILE__, __LINE__);                                          \
+  } while (0)
+
+bool valid_cfg(const hydro_gpu_cfg* c, char* why, size_t n) {
+  if (c->ny < 4 || c->nx < 2) {
+    std::snprintf(why, n, "grid interior must be at least 4x4, got %dx%d", c->nx, c->ny);
+    return false;
+  }
+  if (c->wall_lo && c->wall_hi && c->nx < 4) {
+    std::snprintf(why, n, "grid interior must be at least 4x4, got %dx%d", c->nx, c->ny);
+    return false;
+  }
+  if (!(c->dx > 0.0) || !(c->dy > 0.0)) {
+    std::snprintf(why, n, "cell sizes must be positive");
+    return false;
+  }
+  if (!(c->gamma > 1.0)) {
+    std::snprintf(why, n, "gamma must exceed 1");
+    return false;
+  }
+  if (c->bc != HYDRO_GPU_BC_REFLECT && c->bc != HYDRO_GPU_BC_TRANSMIT) {
+    std::snprintf(why, n, "unknown boundary kind %d", c->bc);
+    return false;
+  }
+  if (c->flux != HYDRO_GPU_FLUX_HLLC) {
+    std::snprintf(why, n, "unknown flux kind %d", c->flux);
+    return false;
+  }
+  if (c->row0 < 0 || c->global_nx < c->row0 + c->nx) {
+    std::snprintf(why, n, "slab rows [%d, %d) outside a %d-row grid", c->row0,
+                  c->row0 + c->nx, c->global_nx);
+    return false;
+  }
+  if (c->global_nx > (1 << 18) - 8 || c->ny > (1 << 18) - 8) {
+    std::snprintf(why, n, "grid extent exceeds the 2^18-cell strip limit");
+    return false;
+  }
+  return true;
+}
+
+double as_double(unsigned long long bits) {
+  double d;
+  std::memcpy(&d, &bits, sizeof d);
+  return d;
+}
+
+// Event bracket for one launch (timing mode only).
+void ev_begin(hydro_gpu_ctx* c, cudaEvent_t* a) {
+  if (!c->timing) return;
+  if (c->ev_next + 2 > c->ev_pool.size()) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      c->ev_pool.push_back(e);
+    }
+  }
+  *a = c->ev_pool[c->ev_next++];
+  cudaEventRecord(*a, c->stream);
+}
+
+void ev_end(hydro_gpu_ctx* c, cudaEvent_t a, int kind) {
+  if (!c->timing) return;
+  cudaEvent_t b = c->ev_pool[c->ev_next++];
+  cudaEventRecord(b, c->stream);
+  c->pending.push_back({a, b, kind});
+}
+
+void harvest(hydro_gpu_ctx* c) {
+  for (auto& p : c->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+      c->ms[p.kind] += ms;
+      c->n[p.kind] += 1;
+    }
+  }
+  c->pending.clear();
+  c->ev_next = 0;
+}
+
+hb::SweepArgs sweep_args(hydro_gpu_ctx* c, int axis, int step) {
+  hb::SweepArgs a{};
+  a.pitch = c->pitch;
+  a.nx = c->cfg.nx;
+  a.ny = c->cfg.ny;
+  a.dx = axis == 0 ? c->cfg.dx : c->cfg.dy;
+  a.spacing = c->cfg.dx < c->cfg.dy ? c->cfg.dx : c->cfg.dy;  // std::min(dx, dy)
+  a.gamma = c->cfg.gamma;
+  a.cfl = c->cfg.cfl;
+  a.bc = c->cfg.bc;
+  a.wall_lo = c->cfg.wall_lo;
+  a.wall_hi = c->cfg.wall_hi;
+  a.row0 = c->cfg.row0;
+  a.limit_in = c->slots + (step & 1);
+  a.limit_out = c->slots + ((step + 1) & 1);
+  a.err = c->slots + kSlotErr;
+  a.dt_err = c->slots + kSlotDtErr;
+  a.step = step;
+  if (axis == 0) {
+    a.src = c->A;
+    a.dst = c->B;
+    a.seg = c->seg_x;
+  } else {
+    a.src = c->B;
+    a.dst = c->A;
+    a.seg = c->seg_y;
+  }
+  return a;
+}
+
+void enqueue_x(hydro_gpu_ctx* c, int step, int explicit_dt, double dt) {
+  hb::SweepArgs a = sweep_args(c, 0, step);
+  a.explicit_dt = explicit_dt;
+  a.dt_value = dt;
+  cudaEvent_t e0{};
+  ev_begin(c, &e0);
+  hb::launch_sweep_x(a, c->block, c->stream);
+  ev_end(c, e0, 0);
+}
+
+void enqueue_y(hydro_gpu_ctx* c, int step, int explicit_dt, double dt, int want_limit) {
+  hb::SweepArgs a = sweep_args(c, 1, step);
+  a.explicit_dt = explicit_dt;
+  a.dt_value = dt;
+  a.want_limit = want_limit;
+  cudaEvent_t e0{};
+  ev_begin(c, &e0);
+  hb::launch_sweep_y(a, c->block, c->stream);
+  ev_end(c, e0, 1);
+}
+
+// wall_bc: x-wall ghost rows; full_bc: also the y-wall columns;
+// limit_step >= 0: dt limit of that step into its slot.
+void enqueue_prologue(hydro_gpu_ctx* c, int wall_bc, int full_bc, int limit_step) {
+  hb::PrologueArgs p{};
+  p.u = c->A;
+  p.pitch = c->pitch;
+  p.nx = c->cfg.nx;
+  p.ny = c->cfg.ny;
+  p.spacing = c->cfg.dx < c->cfg.dy ? c->cfg.dx : c->cfg.dy;
+  p.gamma = c->cfg.gamma;
+  p.bc = c->cfg.bc;
+  p.wall_lo = wall_bc && c->cfg.wall_lo;
+  p.wall_hi = wall_bc && c->cfg.wall_hi;
+  p.row0 = c->cfg.row0;
+  p.full_bc = full_bc;
+  p.want_limit = limit_step >= 0;
+  p.step = limit_step < 0 ? 0 : limit_step;
+  p.limit_out = c->slots + (p.step & 1);
+  p.err = c->slots + kSlotErr;
+  p.dt_err = c->slots + kSlotDtErr;
+  cudaEvent_t e0{};
+  ev_begin(c, &e0);
+  hb::launch_prologue(p, c->stream);
+  ev_end(c, e0, 2);
+}
+
+void enqueue_finish(hydro_gpu_ctx* c) {
+  hb::FinishArgs f{};
+  f.post_x = c->B;
+  f.u = c->A;
+  f.pitch = c->pitch;
+  f.nx = c->cfg.nx;
+  f.ny = c->cfg.ny;
+  f.bc = c->cfg.bc;
+  f.wall_lo = c->cfg.wall_lo;
+  f.wall_hi = c->cfg.wall_hi;
+  cudaEvent_t e0{};
+  ev_begin(c, &e0);
+  hb::launch_finish(f, c->stream);
+  ev_end(c, e0, 2);
+}
+
+int reset_slots(hydro_gpu_ctx* c) {
+  CUDA_TRY(c, cudaMemsetAsync(c->slots, 0xff, 4 * sizeof(unsigned long long), c->stream));
+  return 0;
+}
+
+void decode(unsigned long long key, hydro_gpu_error* e, bool with_step) {
+  *e = hydro_gpu_error{};
+  e->category = HYDRO_GPU_ERR_POSITIVITY;
+  e->step = (int)(key >> 41);
+  e->phase = (int)((key >> 39) & 3);
+  e->strip = (int)((key >> 21) & 0x3ffff);
+  e->loop = (int)((key >> 20) & 1);
+  const int k = (int)((key >> 2) & 0x3ffff);
+  e->field = (int)(key & 3);
+  char body[200];
+  const char* fname = kFieldName[e->field < 3 ? e->field : 0];
+  if (e->phase == 0) {
+    e->cell = k;  // column j of the failing cell; compute_dt has no strip context
+    std::snprintf(body, sizeof body, "%s non-positive at cons_to_prim input", fname);
+  } else {
+    e->cell = k - 2;  // k - kGhost
+    std::snprintf(body, sizeof body, "%s sweep strip %d: %s non-positive at %sstrip cell %d",
+                  e->phase == 1 ? "column" : "row", e->strip, fname, e->loop ? "updated " : "",
+                  e->cell);
+  }
+  if (with_step)
+    std::snprintf(e->message, sizeof e->message, "step %d: %s", e->step, body);
+  else
+    std::snprintf(e->message, sizeof e->message, "%s", body);
+}
+
+// Synchronises and converts a latched key into a status.
+int finish_status(hydro_gpu_ctx* c, bool with_step) {
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  CUDA_TRY(c, cudaGetLastError());
+  harvest(c);
+  unsigned long long key = 0;
+  CUDA_TRY(c, cudaMemcpy(&key, c->slots + kSlotErr, sizeof key, cudaMemcpyDeviceToHost));
+  if (key == hb::kNoError) {
+    c->last = hydro_gpu_error{};
+    return HYDRO_GPU_OK;
+  }
+  decode(key, &c->last, with_step);
+  return HYDRO_GPU_ERR_POSITIVITY;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int hydro_gpu_abi_version(void) { return HYDRO_GPU_ABI_VERSION; }
+
+const char* hydro_gpu_status_string(int s) {
+  switch (s) {
+    case HYDRO_GPU_OK: return "ok";
+    case HYDRO_GPU_ERR_CONFIG: return "config";
+    case HYDRO_GPU_ERR_POSITIVITY: return "positivity";
+    case HYDRO_GPU_ERR_PROTOCOL: return "protocol";
+    case HYDRO_GPU_ERR_TASKGRAPH: return "task-graph";
+    case HYDRO_GPU_ERR_EQUIVALENCE: return "equivalence";
+    case HYDRO_GPU_ERR_IO: return "io";
+    case HYDRO_GPU_ERR_VALIDATION: return "validation";
+    case HYDRO_GPU_ERR_CUDA: return "cuda";
+  }
+  return "unknown";
+}
+
+int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out) {
+  if (!cfg || !out) return HYDRO_GPU_ERR_CONFIG;
+  *out = nullptr;
+  hydro_gpu_cfg c = *cfg;
+  if (c.global_nx <= 0) c.global_nx = c.nx + c.row0;
+  char why[160];
+  if (!valid_cfg(&c, why, sizeof why)) return HYDRO_GPU_ERR_CONFIG;
+  auto* ctx = new (std::nothrow) hydro_gpu_ctx;
+  if (!ctx) return HYDRO_GPU_ERR_CUDA;
+  ctx->cfg = c;
+  if (c.device >= 0) {
+    if (cudaSetDevice(c.device) != cudaSuccess) {
+      delete ctx;
+      return HYDRO_GPU_ERR_CUDA;
+    }
+  }
+  cudaGetDevice(&ctx->device);
+  ctx->pitch = hb::pitch_for(c.ny);
+  ctx->count = (size_t)(c.nx + 4) * 4 * ctx->pitch;
+  const size_t bytes = ctx->count * sizeof(double);
+  if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&ctx->A, bytes) != cudaSuccess || cudaMalloc(&ctx->B, bytes) != cudaSuccess ||
+      cudaMalloc(&ctx->slots, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+    hydro_gpu_destroy(ctx);
+    cudaGetLastError();
+    return HYDRO_GPU_ERR_CUDA;
+  }
+  ctx->stream = ctx->own_stream;
+  cudaMemsetAsync(ctx->A, 0, bytes, ctx->stream);
+  cudaMemsetAsync(ctx->B, 0, bytes, ctx->stream);
+  cudaMemsetAsync(ctx->slots, 0xff, 4 * sizeof(unsigned long long), ctx->stream);
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+    hydro_gpu_destroy(ctx);
+    return HYDRO_GPU_ERR_CUDA;
+  }
+  *out = ctx;
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_destroy(hydro_gpu_ctx* ctx) {
+  if (!ctx) return HYDRO_GPU_OK;
+  DeviceGuard g(ctx->device);
+  if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->A) cudaFree(ctx->A);
+  if (ctx->B) cudaFree(ctx->B);
+  if (ctx->slots) cudaFree(ctx->slots);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_last_error(const hydro_gpu_ctx* ctx, hydro_gpu_error* out) {
+  if (!ctx || !out) return HYDRO_GPU_ERR_CONFIG;
+  *out = ctx->last;
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_set_stream(hydro_gpu_ctx* ctx, void* s) {
+  if (!ctx) return HYDRO_GPU_ERR_CONFIG;
+  ctx->stream = s ? (cudaStream_t)s : ctx->own_stream;
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_upload(hydro_gpu_ctx* c, const double* const planes[4], size_t row_stride) {
+  if (!c || !planes) return HYDRO_GPU_ERR_CONFIG;
+  if (row_stride < (size_t)c->cfg.ny + 4)
+    return set_err(c, HYDRO_GPU_ERR_CONFIG, "row stride %zu below ny+4", row_stride);
+  DeviceGuard g(c->device);
+  for (int v = 0; v < 4; ++v) {
+    if (!planes[v]) return set_err(c, HYDRO_GPU_ERR_CONFIG, "null plane %d", v);
+    CUDA_TRY(c, cudaMemcpy2DAsync(c->A + cell_index(c->pitch, v, -1, -1), 4 * c->pitch * 8,
+                                  planes[v], row_stride * 8, (size_t)(c->cfg.ny + 4) * 8,
+                                  (size_t)(c->cfg.nx + 4), cudaMemcpyHostToDevice, c->stream));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_download(hydro_gpu_ctx* c, double* const planes[4], size_t row_stride) {
+  if (!c || !planes) return HYDRO_GPU_ERR_CONFIG;
+  if (row_stride < (size_t)c->cfg.ny + 4)
+    return set_err(c, HYDRO_GPU_ERR_CONFIG, "row stride %zu below ny+4", row_stride);
+  DeviceGuard g(c->device);
+  for (int v = 0; v < 4; ++v) {
+    if (!planes[v]) return set_err(c, HYDRO_GPU_ERR_CONFIG, "null plane %d", v);
+    CUDA_TRY(c, cudaMemcpy2DAsync(planes[v], row_stride * 8,
+                                  c->A + cell_index(c->pitch, v, -1, -1), 4 * c->pitch * 8,
+                                  (size_t)(c->cfg.ny + 4) * 8, (size_t)(c->cfg.nx + 4),
+                                  cudaMemcpyDeviceToHost, c->stream));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_init_case(hydro_gpu_ctx* c, int case_id, uint64_t seed) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  if (case_id < 0 || case_id > 5) return set_err(c, HYDRO_GPU_ERR_CONFIG, "unknown case %d", case_id);
+  DeviceGuard g(c->device);
+  CUDA_TRY(c, cudaMemsetAsync(c->A, 0, c->count * sizeof(double), c->stream));
+  hb::InitArgs a{};
+  a.u = c->A;
+  a.pitch = c->pitch;
+  a.nx = c->cfg.nx;
+  a.ny = c->cfg.ny;
+  a.global_nx = c->cfg.global_nx;
+  a.row0 = c->cfg.row0;
+  a.case_id = case_id;
+  a.gamma = c->cfg.gamma;
+  a.dx = c->cfg.dx;
+  a.dy = c->cfg.dy;
+  a.seed = seed;
+  hb::launch_init(a, c->stream);
+  CUDA_TRY(c, cudaGetLastError());
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_run_async(hydro_gpu_ctx* c, int steps) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  if (steps <= 0) return HYDRO_GPU_OK;
+  DeviceGuard g(c->device);
+  int rc = reset_slots(c);
+  if (rc) return rc;
+  enqueue_prologue(c, 1, 0, 0);
+  for (int s = 0; s < steps; ++s) {
+    enqueue_x(c, s, 0, 0.0);
+    enqueue_y(c, s, 0, 0.0, s + 1 < steps);
+  }
+  enqueue_finish(c);
+  CUDA_TRY(c, cudaGetLastError());
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_sync(hydro_gpu_ctx* c) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  return finish_status(c, true);
+}
+
+int hydro_gpu_run(hydro_gpu_ctx* c, int steps, double* last_dt) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  if (steps < 0) return set_err(c, HYDRO_GPU_ERR_CONFIG, "negative step count");
+  if (steps == 0) return HYDRO_GPU_OK;
+  DeviceGuard g(c->device);
+  int rc = hydro_gpu_run_async(c, steps);
+  if (rc) return rc;
+  rc = finish_status(c, true);
+  if (rc == HYDRO_GPU_OK && last_dt) {
+    unsigned long long bits = 0;
+    CUDA_TRY(c, cudaMemcpy(&bits, c->slots + ((steps - 1) & 1), sizeof bits,
+                           cudaMemcpyDeviceToHost));
+    *last_dt = c->cfg.cfl * as_double(bits);  // dt = model.cfl * limit (:241)
+  }
+  return rc;
+}
+
+int hydro_gpu_advance(hydro_gpu_ctx* c, double dt) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  int rc = reset_slots(c);
+  if (rc) return rc;
+  enqueue_prologue(c, 1, 0, -1);
+  enqueue_x(c, 0, 1, dt);
+  enqueue_y(c, 0, 1, dt, 0);
+  enqueue_finish(c);
+  return finish_status(c, false);
+}
+
+int hydro_gpu_compute_dt(hydro_gpu_ctx* c, double* dt) {
+  if (!c || !dt) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  int rc = reset_slots(c);
+  if (rc) return rc;
+  enqueue_prologue(c, 0, 0, 0);
+  rc = finish_status(c, false);
+  if (rc) return rc;
+  unsigned long long bits = 0;
+  CUDA_TRY(c, cudaMemcpy(&bits, c->slots, sizeof bits, cudaMemcpyDeviceToHost));
+  *dt = c->cfg.cfl * as_double(bits);
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_run_until(hydro_gpu_ctx* c, double t_end, int* steps_out) {
+  if (!c || !steps_out) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  *steps_out = 0;
+  double t = 0.0;
+  int steps = 0;
+  int rc = reset_slots(c);
+  if (rc) return rc;
+  bool started = false;
+  while (t < t_end) {  // schedulers.cpp:118-138
+    if (!started) {
+      enqueue_prologue(c, 1, 0, 0);
+      started = true;
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    unsigned long long sl[4];
+    CUDA_TRY(c, cudaMemcpy(sl, c->slots, sizeof sl, cudaMemcpyDeviceToHost));
+    unsigned long long key = sl[kSlotErr] < sl[kSlotDtErr] ? sl[kSlotErr] : sl[kSlotDtErr];
+    if (key != hb::kNoError) {
+      *steps_out = steps;
+      decode(key, &c->last, true);
+      return HYDRO_GPU_ERR_POSITIVITY;
+    }
+    double dt = c->cfg.cfl * as_double(sl[steps & 1]);
+    if (t + dt > t_end) dt = t_end - t;
+    if (!(dt > 0.0) || t + dt == t) {
+      // the reference applied the boundary before breaking out
+      enqueue_prologue(c, 1, 1, -1);
+      rc = finish_status(c, true);
+      *steps_out = steps;
+      return rc;
+    }
+    enqueue_x(c, steps, 1, dt);
+    enqueue_y(c, steps, 1, dt, 1);
+    t += dt;
+    ++steps;
+  }
+  if (steps > 0) enqueue_finish(c);
+  rc = finish_status(c, true);
+  *steps_out = steps;
+  return rc;
+}
+
+// ---- slab phases -----------------------------------------------------------
+
+int hydro_gpu_slab_prologue(hydro_gpu_ctx* c, int step) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  int rc = reset_slots(c);
+  if (rc) return rc;
+  enqueue_prologue(c, 1, 0, step);
+  CUDA_TRY(c, cudaGetLastError());
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_limit_slot(hydro_gpu_ctx* c, int step, double** p) {
+  if (!c || !p) return HYDRO_GPU_ERR_CONFIG;
+  *p = reinterpret_cast<double*>(c->slots + (step & 1));
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_error_slot(hydro_gpu_ctx* c, uint64_t** p) {
+  if (!c || !p) return HYDRO_GPU_ERR_CONFIG;
+  *p = reinterpret_cast<uint64_t*>(c->slots + kSlotErr);
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_halo(hydro_gpu_ctx* c, double** send_lo, double** send_hi, double** recv_lo,
+                   double** recv_hi, size_t* count) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  const int nx = c->cfg.nx;
+  const size_t rowblk = 4 * c->pitch;
+  if (send_lo) *send_lo = c->A + (size_t)(1 + 1) * rowblk;       // rows 1..2
+  if (send_hi) *send_hi = c->A + (size_t)(nx - 1 + 1) * rowblk;  // rows nx-1..nx
+  if (recv_lo) *recv_lo = c->A + (size_t)(-1 + 1) * rowblk;      // rows -1..0
+  if (recv_hi) *recv_hi = c->A + (size_t)(nx + 1 + 1) * rowblk;  // rows nx+1..nx+2
+  if (count) *count = 2 * rowblk;
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_slab_sweep_x(hydro_gpu_ctx* c, int step) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  enqueue_x(c, step, 0, 0.0);
+  CUDA_TRY(c, cudaGetLastError());
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_slab_sweep_y(hydro_gpu_ctx* c, int step) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  enqueue_y(c, step, 0, 0.0, 1);
+  CUDA_TRY(c, cudaGetLastError());
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_slab_finish(hydro_gpu_ctx* c) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  enqueue_finish(c);
+  CUDA_TRY(c, cudaGetLastError());
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_decode_error(hydro_gpu_ctx* c, uint64_t key, hydro_gpu_error* out) {
+  if (!c || !out) return HYDRO_GPU_ERR_CONFIG;
+  if (key == hb::kNoError) {
+    *out = hydro_gpu_error{};
+    return HYDRO_GPU_OK;
+  }
+  decode(key, out, true);
+  c->last = *out;
+  return HYDRO_GPU_ERR_POSITIVITY;
+}
+
+// ---- instrumentation ---------------------------------------------------------
+
+int hydro_gpu_set_timing(hydro_gpu_ctx* c, int on) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  c->timing = on != 0;
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_kernel_times(hydro_gpu_ctx* c, double* ms_x, double* ms_y, double* ms_o,
+                           long long* n_x, long long* n_y, long long* n_o) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  harvest(c);
+  if (ms_x) *ms_x = c->ms[0];
+  if (ms_y) *ms_y = c->ms[1];
+  if (ms_o) *ms_o = c->ms[2];
+  if (n_x) *n_x = c->n[0];
+  if (n_y) *n_y = c->n[1];
+  if (n_o) *n_o = c->n[2];
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_reset_counters(hydro_gpu_ctx* c) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->pending.clear();
+  c->ev_next = 0;
+  for (int k = 0; k < 3; ++k) {
+    c->ms[k] = 0;
+    c->n[k] = 0;
+  }
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_tune(hydro_gpu_ctx* c, int seg_x, int seg_y, int block) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  if (seg_x < 0 || seg_y < 0 || (block != 0 && (block % 32 || block > 128)))
+    return set_err(c, HYDRO_GPU_ERR_CONFIG, "bad launch geometry");
+  c->seg_x = seg_x;
+  c->seg_y = seg_y;
+  c->block = block ? block : 128;
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_state(hydro_gpu_ctx* c, double** p, size_t* pitch) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  if (p) *p = c->A;
+  if (pitch) *pitch = c->pitch;
+  return HYDRO_GPU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+// hydro_kernels.cuh -- device-side state layout and kernel parameter blocks.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include "hydro_physics.cuh"
+
+namespace hb {
+
+// HBM layout ("row-interleaved planes"): for each grid row i in [-1, nx+2]
+// the four variable rows rho, mom_x, mom_y, ener are stored back to back,
+// each `pitch` doubles long; column j in [-1, ny+2] sits at offset j + kColOff,
+// so interior column 1 starts on a 32-byte sector.  Two consecutive grid rows
+// (all four variables) are therefore one contiguous block of 8*pitch
+// doubles -- a slab halo is a single contiguous send/recv.
+constexpr int kColOff = 3;
+
+__host__ __device__ __forceinline__ size_t cell_index(size_t pitch, int v, int i, int j) {
+  return ((size_t)(i + 1) * 4 + (size_t)v) * pitch + (size_t)(j + kColOff);
+}
+
+inline size_t pitch_for(int ny) {
+  const size_t need = (size_t)ny + 6;  // offsets 0..ny+5
+  return (need + 15) / 16 * 16;        // 128-byte rows
+}
+
+struct SweepArgs {
+  const double* __restrict__ src;
+  double* __restrict__ dst;
+  size_t pitch;
+  int nx, ny;                 // local interior extent
+  int seg;                    // strip segment length per thread
+  double dx;                  // spacing along the sweep
+  double spacing;             // min(dx, dy) for the dt limit
+  double gamma, cfl;
+  int bc;                     // 0 reflect, 1 transmit
+  int wall_lo, wall_hi;       // physical walls on the i sides of this slab
+  int row0;                   // global row of local row 1, minus 1
+  unsigned long long* limit_in;   // dt limit consumed by this step
+  unsigned long long* limit_out;  // dt limit produced for the next step
+  unsigned long long* err;        // latched error key
+  unsigned long long* dt_err;     // dt failure for the next step
+  int step;
+  int explicit_dt;            // 1: use dt_value instead of cfl*limit_in
+  double dt_value;
+  int want_limit;             // row sweep: produce limit_out
+};
+
+struct PrologueArgs {
+  double* u;
+  size_t pitch;
+  int nx, ny;
+  double spacing, gamma;
+  int bc, wall_lo, wall_hi, row0;
+  int want_limit, full_bc;
+  unsigned long long* limit_out;
+  unsigned long long* err;
+  unsigned long long* dt_err;
+  unsigned long long* reset;   // slot reset to +inf bits (may be null)
+  int step;
+};
+
+struct FinishArgs {
+  const double* post_x;       // column-sweep output of the last step
+  double* u;                  // final state
+  size_t pitch;
+  int nx, ny, bc, wall_lo, wall_hi;
+};
+
+struct InitArgs {
+  double* u;
+  size_t pitch;
+  int nx, ny, global_nx, row0;
+  int case_id;
+  double gamma, dx, dy;
+  unsigned long long seed;
+};
+
+void launch_sweep_x(const SweepArgs& a, int block, cudaStream_t s);
+void launch_sweep_y(const SweepArgs& a, int block, cudaStream_t s);
+void launch_prologue(const PrologueArgs& a, cudaStream_t s);
+void launch_finish(const FinishArgs& a, cudaStream_t s);
+void launch_init(const InitArgs& a, cudaStream_t s);
+
+}  // namespace hb

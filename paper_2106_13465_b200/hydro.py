@@ -1,0 +1,352 @@
+"""Host-side mirror of the reference hydro2d interface for the GPU path.
+
+Names, argument meaning and error behaviour follow the reference (paths
+relative to /root/reference/):
+
+===========================================  =================================
+reference                                    here
+===========================================  =================================
+``GasModel`` (include/hydro/types.hpp:38-41)  :class:`GasModel`
+``Grid2D`` (include/hydro/grid.hpp:26-64)     :class:`Grid2D` (numpy planes)
+``make_case`` (src/bench.cpp:24-37)           :func:`make_case` (+ BASELINE cases)
+``run_sequential`` (schedulers.hpp:24)        :func:`run_gpu`
+``advance_sequential`` (schedulers.hpp:21)    :func:`advance_gpu`
+``run_until`` (schedulers.hpp:28)             :func:`run_until_gpu`
+``compute_dt`` (euler_kernel.hpp:75)          :func:`compute_dt_gpu`
+``grid_checksum().digest`` (audit.hpp:34)     :func:`grid_digest`
+``hydro::Error`` + categories (errors.hpp)    :class:`HydroError` & subclasses
+===========================================  =================================
+
+All stepping runs in libhydro_b200.so on the GPU; nothing here computes
+physics.  Errors carry the reference's category and message text, e.g.
+``step 3: column sweep strip 17: rho non-positive at strip cell -2``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from enum import IntEnum
+
+import numpy as np
+
+from . import _lib as L
+
+
+class ErrorCategory(IntEnum):
+    """hydro::ErrorCategory (errors.hpp:10-18), numbered +1; CUDA = device failure."""
+    CONFIG = 1
+    POSITIVITY = 2
+    PROTOCOL = 3
+    TASK_GRAPH = 4
+    EQUIVALENCE = 5
+    IO = 6
+    VALIDATION = 7
+    CUDA = 8
+
+
+_CATEGORY_NAME = {1: "config", 2: "positivity", 3: "protocol", 4: "task-graph",
+                  5: "equivalence", 6: "io", 7: "validation", 8: "cuda"}
+
+
+class HydroError(RuntimeError):
+    """hydro::Error: a message plus an ErrorCategory (errors.hpp:20-29)."""
+
+    def __init__(self, category: int, message: str, info: dict | None = None):
+        super().__init__(message)
+        self.category = ErrorCategory(category)
+        self.info = info or {}
+
+    def cli_line(self) -> str:
+        """The CLI's one-line rendering (tools/hydrobench.cpp:153-159)."""
+        return f"error: {_CATEGORY_NAME[int(self.category)]}: {self}"
+
+
+class ConfigError(HydroError):
+    def __init__(self, message: str):
+        super().__init__(ErrorCategory.CONFIG, message)
+
+
+class PositivityError(HydroError):
+    """Carries the non-positive field like PositivityError (errors.hpp:40-49)."""
+
+    @property
+    def field(self) -> str:
+        return ("rho", "pres", "internal energy")[self.info.get("field", 0)]
+
+
+class DeviceError(HydroError):
+    pass
+
+
+def _raise_for(status: int, info: L.ErrorInfo | None = None, message: str | None = None):
+    if status == 0:
+        return
+    msg = message if message is not None else (info.message.decode() if info else "")
+    details = {}
+    if info is not None:
+        details = {k: getattr(info, k) for k in ("step", "phase", "strip", "loop", "cell", "field")}
+    if status == ErrorCategory.POSITIVITY:
+        raise PositivityError(status, msg, details)
+    if status == ErrorCategory.CONFIG:
+        raise ConfigError(msg or "invalid configuration")
+    if status == ErrorCategory.CUDA:
+        raise DeviceError(status, msg or "CUDA failure")
+    raise HydroError(status, msg, details)
+
+
+@dataclass(frozen=True)
+class GasModel:
+    gamma: float = 1.4
+    cfl: float = 0.8
+
+
+BC = {"reflect": 0, "transmit": 1}
+CASES = {"uniform": 0, "blast": 1, "sod": 2, "corner_blast": 3, "sod_x": 4, "random": 5}
+RHO, MOM_X, MOM_Y, ENER = 0, 1, 2, 3
+
+
+class Grid2D:
+    """Four (nx+4) x (ny+4) fp64 planes, row-major, j fastest (grid.hpp:15-19)."""
+
+    def __init__(self, nx: int, ny: int, dx: float, dy: float, planes: np.ndarray | None = None):
+        if nx < 4 or ny < 4:
+            raise ConfigError(f"grid interior must be at least 4x4, got {nx}x{ny}")
+        if not (dx > 0.0) or not (dy > 0.0):
+            raise ConfigError("cell sizes must be positive")
+        self.nx, self.ny, self.dx, self.dy = nx, ny, dx, dy
+        if planes is None:
+            planes = np.zeros((4, nx + 4, ny + 4))
+        if planes.shape != (4, nx + 4, ny + 4) or planes.dtype != np.float64:
+            raise ConfigError("planes must be float64 of shape (4, nx+4, ny+4)")
+        self.planes = np.ascontiguousarray(planes)
+
+    def at(self, var: int, i: int, j: int) -> float:
+        return float(self.planes[var, i + 1, j + 1])
+
+    def cell(self, i: int, j: int) -> tuple:
+        return tuple(float(self.planes[v, i + 1, j + 1]) for v in range(4))
+
+    def interior(self) -> np.ndarray:
+        return self.planes[:, 2:self.nx + 2, 2:self.ny + 2]
+
+    def copy(self) -> "Grid2D":
+        return Grid2D(self.nx, self.ny, self.dx, self.dy, self.planes.copy())
+
+
+def make_case(case: str, nx: int, ny: int, model: GasModel = GasModel(), seed: int = 0) -> Grid2D:
+    """Initial conditions: the reference's uniform/blast/sod (cases.cpp:11-69)
+    plus the BASELINE configs' corner_blast, sod_x and random."""
+    if case not in CASES:
+        raise ConfigError(f"unknown case '{case}' (expected one of {', '.join(CASES)})")
+    if case == "sod":
+        nx = 4
+    planes = np.zeros((4, nx + 4, ny + 4))
+    dx, dy = C.c_double(), C.c_double()
+    rc = L.lib().hydro_init_case_host(CASES[case], nx, ny, model.gamma, seed,
+                                      L.planes_of(planes), ny + 4, C.byref(dx), C.byref(dy))
+    if rc:
+        raise ConfigError(f"cannot build case '{case}' on a {nx}x{ny} grid")
+    return Grid2D(nx, ny, dx.value, dy.value, planes)
+
+
+def grid_digest(grid: Grid2D) -> int:
+    """FNV-1a over the interior bytes (audit.cpp:53-76)."""
+    return int(L.lib().hydro_grid_digest(L.planes_of(grid.planes), grid.ny + 4, grid.nx, grid.ny))
+
+
+class GpuGrid:
+    """One device-resident grid (or row slab): a hydro_gpu_ctx."""
+
+    def __init__(self, nx: int, ny: int, dx: float, dy: float, model: GasModel = GasModel(),
+                 bc: str = "reflect", device: int = -1, row0: int = 0, global_nx: int | None = None,
+                 wall_lo: bool = True, wall_hi: bool = True):
+        if bc not in BC:
+            raise ConfigError(f"unknown boundary '{bc}' (expected reflect or transmit)")
+        self.nx, self.ny, self.dx, self.dy = nx, ny, dx, dy
+        self.model, self.bc = model, bc
+        self.row0 = row0
+        self.global_nx = global_nx if global_nx is not None else nx
+        cfg = L.Cfg(nx, ny, dx, dy, model.gamma, model.cfl, BC[bc], 0, device, row0,
+                    self.global_nx, int(wall_lo), int(wall_hi))
+        self._lib = L.lib()
+        self._ctx = C.c_void_p()
+        rc = self._lib.hydro_gpu_create(C.byref(cfg), C.byref(self._ctx))
+        if rc:
+            _raise_for(rc, message=f"hydro_gpu_create failed ({self._lib.hydro_gpu_status_string(rc).decode()}) "
+                                   f"for a {nx}x{ny} grid")
+
+    # -- lifetime ---------------------------------------------------------
+    def close(self):
+        if self._ctx:
+            self._lib.hydro_gpu_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._ctx
+
+    def _check(self, rc: int):
+        if rc:
+            info = L.ErrorInfo()
+            self._lib.hydro_gpu_last_error(self._ctx, C.byref(info))
+            _raise_for(rc, info)
+
+    # -- transfer ---------------------------------------------------------
+    def upload(self, planes: np.ndarray):
+        self._check(self._lib.hydro_gpu_upload(self._ctx, L.planes_of(planes), planes.shape[2]))
+
+    def download(self, planes: np.ndarray):
+        self._check(self._lib.hydro_gpu_download(self._ctx, L.planes_of(planes), planes.shape[2]))
+
+    def upload_ptr(self, plane_ptrs, row_stride: int):
+        arr = L._planes(*[C.cast(C.c_void_p(p), L._dp) for p in plane_ptrs])
+        self._check(self._lib.hydro_gpu_upload(self._ctx, arr, row_stride))
+
+    def download_ptr(self, plane_ptrs, row_stride: int):
+        arr = L._planes(*[C.cast(C.c_void_p(p), L._dp) for p in plane_ptrs])
+        self._check(self._lib.hydro_gpu_download(self._ctx, arr, row_stride))
+
+    def init_case(self, case: str, seed: int = 0):
+        self._check(self._lib.hydro_gpu_init_case(self._ctx, CASES[case], seed))
+
+    # -- stepping ---------------------------------------------------------
+    def run(self, steps: int) -> float:
+        last = C.c_double(0.0)
+        self._check(self._lib.hydro_gpu_run(self._ctx, steps, C.byref(last)))
+        return last.value
+
+    def advance(self, dt: float):
+        self._check(self._lib.hydro_gpu_advance(self._ctx, dt))
+
+    def run_until(self, t_end: float) -> int:
+        steps = C.c_int(0)
+        self._check(self._lib.hydro_gpu_run_until(self._ctx, t_end, C.byref(steps)))
+        return steps.value
+
+    def compute_dt(self) -> float:
+        dt = C.c_double(0.0)
+        self._check(self._lib.hydro_gpu_compute_dt(self._ctx, C.byref(dt)))
+        return dt.value
+
+    def set_stream(self, stream_ptr: int | None):
+        self._check(self._lib.hydro_gpu_set_stream(self._ctx, C.c_void_p(stream_ptr or 0)))
+
+    def run_async(self, steps: int):
+        self._check(self._lib.hydro_gpu_run_async(self._ctx, steps))
+
+    def sync(self):
+        self._check(self._lib.hydro_gpu_sync(self._ctx))
+
+    # -- slab phases --------------------------------------------------------
+    def slab_prologue(self, step: int = 0):
+        self._check(self._lib.hydro_gpu_slab_prologue(self._ctx, step))
+
+    def slab_sweep_x(self, step: int):
+        self._check(self._lib.hydro_gpu_slab_sweep_x(self._ctx, step))
+
+    def slab_sweep_y(self, step: int):
+        self._check(self._lib.hydro_gpu_slab_sweep_y(self._ctx, step))
+
+    def slab_finish(self):
+        self._check(self._lib.hydro_gpu_slab_finish(self._ctx))
+
+    def limit_slot(self, step: int) -> int:
+        p = L._dp()
+        self._check(self._lib.hydro_gpu_limit_slot(self._ctx, step, C.byref(p)))
+        return C.cast(p, C.c_void_p).value
+
+    def error_slot(self) -> int:
+        p = C.POINTER(C.c_uint64)()
+        self._check(self._lib.hydro_gpu_error_slot(self._ctx, C.byref(p)))
+        return C.cast(p, C.c_void_p).value
+
+    def halo(self) -> dict:
+        ptrs = [L._dp() for _ in range(4)]
+        count = C.c_size_t()
+        self._check(self._lib.hydro_gpu_halo(self._ctx, *[C.byref(p) for p in ptrs], C.byref(count)))
+        names = ("send_lo", "send_hi", "recv_lo", "recv_hi")
+        out = {n: C.cast(p, C.c_void_p).value for n, p in zip(names, ptrs)}
+        out["count"] = count.value
+        return out
+
+    def raise_error_key(self, key: int):
+        info = L.ErrorInfo()
+        rc = self._lib.hydro_gpu_decode_error(self._ctx, key, C.byref(info))
+        _raise_for(rc, info)
+
+    # -- instrumentation ----------------------------------------------------
+    def set_timing(self, on: bool):
+        self._check(self._lib.hydro_gpu_set_timing(self._ctx, int(on)))
+
+    def kernel_times(self) -> dict:
+        ms = [C.c_double() for _ in range(3)]
+        n = [C.c_longlong() for _ in range(3)]
+        self._check(self._lib.hydro_gpu_kernel_times(self._ctx, *[C.byref(x) for x in ms],
+                                                     *[C.byref(x) for x in n]))
+        return {"ms_x": ms[0].value, "ms_y": ms[1].value, "ms_other": ms[2].value,
+                "n_x": n[0].value, "n_y": n[1].value, "n_other": n[2].value}
+
+    def reset_counters(self):
+        self._check(self._lib.hydro_gpu_reset_counters(self._ctx))
+
+    def tune(self, seg_x: int = 0, seg_y: int = 0, block: int = 0):
+        self._check(self._lib.hydro_gpu_tune(self._ctx, seg_x, seg_y, block))
+
+    def state(self) -> tuple[int, int]:
+        p = L._dp()
+        pitch = C.c_size_t()
+        self._check(self._lib.hydro_gpu_state(self._ctx, C.byref(p), C.byref(pitch)))
+        return C.cast(p, C.c_void_p).value, pitch.value
+
+
+def _context_for(grid: Grid2D, model: GasModel, bc: str) -> GpuGrid:
+    g = GpuGrid(grid.nx, grid.ny, grid.dx, grid.dy, model, bc)
+    g.upload(grid.planes)
+    return g
+
+
+def run_gpu(grid: Grid2D, model: GasModel = GasModel(), steps: int = 1, bc: str = "reflect") -> float:
+    """run_sequential(grid, model, steps) on the GPU, in place; returns the last dt."""
+    with _context_for(grid, model, bc) as g:
+        try:
+            last = g.run(steps)
+        finally:
+            g.download(grid.planes)
+    return last
+
+
+def advance_gpu(grid: Grid2D, model: GasModel, dt: float, bc: str = "reflect") -> None:
+    """advance_sequential(grid, model, dt) on the GPU, in place."""
+    with _context_for(grid, model, bc) as g:
+        try:
+            g.advance(dt)
+        finally:
+            g.download(grid.planes)
+
+
+def run_until_gpu(grid: Grid2D, model: GasModel, t_end: float, bc: str = "reflect") -> int:
+    """run_until(grid, model, t_end) on the GPU, in place; returns steps taken."""
+    with _context_for(grid, model, bc) as g:
+        try:
+            steps = g.run_until(t_end)
+        finally:
+            g.download(grid.planes)
+    return steps
+
+
+def compute_dt_gpu(grid: Grid2D, model: GasModel = GasModel()) -> float:
+    """compute_dt(grid, model): cfl * min cell_dt_limit over the interior."""
+    with _context_for(grid, model, "reflect") as g:
+        return g.compute_dt()

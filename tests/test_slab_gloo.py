@@ -1,0 +1,128 @@
+"""The multi-GPU slab driver (paper_2106_13465_b200/slab.py) over a real
+2-rank torch.distributed gloo group on CPU.
+
+The per-slab physics is supplied by the oracle (test infrastructure), so what
+is under test is the driver itself: row split, which rows are exchanged with
+which neighbour, the order of halo swap / dt min-allreduce / sweeps, and the
+first-error gather.  The gathered result must be bitwise the single-domain
+reference run.
+"""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+from paper_2106_13465_b200 import slab as S
+
+NX, NY, STEPS = 41, 26, 14
+
+
+class OracleSlab:
+    """Slab backend computing with the CPU oracle on numpy planes."""
+
+    def __init__(self, geo, planes, dx, dy, bc, cfl=0.8):
+        self.geo, self.bc, self.cfl = geo, bc, cfl
+        self.g = O.Grid(geo.nx, NY, dx, dy, planes)
+        self.lims = [torch.zeros(1, dtype=torch.float64) for _ in range(2)]
+        self._recv = None
+        self.err = torch.full((1,), -1, dtype=torch.int64)
+        self.walls = (O.WALL_XLO if geo.wall_lo else 0) | (O.WALL_XHI if geo.wall_hi else 0)
+
+    def prologue(self, step):
+        O.apply_boundary(self.g, self.bc, self.walls)
+        self.lims[step & 1][0] = O.compute_limit(self.g)
+
+    def limit(self, step):
+        return self.lims[step & 1]
+
+    def halo_send(self):
+        n = self.geo.nx
+        u = self.g.u
+        return (torch.from_numpy(np.ascontiguousarray(u[:, 2:4, :])).reshape(-1),
+                torch.from_numpy(np.ascontiguousarray(u[:, n:n + 2, :])).reshape(-1))
+
+    def halo_recv(self):
+        size = 4 * 2 * (NY + 4)
+        self._recv = (torch.zeros(size, dtype=torch.float64), torch.zeros(size, dtype=torch.float64))
+        return self._recv
+
+    def halo_done(self):
+        n = self.geo.nx
+        if not self.geo.wall_lo:
+            self.g.u[:, 0:2, :] = self._recv[0].numpy().reshape(4, 2, NY + 4)
+        if not self.geo.wall_hi:
+            self.g.u[:, n + 2:n + 4, :] = self._recv[1].numpy().reshape(4, 2, NY + 4)
+
+    def sweep_x(self, step):
+        dt = self.cfl * float(self.lims[step & 1][0])
+        O.sweep_axis(self.g, 0, dt)
+        O.apply_boundary(self.g, self.bc, O.WALL_Y)
+
+    def sweep_y(self, step):
+        dt = self.cfl * float(self.lims[step & 1][0])
+        O.sweep_axis(self.g, 1, dt)
+        O.apply_boundary(self.g, self.bc, self.walls)
+        self.lims[(step + 1) & 1][0] = O.compute_limit(self.g)
+
+    def finish(self):
+        pass
+
+    def error_key(self):
+        return self.err
+
+    def raise_error(self, key):
+        raise RuntimeError(f"error key {key:x}")
+
+
+def _worker(rank, world, port, case, bc, outdir):
+    import torch.distributed as dist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                           world_size=world)
+    full = O.make_case(case, NX, NY, seed=6)
+    geo = S.SlabGeometry(NX, NY, rank, world)
+    planes = S.slab_planes(full.u, NX, world, rank)
+    sl = OracleSlab(geo, planes, full.dx, full.dy, bc)
+    S.run_slab(sl, S.TorchComm(), STEPS)
+    np.save(os.path.join(outdir, f"slab{rank}.npy"), sl.g.u)
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world,case,bc", [(2, "corner_blast", "reflect"), (2, "random", "transmit"),
+                                           (3, "sod_x", "transmit")])
+def test_slab_driver_over_gloo_matches_single_domain(world, case, bc):
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(world, _free_port(), case, bc, d), nprocs=world, join=True)
+        parts = [np.load(os.path.join(d, f"slab{r}.npy")) for r in range(world)]
+    got = S.gather_planes(parts, NX, NY)
+    ref = O.make_case(case, NX, NY, seed=6)
+    O.run_sequential(ref, STEPS, bc)
+    assert np.array_equal(got[:, 2:NX + 2, 2:NY + 2], ref.u[:, 2:NX + 2, 2:NY + 2])
+
+
+@pytest.mark.parametrize("nx,parts", [(10, 3), (41, 2), (16384 * 8, 8), (7, 7)])
+def test_split_rows_is_split_range(nx, parts):
+    rows = [S.split_rows(nx, parts, p) for p in range(parts)]
+    assert sum(n for _, n in rows) == nx
+    assert rows[0][0] == 0
+    for (r0, n), (r1, _) in zip(rows, rows[1:]):
+        assert r1 == r0 + n
+    assert max(n for _, n in rows) - min(n for _, n in rows) <= 1
+    assert rows[0][1] >= rows[-1][1]  # extra rows go to the first slabs
+
+
+def test_gather_of_cut_slabs_is_identity():
+    full = O.make_case("random", NX, NY, seed=2).u
+    for world in (1, 2, 5):
+        parts = [S.slab_planes(full, NX, world, r) for r in range(world)]
+        assert np.array_equal(S.gather_planes(parts, NX, NY), full)
