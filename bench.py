@@ -178,7 +178,8 @@ def main():
     model = P.GasModel()
     global_nx = NX * world
     dx, dy = 1.0 / global_nx, 1.0 / NY
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # a real stream: library kernels, NCCL and events share it
+    torch.cuda.set_stream(stream)
 
     geo = S.SlabGeometry(global_nx, NY, rank, world)
     if world == 1:

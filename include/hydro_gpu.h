@@ -128,9 +128,11 @@ int hydro_gpu_run_until(hydro_gpu_ctx* ctx, double t_end, int* steps);
 int hydro_gpu_compute_dt(hydro_gpu_ctx* ctx, double* dt);
 
 /* ---- asynchronous, device-resident interface --------------------------- */
-/* Stream all work of this context is issued on (a cudaStream_t); NULL =
- * the context's own stream. */
+/* Stream all work of this context is issued on (a cudaStream_t; NULL is the
+ * CUDA default stream, as everywhere in CUDA).  A new context uses its own
+ * non-blocking stream; hydro_gpu_use_own_stream restores it. */
 int hydro_gpu_set_stream(hydro_gpu_ctx* ctx, void* cuda_stream);
+int hydro_gpu_use_own_stream(hydro_gpu_ctx* ctx);
 /* Enqueues `steps` steps without synchronising; errors are latched on the
  * device and reported by the next hydro_gpu_sync. */
 int hydro_gpu_run_async(hydro_gpu_ctx* ctx, int steps);

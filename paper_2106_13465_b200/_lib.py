@@ -66,6 +66,7 @@ def lib() -> C.CDLL:
         "hydro_gpu_run_until": ([_ctx, d, P(i)], i),
         "hydro_gpu_compute_dt": ([_ctx, _dp], i),
         "hydro_gpu_set_stream": ([_ctx, C.c_void_p], i),
+        "hydro_gpu_use_own_stream": ([_ctx], i),
         "hydro_gpu_run_async": ([_ctx, i], i),
         "hydro_gpu_sync": ([_ctx], i),
         "hydro_gpu_slab_prologue": ([_ctx, i], i),

@@ -376,9 +376,16 @@ int hydro_gpu_last_error(const hydro_gpu_ctx* ctx, hydro_gpu_error* out) {
   return HYDRO_GPU_OK;
 }
 
+int hydro_gpu_use_own_stream(hydro_gpu_ctx* ctx) {
+  if (!ctx) return HYDRO_GPU_ERR_CONFIG;
+  ctx->stream = ctx->own_stream;
+  return HYDRO_GPU_OK;
+}
+
 int hydro_gpu_set_stream(hydro_gpu_ctx* ctx, void* s) {
   if (!ctx) return HYDRO_GPU_ERR_CONFIG;
-  ctx->stream = s ? (cudaStream_t)s : ctx->own_stream;
+  // CUDA convention: a null handle is the (legacy) default stream.
+  ctx->stream = (cudaStream_t)s;
   return HYDRO_GPU_OK;
 }
 

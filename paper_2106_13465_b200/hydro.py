@@ -241,7 +241,12 @@ class GpuGrid:
         return dt.value
 
     def set_stream(self, stream_ptr: int | None):
-        self._check(self._lib.hydro_gpu_set_stream(self._ctx, C.c_void_p(stream_ptr or 0)))
+        """Issue all work on this cudaStream_t (0 = the CUDA default stream);
+        None restores the context's own stream."""
+        if stream_ptr is None:
+            self._check(self._lib.hydro_gpu_use_own_stream(self._ctx))
+        else:
+            self._check(self._lib.hydro_gpu_set_stream(self._ctx, C.c_void_p(stream_ptr)))
 
     def run_async(self, steps: int):
         self._check(self._lib.hydro_gpu_run_async(self._ctx, steps))
