@@ -83,6 +83,7 @@ def lib() -> C.CDLL:
         "hydro_gpu_reset_counters": ([_ctx], i),
         "hydro_gpu_tune": ([_ctx, i, i, i], i),
         "hydro_gpu_state": ([_ctx, P(_dp), P(sz)], i),
+        "hydro_gpu_math_selftest": ([i, _dp, _dp, _dp, _dp, P(i), sz], i),
         "hydro_grid_digest": ([_planes, sz, i, i], u64),
         "hydro_init_case_host": ([i, i, i, d, u64, _planes, sz, _dp, _dp], i),
     }

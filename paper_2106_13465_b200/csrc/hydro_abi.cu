@@ -36,6 +36,8 @@ struct hydro_gpu_ctx {
   unsigned long long* slots = nullptr;  // [0],[1] dt limits, [2] error, [3] dt error
   hydro_gpu_error last{};
   int seg_x = 0, seg_y = 0, block = 128;
+  hb::Geometry geo{};
+  hb::TmaMaps maps{};
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
   struct Pending { cudaEvent_t a, b; int kind; };
@@ -183,7 +185,7 @@ void enqueue_x(hydro_gpu_ctx* c, int step, int explicit_dt, double dt) {
   a.dt_value = dt;
   cudaEvent_t e0{};
   ev_begin(c, &e0);
-  hb::launch_sweep_x(a, c->block, c->stream);
+  hb::launch_sweep_x(a, c->geo, c->stream);
   ev_end(c, e0, 0);
 }
 
@@ -194,7 +196,7 @@ void enqueue_y(hydro_gpu_ctx* c, int step, int explicit_dt, double dt, int want_
   a.want_limit = want_limit;
   cudaEvent_t e0{};
   ev_begin(c, &e0);
-  hb::launch_sweep_y(a, c->block, c->stream);
+  hb::launch_sweep_y(a, c->maps, c->geo, c->stream);
   ev_end(c, e0, 1);
 }
 
@@ -336,7 +338,8 @@ int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out) {
   }
   cudaGetDevice(&ctx->device);
   ctx->pitch = hb::pitch_for(c.ny);
-  ctx->count = (size_t)(c.nx + 4) * 4 * ctx->pitch;
+  // rows -1..nx+2 plus one padding row read by the column sweep's prefetch
+  ctx->count = (size_t)(c.nx + 5) * 4 * ctx->pitch;
   const size_t bytes = ctx->count * sizeof(double);
   if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&ctx->A, bytes) != cudaSuccess || cudaMalloc(&ctx->B, bytes) != cudaSuccess ||
@@ -346,6 +349,12 @@ int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out) {
     return HYDRO_GPU_ERR_CUDA;
   }
   ctx->stream = ctx->own_stream;
+  if (hb::query_geometry(&ctx->geo) != 0 ||
+      !hb::make_tma_maps(&ctx->maps, ctx->A, ctx->B, ctx->pitch, c.nx, c.ny)) {
+    hydro_gpu_destroy(ctx);
+    cudaGetLastError();
+    return HYDRO_GPU_ERR_CUDA;
+  }
   cudaMemsetAsync(ctx->A, 0, bytes, ctx->stream);
   cudaMemsetAsync(ctx->B, 0, bytes, ctx->stream);
   cudaMemsetAsync(ctx->slots, 0xff, 4 * sizeof(unsigned long long), ctx->stream);
@@ -661,12 +670,39 @@ int hydro_gpu_reset_counters(hydro_gpu_ctx* c) {
 
 int hydro_gpu_tune(hydro_gpu_ctx* c, int seg_x, int seg_y, int block) {
   if (!c) return HYDRO_GPU_ERR_CONFIG;
-  if (seg_x < 0 || seg_y < 0 || (block != 0 && (block % 32 || block > 128)))
+  if (seg_x < 0 || seg_y < 0 || (block != 0 && block != 128))
     return set_err(c, HYDRO_GPU_ERR_CONFIG, "bad launch geometry");
   c->seg_x = seg_x;
   c->seg_y = seg_y;
-  c->block = block ? block : 128;
   return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_math_selftest(int op, const double* a, const double* b, double* fast,
+                            double* exact, int* in_range, size_t n) {
+  if (op < 0 || op > 1 || !a || !fast || !exact || !in_range) return HYDRO_GPU_ERR_CONFIG;
+  double *da = nullptr, *db = nullptr, *df = nullptr, *dr = nullptr;
+  int* dk = nullptr;
+  const size_t bytes = n * sizeof(double);
+  int rc = HYDRO_GPU_OK;
+  if (cudaMalloc(&da, bytes) || cudaMalloc(&db, bytes) || cudaMalloc(&df, bytes) ||
+      cudaMalloc(&dr, bytes) || cudaMalloc(&dk, n * sizeof(int))) {
+    rc = HYDRO_GPU_ERR_CUDA;
+  } else {
+    cudaMemcpy(da, a, bytes, cudaMemcpyHostToDevice);
+    cudaMemcpy(db, b ? b : a, bytes, cudaMemcpyHostToDevice);
+    hb::launch_math_selftest(op, da, db, df, dr, dk, n, 0);
+    if (cudaDeviceSynchronize() != cudaSuccess) rc = HYDRO_GPU_ERR_CUDA;
+    cudaMemcpy(fast, df, bytes, cudaMemcpyDeviceToHost);
+    cudaMemcpy(exact, dr, bytes, cudaMemcpyDeviceToHost);
+    cudaMemcpy(in_range, dk, n * sizeof(int), cudaMemcpyDeviceToHost);
+  }
+  cudaFree(da);
+  cudaFree(db);
+  cudaFree(df);
+  cudaFree(dr);
+  cudaFree(dk);
+  cudaGetLastError();
+  return rc;
 }
 
 int hydro_gpu_state(hydro_gpu_ctx* c, double** p, size_t* pitch) {

@@ -13,9 +13,19 @@
 // Every thread owns one strip segment and walks it with a register sliding
 // window: primitive conversion, minmod slopes, Hancock predictor, evolved
 // faces, HLLC flux and the conservative update of the reference's four strip
-// loops (euler_kernel.cpp:111-223) are fused, no per-strip scratch touches
+// loops (euler_kernel.cpp:111-223) are fused; no per-strip scratch touches
 // HBM.  Segments overlap by the 2-cell stencil halo only.
+//
+// Memory paths: in the column sweep a warp's 32 threads are 32 adjacent
+// columns, so every row it reads or writes is one coalesced 256-byte access
+// per variable (loads software-pipelined one cell ahead).  In the row sweep
+// the strips run along the contiguous axis, so tiles of 128 rows x 2 columns
+// x 4 variables are staged with TMA (cp.async.bulk.tensor, one box per
+// variable, mbarrier completion) into shared memory -- a transposed tile from
+// each thread's point of view -- and results leave through the same layout
+// with TMA bulk-tensor stores.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include "hydro_kernels.cuh"
 
@@ -24,10 +34,6 @@ namespace hb {
 namespace {
 
 constexpr unsigned long long kEmptyLimit = ~0ull;  // sentinel above every positive double
-
-__device__ __forceinline__ void record(unsigned long long* err, unsigned long long key) {
-  atomicMin(err, key);
-}
 
 __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
 #pragma unroll
@@ -38,51 +44,96 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
   return v;
 }
 
-// Walks strip cells [ka, kb] (local strip coordinates: cell k holds grid
-// index k-1).  load(k) returns the conserved state of cell k in sweep
-// orientation; sink(k, u, rr) receives the updated cell and 1/rho.
-// kg converts a local strip cell to the global one used in error keys.
-template <class Load, class Sink>
-__device__ __forceinline__ void walk_strip(int ka, int kb, const Load& load, Sink& sink,
-                                           const Gas& g, double dtdx, unsigned long long* err,
+// ---------------------------------------------------------------------------
+// The strip walker.
+
+struct Window {
+  Prim wA, wB;      // primitives of cells c-1, c
+  Cons uA, uB;      // conserved cells c-1, c
+  Face frPrev;      // right face of cell c-1
+  Flux fluxPrev;    // flux through interface c-2 | c-1
+};
+
+struct StepOut {
+  Prim wC;          // primitive of the incoming cell c+1
+  int fC;           // its positivity failure (-1 none)
+  Face fr;          // right face of cell c
+  Flux F;           // flux through interface c-1 | c
+  Cons un;          // cell c-1 after the conservative update
+  int fU;
+  double lim;       // cell_dt_limit of the updated cell (row sweep)
+  int fD;
+};
+
+template <bool WANT_DT, class M>
+__device__ __forceinline__ void step_cell(M& m, const Window& w, const Cons& uC, double half,
+                                          double dtdx, double spacing, const Gas& g,
+                                          StepOut& o) {
+  o.fC = to_prim(m, uC, g, o.wC);
+  Face fl;
+  predict_faces(m, w.wA, w.wB, o.wC, half, g, fl, o.fr);
+  o.F = hllc(m, w.frPrev, fl, g);
+  o.un = w.uA;
+  Recip rn;
+  o.fU = update_cell(m, o.un, w.fluxPrev, o.F, dtdx, rn);
+  if (WANT_DT) o.fD = dt_limit(m, o.un, rn, spacing, g, o.lim);
+}
+
+__device__ __forceinline__ void record(unsigned long long* err, unsigned long long key) {
+  atomicMin(err, key);
+}
+
+// Walks strip cells [ka, kb] (strip coordinates: cell k holds grid index
+// k-1).  src.load(k) returns cell k in sweep orientation (called for
+// k = ka-2 .. kb+2 in order), sink(k, out) receives updated cells ka..kb,
+// src.boundary(c) is called after every iteration (chunk bookkeeping).
+// kg converts a local strip cell to the global index used in error keys.
+template <bool WANT_DT, class Src, class Sink>
+__device__ __forceinline__ void walk_strip(int ka, int kb, Src& src, Sink& sink, const Gas& g,
+                                           double dtdx, double spacing, bool active,
+                                           unsigned long long* err,
                                            unsigned long long key_base, int kg) {
   const double half = 0.5 * dtdx;
-  Recip rr;
-  Prim wA, wB, wC;
-  Cons uA, uB, uC;
-  int f;
-  uA = load(ka - 2);
-  if ((f = to_prim(uA, g, wA, rr)) >= 0)
-    record(err, key_base | ((unsigned long long)(ka - 2 + kg) << 2) | (unsigned)f);
-  uB = load(ka - 1);
-  if ((f = to_prim(uB, g, wB, rr)) >= 0)
-    record(err, key_base | ((unsigned long long)(ka - 1 + kg) << 2) | (unsigned)f);
-  Face frPrev;
-  Flux fluxPrev;
+  Window w;
+  {
+    ExactMath em;
+    w.uA = src.load(ka - 2);
+    int f = to_prim(em, w.uA, g, w.wA);
+    if (active && f >= 0) record(err, key_base | ((unsigned long long)(ka - 2 + kg) << 2) | f);
+    w.uB = src.load(ka - 1);
+    f = to_prim(em, w.uB, g, w.wB);
+    if (active && f >= 0) record(err, key_base | ((unsigned long long)(ka - 1 + kg) << 2) | f);
+    // placeholders for the first two iterations, whose flux/update are
+    // discarded: a physical state keeps them on the fast path
+    w.frPrev.w = w.wA;
+    w.frPrev.rr = em.recip(w.wA.r);
+    w.fluxPrev = {0.0, 0.0, 0.0, 0.0};
+  }
+  src.boundary(ka - 2);  // the first staged chunk is consumed
 #pragma unroll 1
   for (int c = ka - 1; c <= kb + 1; ++c) {
-    uC = load(c + 1);
-    if ((f = to_prim(uC, g, wC, rr)) >= 0)
-      record(err, key_base | ((unsigned long long)(c + 1 + kg) << 2) | (unsigned)f);
-    Face fl, fr;
-    predict_faces(wA, wB, wC, half, g, fl, fr);
-    if (c >= ka) {
-      const Flux F = hllc(frPrev, fl, g);
-      if (c > ka) {
-        Cons u = uA;
-        Recip rn;
-        if ((f = update_cell(u, fluxPrev, F, dtdx, rn)) >= 0)
-          record(err, key_base | (1ull << 20) |
-                          ((unsigned long long)(c - 1 + kg) << 2) | (unsigned)f);
-        sink(c - 1, u, rn);
-      }
-      fluxPrev = F;
+    const Cons uC = src.load(c + 1);
+    StepOut o;
+    FastMath fm;
+    step_cell<WANT_DT>(fm, w, uC, half, dtdx, spacing, g, o);
+    if (!fm.ok) {  // some fast path left its proven range: redo the cell exactly
+      ExactMath em;
+      step_cell<WANT_DT>(em, w, uC, half, dtdx, spacing, g, o);
     }
-    frPrev = fr;
-    wA = wB;
-    wB = wC;
-    uA = uB;
-    uB = uC;
+    if (active && o.fC >= 0)
+      record(err, key_base | ((unsigned long long)(c + 1 + kg) << 2) | o.fC);
+    if (c > ka) {
+      if (active && o.fU >= 0)
+        record(err, key_base | (1ull << 20) | ((unsigned long long)(c - 1 + kg) << 2) | o.fU);
+      sink(c - 1, o);
+    }
+    src.boundary(c);
+    w.wA = w.wB;
+    w.wB = o.wC;
+    w.uA = w.uB;
+    w.uB = uC;
+    w.frPrev = o.fr;
+    w.fluxPrev = o.F;
   }
 }
 
@@ -95,115 +146,294 @@ __device__ __forceinline__ double step_dt(const SweepArgs& a) {
 }
 
 // ---------------------------------------------------------------------------
-// Column sweep: thread = column j, segment of rows.  Loads of one row by a
-// warp are 32 consecutive doubles per variable (coalesced).
+// Column sweep: thread = column j, segment of rows.
+
+struct ColumnSource {
+  const double* __restrict__ p;  // next row to fetch (cell k = row k-1)
+  size_t pitch;
+  Cons next;
+  __device__ __forceinline__ Cons fetch() {
+    const Cons u = {__ldg(p), __ldg(p + pitch), __ldg(p + 2 * pitch), __ldg(p + 3 * pitch)};
+    p += 4 * pitch;
+    return u;
+  }
+  __device__ __forceinline__ void start() { next = fetch(); }
+  // Cells arrive strictly in order; the following cell is already in flight.
+  __device__ __forceinline__ Cons load(int) {
+    const Cons u = next;
+    next = fetch();
+    return u;
+  }
+  __device__ __forceinline__ void boundary(int) {}
+};
+
 __global__ void __launch_bounds__(128) sweep_x_kernel(SweepArgs a) {
-  const int j = 1 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (j > a.ny) return;
+  const int jt = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = jt <= a.ny;
+  const int j = active ? jt : a.ny;  // idle lanes shadow the last column, writes masked
   if (latched(a)) return;
   if (*(volatile unsigned long long*)a.dt_err != kNoError) {
     // compute_dt of this step failed (detected by the previous row sweep).
-    record(a.err, *(volatile unsigned long long*)a.dt_err);
+    if (active) record(a.err, *(volatile unsigned long long*)a.dt_err);
     return;
   }
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && a.limit_out)
     *a.limit_out = kEmptyLimit;
   const Gas g = make_gas(a.gamma);
-  const double dt = step_dt(a);
-  const double dtdx = dt / a.dx;
+  const double dtdx = step_dt(a) / a.dx;
   const int i_lo = 1 + blockIdx.y * a.seg;
   const int i_hi = min(a.nx, i_lo + a.seg - 1);
-  const double* __restrict__ src = a.src;
-  double* __restrict__ dst = a.dst;
   const size_t pitch = a.pitch;
-  auto load = [&](int k) -> Cons {
-    const int i = k - 1;
-    return {__ldg(src + cell_index(pitch, 0, i, j)), __ldg(src + cell_index(pitch, 1, i, j)),
-            __ldg(src + cell_index(pitch, 2, i, j)), __ldg(src + cell_index(pitch, 3, i, j))};
-  };
+  ColumnSource src{a.src + cell_index(pitch, 0, i_lo - 2, j), pitch, {}};
+  // the prefetch reads one row past the stencil (row nx+3 at most: a
+  // padding row of the allocation)
+  src.start();
+  double* __restrict__ dst = a.dst;
   const int ny = a.ny;
   const bool refl = a.bc == 0;
-  auto put = [&](int i, int jj, const Cons& u, bool neg) {
-    dst[cell_index(pitch, 0, i, jj)] = u.r;
-    dst[cell_index(pitch, 1, i, jj)] = u.ma;
-    dst[cell_index(pitch, 2, i, jj)] = neg ? -u.mb : u.mb;
-    dst[cell_index(pitch, 3, i, jj)] = u.e;
+  auto put = [&](double* q, const Cons& u, bool neg) {
+    q[0] = u.r;
+    q[pitch] = u.ma;
+    q[2 * pitch] = neg ? -u.mb : u.mb;
+    q[3 * pitch] = u.e;
   };
-  auto sink = [&](int k, const Cons& u, const Recip&) {
-    const int i = k - 1;
-    put(i, j, u, false);
-    // y-wall ghosts of the column-sweep output (grid.cpp:44-59).
-    if (refl) {
-      if (j <= 2) put(i, 1 - j, u, true);
-      if (j >= ny - 1) put(i, 2 * ny + 1 - j, u, true);
-    } else {
-      if (j == 1) { put(i, 0, u, false); put(i, -1, u, false); }
-      if (j == ny) { put(i, ny + 1, u, false); put(i, ny + 2, u, false); }
+  double* out = dst + cell_index(pitch, 0, i_lo, j);
+  auto sink = [&](int, const StepOut& o) {
+    if (active) {
+      put(out, o.un, false);
+      // y-wall ghosts of the column-sweep output (grid.cpp:44-59)
+      if (refl) {
+        if (j <= 2) put(out + (1 - 2 * j), o.un, true);
+        if (j >= ny - 1) put(out + (2 * ny + 1 - 2 * j), o.un, true);
+      } else {
+        if (j == 1) { put(out - 1, o.un, false); put(out - 2, o.un, false); }
+        if (j == ny) { put(out + 1, o.un, false); put(out + 2, o.un, false); }
+      }
     }
+    out += 4 * pitch;
   };
   const unsigned long long base = error_key(a.step, 1, j, 0, 0, 0);
-  walk_strip(i_lo + 1, i_hi + 1, load, sink, g, dtdx, a.err, base, a.row0);
+  walk_strip<false>(i_lo + 1, i_hi + 1, src, sink, g, dtdx, 0.0, active, a.err, base, a.row0);
 }
 
 // ---------------------------------------------------------------------------
-// Row sweep: thread = row i, segment of columns.  Also produces the next
-// step's dt limit and the i-wall ghost rows.
-__global__ void __launch_bounds__(128) sweep_y_kernel(SweepArgs a) {
-  const int i = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+// Row sweep with TMA-staged tiles.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                         int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store(const CUtensorMap* map, const void* src, int c0, int c1,
+                                          int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::
+                   "l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Byte offset of (row r, variable v, column c) in a staged chunk: one TMA box
+// {kChunk columns, 1 variable, kRowsPerCta rows} per variable, so the layout
+// is [v][r][c] with a 16-byte row pitch -- a warp's 32 rows are 512
+// contiguous bytes (the minimum 4 wavefronts for 16-byte accesses).
+constexpr int kVarBytes = kRowsPerCta * kChunk * 8;
+__device__ __forceinline__ uint32_t swz(int r, int v, int c) {
+  return (uint32_t)(v * kVarBytes + r * (kChunk * 8) + c * 8);
+}
+
+struct RowTiles {
+  const CUtensorMap* load_map;
+  const CUtensorMap* store_map;
+  uint8_t* base;        // in[0], in[1], out[0], out[1], consecutive kChunkBytes
+  uint64_t* full;       // 2 mbarriers
+  int row;              // this thread's row within the CTA tile
+  int i0;               // first grid row of the CTA tile
+  int kfirst;           // first strip cell staged (= ka - 2)
+  int ka, kb;           // output cells
+  int nin;              // input chunks needed
+  bool leader;
+  bool active;
+
+  __device__ __forceinline__ void issue(int q) {  // input chunk q -> buffer q&1
+    if (q >= nin) return;
+    mbar_expect_tx(&full[q & 1], kChunkBytes);
+    // strip cell k is column k-1, stored at column offset k-1+kColOff
+    uint8_t* dst = base + (q & 1) * kChunkBytes;
+    const int col = kfirst + q * kChunk - 1 + kColOff;
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+      tma_load(dst + v * kVarBytes, load_map, &full[q & 1], col, v, i0 + 1);
+  }
+
+  __device__ __forceinline__ Cons load(int k) {
+    const int rel = k - kfirst;
+    const int q = rel / kChunk, pos = rel % kChunk;
+    if (pos == 0) mbar_wait(&full[q & 1], (q >> 1) & 1);
+    const uint8_t* b = base + (q & 1) * kChunkBytes;
+    // sweep orientation: mom_a = mom_y (variable 2), mom_b = mom_x
+    Cons u = {*(const double*)(b + swz(row, 0, pos)), *(const double*)(b + swz(row, 2, pos)),
+              *(const double*)(b + swz(row, 1, pos)), *(const double*)(b + swz(row, 3, pos))};
+    if (!active) u = {1.0, 0.0, 0.0, 1.0};  // rows past the grid: inert
+    return u;
+  }
+
+  __device__ __forceinline__ void put(int k, const Cons& u) {
+    const int rel = k - ka;
+    uint8_t* b = base + (2 + ((rel / kChunk) & 1)) * kChunkBytes;
+    const int pos = rel % kChunk;
+    *(double*)(b + swz(row, 0, pos)) = u.r;
+    *(double*)(b + swz(row, 2, pos)) = u.ma;
+    *(double*)(b + swz(row, 1, pos)) = u.mb;
+    *(double*)(b + swz(row, 3, pos)) = u.e;
+  }
+
+  // Called after iteration c; chunk boundaries fall on even c - ka.
+  __device__ __forceinline__ void boundary(int c) {
+    const int rel = c - ka;
+    if (rel & 1) return;
+    flush(c);
+  }
+
+  __device__ __forceinline__ void flush(int c) {
+    const int rel = c - ka;
+    if (leader) bulk_wait_read0();  // previous output chunk has left smem
+    fence_async_smem();             // this thread's tile writes -> async proxy
+    __syncthreads();
+    if (leader) {
+      if (rel >= 2) {  // output chunk (rel-2)/2 complete: cells c-2, c-1
+        const int q = (rel - 2) / kChunk;
+        const uint8_t* src = base + (2 + (q & 1)) * kChunkBytes;
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          tma_store(store_map, src + v * kVarBytes, ka + q * kChunk - 1 + kColOff, v, i0 + 1);
+        bulk_commit();
+      }
+      // input chunk rel/2 + 1 fully consumed: refill its buffer two ahead
+      issue(rel / kChunk + 3);
+    }
+  }
+};
+
+__global__ void __launch_bounds__(128) sweep_y_kernel(SweepArgs a,
+                                                       const __grid_constant__ CUtensorMap load_map,
+                                                       const __grid_constant__ CUtensorMap store_map) {
+  extern __shared__ uint8_t smem_raw[];
   if (latched(a)) return;
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+  const int i0 = 1 + blockIdx.x * kRowsPerCta;
+  const int i = i0 + threadIdx.x;
   const bool active = i <= a.nx;
   const Gas g = make_gas(a.gamma);
-  const double dt = step_dt(a);
-  const double dtdx = dt / a.dx;
+  const double dtdx = step_dt(a) / a.dx;
   const int j_lo = 1 + blockIdx.y * a.seg;
   const int j_hi = min(a.ny, j_lo + a.seg - 1);
-  const double* __restrict__ src = a.src;
-  double* __restrict__ dst = a.dst;
+
+  RowTiles t;
+  t.load_map = &load_map;
+  t.store_map = &store_map;
+  t.base = smem;
+  t.full = (uint64_t*)(smem + 4 * kChunkBytes);
+  t.row = threadIdx.x;
+  t.i0 = i0;
+  t.ka = j_lo + 1;
+  t.kb = j_hi + 1;
+  t.kfirst = t.ka - 2;
+  t.nin = (t.kb + 2 - t.kfirst + kChunk) / kChunk;
+  t.leader = threadIdx.x == 0;
+  t.active = active;
+  if (t.leader) {
+    mbar_init(&t.full[0], 1);
+    mbar_init(&t.full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    t.issue(0);
+    t.issue(1);
+  }
+  __syncthreads();
+
   const size_t pitch = a.pitch;
   const int nx = a.nx;
   const bool refl = a.bc == 0;
-  const bool mirror_lo = a.wall_lo && i <= 2;
-  const bool mirror_hi = a.wall_hi && i >= nx - 1;
+  const bool mirror_lo = active && a.wall_lo && i <= 2;
+  const bool mirror_hi = active && a.wall_hi && i >= nx - 1;
+  double* __restrict__ dst = a.dst;
   double lim_min = __longlong_as_double(0x7ff0000000000000ll);
   unsigned long long dt_key = kNoError;
-  auto load = [&](int k) -> Cons {
-    const int j = k - 1;
-    return {__ldg(src + cell_index(pitch, 0, i, j)), __ldg(src + cell_index(pitch, 2, i, j)),
-            __ldg(src + cell_index(pitch, 1, i, j)), __ldg(src + cell_index(pitch, 3, i, j))};
-  };
-  auto put = [&](int ii, int j, const Cons& u, bool neg) {
-    dst[cell_index(pitch, 0, ii, j)] = u.r;
-    dst[cell_index(pitch, 2, ii, j)] = u.ma;
-    dst[cell_index(pitch, 1, ii, j)] = neg ? -u.mb : u.mb;
-    dst[cell_index(pitch, 3, ii, j)] = u.e;
-  };
   const int gi = a.row0 + i;
-  auto sink = [&](int k, const Cons& u, const Recip& rn) {
+  auto put_row = [&](int ii, int j, const Cons& u, bool neg) {
+    double* q = dst + cell_index(pitch, 0, ii, j);
+    q[0] = u.r;
+    q[2 * pitch] = u.ma;
+    q[pitch] = neg ? -u.mb : u.mb;
+    q[3 * pitch] = u.e;
+  };
+  auto sink = [&](int k, const StepOut& o) {
+    t.put(k, o.un);
+    if (!active) return;
     const int j = k - 1;
-    put(i, j, u, false);
     if (mirror_lo) {  // x-wall ghosts for the next column sweep (grid.cpp:26-42)
-      if (refl) put(1 - i, j, u, true);
-      else if (i == 1) { put(0, j, u, false); put(-1, j, u, false); }
+      if (refl) put_row(1 - i, j, o.un, true);
+      else if (i == 1) { put_row(0, j, o.un, false); put_row(-1, j, o.un, false); }
     }
     if (mirror_hi) {
-      if (refl) put(2 * nx + 1 - i, j, u, true);
-      else if (i == nx) { put(nx + 1, j, u, false); put(nx + 2, j, u, false); }
+      if (refl) put_row(2 * nx + 1 - i, j, o.un, true);
+      else if (i == nx) { put_row(nx + 1, j, o.un, false); put_row(nx + 2, j, o.un, false); }
     }
     if (a.want_limit) {
-      double lim;
-      const int f = dt_limit(u, rn, a.spacing, g, lim);
-      if (f >= 0) {
-        const unsigned long long key = error_key(a.step + 1, 0, gi, 0, j, f);
+      if (o.fD >= 0) {
+        const unsigned long long key = error_key(a.step + 1, 0, gi, 0, j, o.fD);
         dt_key = key < dt_key ? key : dt_key;
       } else {
-        lim_min = smin(lim_min, lim);
+        lim_min = smin(lim_min, o.lim);
       }
     }
   };
-  if (active) {
-    const unsigned long long base = error_key(a.step, 2, gi, 0, 0, 0);
-    walk_strip(j_lo + 1, j_hi + 1, load, sink, g, dtdx, a.err, base, 0);
-  }
+  const unsigned long long base = error_key(a.step, 2, gi, 0, 0, 0);
+  if (a.want_limit)
+    walk_strip<true>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, active, a.err, base, 0);
+  else
+    walk_strip<false>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, active, a.err, base, 0);
+  // an odd-length final segment leaves one output chunk unflushed
+  if (((t.kb + 1 - t.ka) & 1) != 0) t.flush(t.kb + 2);
+  if (t.leader) bulk_wait0();
   if (a.want_limit) {
     const unsigned long long m = warp_min_u64((unsigned long long)__double_as_longlong(lim_min));
     const unsigned long long e = warp_min_u64(dt_key);
@@ -254,9 +484,13 @@ __global__ void __launch_bounds__(256) prologue_kernel(PrologueArgs a) {
       }
     }
     if (a.want_limit) {
-      const Recip rr = make_recip(c.r);
       double l;
-      const int f = dt_limit(c, rr, a.spacing, g, l);
+      FastMath fm;
+      int f = dt_limit(fm, c, fm.recip(c.r), a.spacing, g, l);
+      if (!fm.ok) {
+        ExactMath em;
+        f = dt_limit(em, c, em.recip(c.r), a.spacing, g, l);
+      }
       if (f >= 0) {
         const unsigned long long k = error_key(a.step, 0, a.row0 + i, 0, j, f);
         key = k < key ? k : key;
@@ -325,54 +559,70 @@ __global__ void init_kernel(InitArgs a) {
   const int j = 1 + blockIdx.x * blockDim.x + threadIdx.x;
   if (j > a.ny) return;
   for (int i = 1 + blockIdx.y; i <= a.nx; i += gridDim.y) {
-  const int gi = a.row0 + i;
-  Prim w = {1.0, 0.0, 0.0, 1.0};
-  switch (a.case_id) {
-    case 1: w.p = 1e-5 * (a.gamma - 1.0); break;
-    case 3: w.p = 1e-5; break;
-    case 2:
-      if (!(j <= a.ny / 2)) w = {0.125, 0.0, 0.0, 0.1};
-      break;
-    case 4:
-      if (!(gi <= a.global_nx / 2)) w = {0.125, 0.0, 0.0, 0.1};
-      break;
-    case 5: {
-      const unsigned long long cell =
-          (unsigned long long)(gi - 1) * (unsigned long long)a.ny + (unsigned long long)(j - 1);
-      w.r = 1.0 + 0.1 * rnd_sym(a.seed, cell, 0);
-      w.p = 1.0 + 0.1 * rnd_sym(a.seed, cell, 1);
-      w.va = 0.1 * rnd_sym(a.seed, cell, 2);
-      w.vb = 0.1 * rnd_sym(a.seed, cell, 3);
-      break;
+    const int gi = a.row0 + i;
+    Prim w = {1.0, 0.0, 0.0, 1.0};
+    switch (a.case_id) {
+      case 1: w.p = 1e-5 * (a.gamma - 1.0); break;
+      case 3: w.p = 1e-5; break;
+      case 2:
+        if (!(j <= a.ny / 2)) w = {0.125, 0.0, 0.0, 0.1};
+        break;
+      case 4:
+        if (!(gi <= a.global_nx / 2)) w = {0.125, 0.0, 0.0, 0.1};
+        break;
+      case 5: {
+        const unsigned long long cell =
+            (unsigned long long)(gi - 1) * (unsigned long long)a.ny + (unsigned long long)(j - 1);
+        w.r = 1.0 + 0.1 * rnd_sym(a.seed, cell, 0);
+        w.p = 1.0 + 0.1 * rnd_sym(a.seed, cell, 1);
+        w.va = 0.1 * rnd_sym(a.seed, cell, 2);
+        w.vb = 0.1 * rnd_sym(a.seed, cell, 3);
+        break;
+      }
+      default: break;
     }
-    default: break;
-  }
-  // prim_to_cons (euler_kernel.cpp:22-28)
-  double e = w.p / (a.gamma - 1.0) + 0.5 * w.r * (w.va * w.va + w.vb * w.vb);
-  if (a.case_id == 3 && gi == 1 && j == 1) e = 1.0 / (a.dx * a.dy);
-  if (a.case_id == 1) {
-    const int gnx = a.global_nx, ny = a.ny;
-    const bool ci = (gnx % 2) ? (gi == (gnx + 1) / 2) : (gi == gnx / 2 || gi == gnx / 2 + 1);
-    const bool cj = (ny % 2) ? (j == (ny + 1) / 2) : (j == ny / 2 || j == ny / 2 + 1);
-    if (ci && cj) {
-      const double share = 1.0 / ((double)((gnx % 2) ? 1 : 2) * (double)((ny % 2) ? 1 : 2));
-      e = share / (a.dx * a.dy);
+    // prim_to_cons (euler_kernel.cpp:22-28)
+    double e = w.p / (a.gamma - 1.0) + 0.5 * w.r * (w.va * w.va + w.vb * w.vb);
+    if (a.case_id == 3 && gi == 1 && j == 1) e = 1.0 / (a.dx * a.dy);
+    if (a.case_id == 1) {
+      const int gnx = a.global_nx, ny = a.ny;
+      const bool ci = (gnx % 2) ? (gi == (gnx + 1) / 2) : (gi == gnx / 2 || gi == gnx / 2 + 1);
+      const bool cj = (ny % 2) ? (j == (ny + 1) / 2) : (j == ny / 2 || j == ny / 2 + 1);
+      if (ci && cj) {
+        const double share = 1.0 / ((double)((gnx % 2) ? 1 : 2) * (double)((ny % 2) ? 1 : 2));
+        e = share / (a.dx * a.dy);
+      }
     }
-  }
-  const size_t p = a.pitch;
-  a.u[cell_index(p, 0, i, j)] = w.r;
-  a.u[cell_index(p, 1, i, j)] = w.r * w.va;
-  a.u[cell_index(p, 2, i, j)] = w.r * w.vb;
-  a.u[cell_index(p, 3, i, j)] = e;
+    const size_t p = a.pitch;
+    a.u[cell_index(p, 0, i, j)] = w.r;
+    a.u[cell_index(p, 1, i, j)] = w.r * w.va;
+    a.u[cell_index(p, 2, i, j)] = w.r * w.vb;
+    a.u[cell_index(p, 3, i, j)] = e;
   }
 }
 
-int segments(int n, int strips, int want_seg) {
-  if (want_seg > 0) return (n + want_seg - 1) / want_seg;
-  // Enough threads for ~2 waves of 148 SMs x 16 warps, segments >= 24 cells.
-  const long long target = 148LL * 512 * 2;
-  long long nseg = (target + strips - 1) / strips;
-  const long long max_seg = (n + 23) / 24;
+// FastMath against the compiler's IEEE operations (tests/test_gpu_math.py).
+__global__ void math_selftest_kernel(int op, const double* a, const double* b, double* fast,
+                                     double* ref, int* okv, size_t n) {
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  FastMath fm;
+  if (op == 0) {
+    fast[t] = fm.divf(a[t], b[t]);
+    ref[t] = a[t] / b[t];
+  } else {
+    fast[t] = fm.sqrt(a[t]);
+    ref[t] = sqrt(a[t]);
+  }
+  okv[t] = fm.ok ? 1 : 0;
+}
+
+// Segments per strip: about one wave of resident CTAs; a multiple of
+// kChunk cells per segment where the row sweep needs it.
+int pick_segments(int n, int strip_blocks, int ctas_per_wave, int align) {
+  long long nseg = ctas_per_wave / (strip_blocks > 0 ? strip_blocks : 1);
+  if (nseg < 1) nseg = 1;
+  const long long max_seg = (n + 15) / 16;  // keep segments >= 16 cells
   if (nseg > max_seg) nseg = max_seg;
   if (nseg < 1) nseg = 1;
   return (int)nseg;
@@ -380,20 +630,70 @@ int segments(int n, int strips, int want_seg) {
 
 }  // namespace
 
-void launch_sweep_x(const SweepArgs& a0, int block, cudaStream_t s) {
-  SweepArgs a = a0;
-  const int nseg = segments(a.nx, a.ny, a.seg);
-  a.seg = (a.nx + nseg - 1) / nseg;
-  dim3 grid((a.ny + block - 1) / block, nseg);
-  sweep_x_kernel<<<grid, block, 0, s>>>(a);
+int query_geometry(Geometry* g) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(sweep_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
+  int ox = 0, oy = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, sweep_x_kernel, 128, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy, sweep_y_kernel, 128, kYSmemBytes);
+  g->ctas_x_per_sm = ox > 0 ? ox : 1;
+  g->ctas_y_per_sm = oy > 0 ? oy : 1;
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
-void launch_sweep_y(const SweepArgs& a0, int block, cudaStream_t s) {
+bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, int ny) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  const cuuint64_t strides[2] = {pitch * 8, 4 * pitch * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)kChunk, 1, (cuuint32_t)kRowsPerCta};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  // load: all of U_b (ghost rows/columns included)
+  const cuuint64_t dim_load[3] = {pitch, 4, (cuuint64_t)nx + 4};
+  CUresult r1 = encode(&maps->y_load, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, B, dim_load, strides,
+                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  // store: rows -1..nx (the tail CTA's rows past nx are clipped) and
+  // column offsets up to j = ny (a short final segment is clipped)
+  const cuuint64_t dim_store[3] = {(cuuint64_t)ny + 1 + kColOff, 4, (cuuint64_t)nx + 2};
+  CUresult r2 = encode(&maps->y_store, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, A, dim_store, strides,
+                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r1 == CUDA_SUCCESS && r2 == CUDA_SUCCESS;
+}
+
+void launch_sweep_x(const SweepArgs& a0, const Geometry& geo, cudaStream_t s) {
   SweepArgs a = a0;
-  const int nseg = segments(a.ny, a.nx, a.seg);
-  a.seg = (a.ny + nseg - 1) / nseg;
-  dim3 grid((a.nx + block - 1) / block, nseg);
-  sweep_y_kernel<<<grid, block, 0, s>>>(a);
+  const int blocks = (a.ny + 127) / 128;
+  int nseg = a.seg > 0 ? (a.nx + a.seg - 1) / a.seg
+                       : pick_segments(a.nx, blocks, geo.sms * geo.ctas_x_per_sm, 1);
+  a.seg = (a.nx + nseg - 1) / nseg;
+  nseg = (a.nx + a.seg - 1) / a.seg;
+  a.nseg = nseg;
+  sweep_x_kernel<<<dim3(blocks, nseg), 128, 0, s>>>(a);
+}
+
+void launch_sweep_y(const SweepArgs& a0, const TmaMaps& maps, const Geometry& geo,
+                    cudaStream_t s) {
+  SweepArgs a = a0;
+  const int blocks = (a.nx + kRowsPerCta - 1) / kRowsPerCta;
+  int nseg = a.seg > 0 ? (a.ny + a.seg - 1) / a.seg
+                       : pick_segments(a.ny, blocks, geo.sms * geo.ctas_y_per_sm, kChunk);
+  int seg = (a.ny + nseg - 1) / nseg;
+  seg = (seg + kChunk - 1) / kChunk * kChunk;  // whole output chunks per segment
+  a.seg = seg;
+  a.nseg = (a.ny + seg - 1) / seg;
+  sweep_y_kernel<<<dim3(blocks, a.nseg), kRowsPerCta, kYSmemBytes, s>>>(a, maps.y_load,
+                                                                        maps.y_store);
 }
 
 void launch_prologue(const PrologueArgs& a, cudaStream_t s) {
@@ -409,6 +709,11 @@ void launch_finish(const FinishArgs& a, cudaStream_t s) {
 void launch_init(const InitArgs& a, cudaStream_t s) {
   dim3 grid((a.ny + 255) / 256, a.nx < 4096 ? a.nx : 4096);
   init_kernel<<<grid, 256, 0, s>>>(a);
+}
+
+void launch_math_selftest(int op, const double* a, const double* b, double* fast, double* ref,
+                          int* ok, size_t n, cudaStream_t s) {
+  math_selftest_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(op, a, b, fast, ref, ok, n);
 }
 
 }  // namespace hb

@@ -1,6 +1,8 @@
 // hydro_kernels.cuh -- device-side state layout and kernel parameter blocks.
 #pragma once
 
+#include <cuda.h>
+
 #include <cstddef>
 #include <cstdint>
 
@@ -15,6 +17,13 @@ namespace hb {
 // (all four variables) are therefore one contiguous block of 8*pitch
 // doubles -- a slab halo is a single contiguous send/recv.
 constexpr int kColOff = 3;
+
+// Row-sweep tiling: a CTA owns kRowsPerCta rows; TMA stages kChunk columns
+// of all four variables per chunk (two input and two output buffers).
+constexpr int kRowsPerCta = 128;
+constexpr int kChunk = 2;
+constexpr int kChunkBytes = kRowsPerCta * 4 * kChunk * 8;  // 8 KB
+constexpr int kYSmemBytes = 4 * kChunkBytes + 128 + 64;     // + alignment, mbarriers
 
 __host__ __device__ __forceinline__ size_t cell_index(size_t pitch, int v, int i, int j) {
   return ((size_t)(i + 1) * 4 + (size_t)v) * pitch + (size_t)(j + kColOff);
@@ -31,6 +40,7 @@ struct SweepArgs {
   size_t pitch;
   int nx, ny;                 // local interior extent
   int seg;                    // strip segment length per thread
+  int nseg;                   // segments per strip
   double dx;                  // spacing along the sweep
   double spacing;             // min(dx, dy) for the dt limit
   double gamma, cfl;
@@ -47,6 +57,11 @@ struct SweepArgs {
   int want_limit;             // row sweep: produce limit_out
 };
 
+struct TmaMaps {
+  CUtensorMap y_load;         // U_b, box {kChunk cols, 1 var, kRowsPerCta rows}
+  CUtensorMap y_store;        // U_a interior rows/cols only (clips ghosts)
+};
+
 struct PrologueArgs {
   double* u;
   size_t pitch;
@@ -57,7 +72,6 @@ struct PrologueArgs {
   unsigned long long* limit_out;
   unsigned long long* err;
   unsigned long long* dt_err;
-  unsigned long long* reset;   // slot reset to +inf bits (may be null)
   int step;
 };
 
@@ -77,10 +91,20 @@ struct InitArgs {
   unsigned long long seed;
 };
 
-void launch_sweep_x(const SweepArgs& a, int block, cudaStream_t s);
-void launch_sweep_y(const SweepArgs& a, int block, cudaStream_t s);
+struct Geometry {
+  int ctas_x_per_sm;          // resident CTAs per SM (from the occupancy API)
+  int ctas_y_per_sm;
+  int sms;
+};
+
+bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, int ny);
+int query_geometry(Geometry* g);
+void launch_sweep_x(const SweepArgs& a, const Geometry& geo, cudaStream_t s);
+void launch_sweep_y(const SweepArgs& a, const TmaMaps& maps, const Geometry& geo, cudaStream_t s);
 void launch_prologue(const PrologueArgs& a, cudaStream_t s);
 void launch_finish(const FinishArgs& a, cudaStream_t s);
 void launch_init(const InitArgs& a, cudaStream_t s);
+void launch_math_selftest(int op, const double* a, const double* b, double* fast, double* ref,
+                          int* ok, size_t n, cudaStream_t s);
 
 }  // namespace hb

@@ -1,0 +1,80 @@
+"""The device fp64 division / square-root fast paths (FastMath in
+csrc/hydro_physics.cuh) against the compiler's IEEE `/` and sqrt() on the
+same B200: wherever the fast path reports itself in range, the bits must be
+identical; outside its range the kernels recompute with the IEEE operation,
+so only the in-range results matter -- but they must cover the operand
+ranges the physics produces.  Host numpy (x86 IEEE) is the second witness."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2106_13465_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+_dp = C.POINTER(C.c_double)
+
+
+def run(op, a, b=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(a if b is None else b, dtype=np.float64)
+    n = a.size
+    fast, exact = np.empty(n), np.empty(n)
+    ok = np.empty(n, dtype=np.int32)
+    rc = _lib.lib().hydro_gpu_math_selftest(op, a.ctypes.data_as(_dp), b.ctypes.data_as(_dp),
+                                            fast.ctypes.data_as(_dp), exact.ctypes.data_as(_dp),
+                                            ok.ctypes.data_as(C.POINTER(C.c_int)), n)
+    assert rc == 0
+    return fast, exact, ok.astype(bool)
+
+
+def operands(rng, n):
+    mant = rng.uniform(1.0, 2.0, n)
+    expo = rng.integers(-1030, 1024, n)
+    sign = rng.choice([-1.0, 1.0], n)
+    x = sign * np.ldexp(mant, expo)
+    special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, -5e-324, 2.2250738585072014e-308,
+                        1.7976931348623157e308, 1.0, -1.0, 0.4, 0.3999999999999999])
+    return np.concatenate([x, special, rng.uniform(-10, 10, n // 4),
+                           rng.uniform(1e-6, 1e6, n // 4)])
+
+
+def bits(x):
+    return x.view(np.uint64)
+
+
+def test_division_fast_path_is_ieee():
+    rng = np.random.default_rng(2106)
+    a = operands(rng, 1 << 20)
+    b = rng.permutation(operands(rng, 1 << 20))[: a.size]
+    fast, exact, ok = run(0, a, b)
+    assert ok.mean() > 0.85
+    assert np.array_equal(bits(fast[ok]), bits(exact[ok]))
+    with np.errstate(all="ignore"):
+        host = a / b
+    both = ok & ~np.isnan(host)
+    assert np.array_equal(bits(fast[both]), bits(host[both]))
+
+
+def test_division_physics_ranges_all_fast():
+    rng = np.random.default_rng(1)
+    a = rng.uniform(-1e9, 1e9, 1 << 20)
+    b = np.concatenate([rng.uniform(1e-9, 1e9, 1 << 19), -rng.uniform(1e-9, 1e9, 1 << 19)])
+    fast, exact, ok = run(0, a, b)
+    assert ok.mean() > 0.999
+    assert np.array_equal(bits(fast[ok]), bits(exact[ok]))
+    assert np.array_equal(bits(fast[ok]), bits((a / b)[ok]))
+
+
+def test_sqrt_fast_path_is_ieee():
+    rng = np.random.default_rng(13465)
+    x = np.abs(operands(rng, 1 << 20))
+    fast, exact, ok = run(1, x)
+    assert ok.mean() > 0.9
+    assert np.array_equal(bits(fast[ok]), bits(exact[ok]))
+    with np.errstate(all="ignore"):
+        host = np.sqrt(x)
+    assert np.array_equal(bits(fast[ok]), bits(host[ok]))
+    # negative, zero, inf, nan never take the fast path
+    f2, e2, ok2 = run(1, np.array([-1.0, 0.0, -0.0, np.inf, np.nan, 1e-310]))
+    assert not ok2.any()
