@@ -11,7 +11,8 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhydro_b200.so")
+# HYDRO_B200_LIB selects an alternative build (tools/variants.sh); default in-tree.
+LIB_PATH = os.environ.get("HYDRO_B200_LIB") or os.path.join(HERE, "libhydro_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "hydro_gpu.h")
 
 

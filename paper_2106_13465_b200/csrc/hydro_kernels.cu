@@ -167,7 +167,14 @@ struct ColumnSource {
   __device__ __forceinline__ void boundary(int) {}
 };
 
-__global__ void __launch_bounds__(128) sweep_x_kernel(SweepArgs a) {
+#ifndef HB_X_MINB
+#define HB_X_MINB 4
+#endif
+#ifndef HB_Y_MINB
+#define HB_Y_MINB 4
+#endif
+
+__global__ void __launch_bounds__(128, HB_X_MINB) sweep_x_kernel(SweepArgs a) {
   const int jt = 1 + blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = jt <= a.ny;
   const int j = active ? jt : a.ny;  // idle lanes shadow the last column, writes masked
@@ -353,7 +360,7 @@ struct RowTiles {
   }
 };
 
-__global__ void __launch_bounds__(128) sweep_y_kernel(SweepArgs a,
+__global__ void __launch_bounds__(128, HB_Y_MINB) sweep_y_kernel(SweepArgs a,
                                                        const __grid_constant__ CUtensorMap load_map,
                                                        const __grid_constant__ CUtensorMap store_map) {
   extern __shared__ uint8_t smem_raw[];

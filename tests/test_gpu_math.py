@@ -78,3 +78,19 @@ def test_sqrt_fast_path_is_ieee():
     # negative, zero, inf, nan never take the fast path
     f2, e2, ok2 = run(1, np.array([-1.0, 0.0, -0.0, np.inf, np.nan, 1e-310]))
     assert not ok2.any()
+
+
+def test_division_zero_numerator_fast_and_signed():
+    """Zero momenta are everywhere in the benchmark cases (u = v = 0 at rest):
+    +-0 / positive-normal must stay on the fast path with the IEEE sign."""
+    rng = np.random.default_rng(7)
+    b = np.concatenate([rng.uniform(1e-300, 1e300, 4096), rng.uniform(1e-6, 1e6, 4096)])
+    for zero in (0.0, -0.0):
+        a = np.full(b.size, zero)
+        fast, exact, ok = run(0, a, b)
+        assert ok.all()
+        assert np.array_equal(bits(fast), bits(exact))
+        assert np.array_equal(bits(fast), bits(a / b))
+    # negative or non-normal denominators leave the fast path (exact recompute)
+    _, _, ok = run(0, np.array([-0.0, 0.0, 0.0, 0.0]), np.array([-2.0, 0.0, 5e-324, np.inf]))
+    assert not ok.any()
