@@ -109,7 +109,6 @@ __device__ __forceinline__ void walk_strip(int ka, int kb, Src& src, Sink& sink,
     w.frPrev.rr = em.recip(w.wA.r);
     w.fluxPrev = {0.0, 0.0, 0.0, 0.0};
   }
-  src.boundary(ka - 2);  // the first staged chunk is consumed
 #pragma unroll 1
   for (int c = ka - 1; c <= kb + 1; ++c) {
     const Cons uC = src.load(c + 1);
@@ -171,7 +170,7 @@ struct ColumnSource {
 #define HB_X_MINB 4
 #endif
 #ifndef HB_Y_MINB
-#define HB_Y_MINB 4
+#define HB_Y_MINB 8
 #endif
 
 __global__ void __launch_bounds__(128, HB_X_MINB) sweep_x_kernel(SweepArgs a) {
@@ -278,89 +277,94 @@ __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// Byte offset of (row r, variable v, column c) in a staged chunk: one TMA box
-// {kChunk columns, 1 variable, kRowsPerCta rows} per variable, so the layout
-// is [v][r][c] with a 16-byte row pitch -- a warp's 32 rows are 512
-// contiguous bytes (the minimum 4 wavefronts for 16-byte accesses).
+// Row-sweep staging: a CTA of kRowsPerCta threads (one row each) walks a
+// column segment in chunks of kChunk columns.  Chunk Q holds strip cells
+// [ka-4+4Q, ka-1+4Q] of all four variables, laid out [v][row][col] (one TMA
+// box {kChunk cols, 1 var, kRowsPerCta rows} per variable, 32-byte rows =
+// whole DRAM sectors).  A ring of kNBuf buffers is used in place: once a
+// cell has been read into registers its slot receives the updated cell
+// (2 iterations later), and a completed chunk leaves with TMA bulk-tensor
+// stores before its buffer is refilled kNBuf-1 chunks ahead.
 constexpr int kVarBytes = kRowsPerCta * kChunk * 8;
-__device__ __forceinline__ uint32_t swz(int r, int v, int c) {
+__device__ __forceinline__ uint32_t slot(int r, int v, int c) {
   return (uint32_t)(v * kVarBytes + r * (kChunk * 8) + c * 8);
 }
 
 struct RowTiles {
   const CUtensorMap* load_map;
   const CUtensorMap* store_map;
-  uint8_t* base;        // in[0], in[1], out[0], out[1], consecutive kChunkBytes
-  uint64_t* full;       // 2 mbarriers
+  uint8_t* base;        // kNBuf consecutive kChunkBytes buffers
+  uint64_t* full;       // kNBuf mbarriers
   int row;              // this thread's row within the CTA tile
   int i0;               // first grid row of the CTA tile
-  int kfirst;           // first strip cell staged (= ka - 2)
-  int ka, kb;           // output cells
-  int nin;              // input chunks needed
+  int ka, kb;           // output strip cells
+  int nq;               // chunks needed (cells ka-4 .. kb+2)
+  int ready;            // highest chunk this thread has waited for
   bool leader;
   bool active;
 
-  __device__ __forceinline__ void issue(int q) {  // input chunk q -> buffer q&1
-    if (q >= nin) return;
-    mbar_expect_tx(&full[q & 1], kChunkBytes);
+  __device__ __forceinline__ uint8_t* buf(int q) { return base + (q % kNBuf) * kChunkBytes; }
+
+  __device__ __forceinline__ void issue(int q) {
+    if (q >= nq) return;
+    mbar_expect_tx(&full[q % kNBuf], kChunkBytes);
     // strip cell k is column k-1, stored at column offset k-1+kColOff
-    uint8_t* dst = base + (q & 1) * kChunkBytes;
-    const int col = kfirst + q * kChunk - 1 + kColOff;
+    const int col = ka - 4 + q * kChunk - 1 + kColOff;
 #pragma unroll
-    for (int v = 0; v < 4; ++v)
-      tma_load(dst + v * kVarBytes, load_map, &full[q & 1], col, v, i0 + 1);
+    for (int v = 0; v < 4; ++v) tma_load(buf(q) + v * kVarBytes, load_map, &full[q % kNBuf], col, v, i0 + 1);
   }
 
   __device__ __forceinline__ Cons load(int k) {
-    const int rel = k - kfirst;
+    const int rel = k - ka + 4;
     const int q = rel / kChunk, pos = rel % kChunk;
-    if (pos == 0) mbar_wait(&full[q & 1], (q >> 1) & 1);
-    const uint8_t* b = base + (q & 1) * kChunkBytes;
+    if (q > ready) {
+      mbar_wait(&full[q % kNBuf], (q / kNBuf) & 1);
+      ready = q;
+    }
+    const uint8_t* b = buf(q);
     // sweep orientation: mom_a = mom_y (variable 2), mom_b = mom_x
-    Cons u = {*(const double*)(b + swz(row, 0, pos)), *(const double*)(b + swz(row, 2, pos)),
-              *(const double*)(b + swz(row, 1, pos)), *(const double*)(b + swz(row, 3, pos))};
+    Cons u = {*(const double*)(b + slot(row, 0, pos)), *(const double*)(b + slot(row, 2, pos)),
+              *(const double*)(b + slot(row, 1, pos)), *(const double*)(b + slot(row, 3, pos))};
     if (!active) u = {1.0, 0.0, 0.0, 1.0};  // rows past the grid: inert
     return u;
   }
 
   __device__ __forceinline__ void put(int k, const Cons& u) {
-    const int rel = k - ka;
-    uint8_t* b = base + (2 + ((rel / kChunk) & 1)) * kChunkBytes;
+    const int rel = k - ka + 4;
+    uint8_t* b = buf(rel / kChunk);
     const int pos = rel % kChunk;
-    *(double*)(b + swz(row, 0, pos)) = u.r;
-    *(double*)(b + swz(row, 2, pos)) = u.ma;
-    *(double*)(b + swz(row, 1, pos)) = u.mb;
-    *(double*)(b + swz(row, 3, pos)) = u.e;
+    *(double*)(b + slot(row, 0, pos)) = u.r;
+    *(double*)(b + slot(row, 2, pos)) = u.ma;
+    *(double*)(b + slot(row, 1, pos)) = u.mb;
+    *(double*)(b + slot(row, 3, pos)) = u.e;
   }
 
-  // Called after iteration c; chunk boundaries fall on even c - ka.
+  // After iteration c: chunk boundaries fall on c - ka = 4T.
   __device__ __forceinline__ void boundary(int c) {
     const int rel = c - ka;
-    if (rel & 1) return;
-    flush(c);
+    if (rel < 0 || (rel % kChunk) != 0) return;
+    flush(rel / kChunk);
   }
 
-  __device__ __forceinline__ void flush(int c) {
-    const int rel = c - ka;
-    if (leader) bulk_wait_read0();  // previous output chunk has left smem
-    fence_async_smem();             // this thread's tile writes -> async proxy
+  // Chunk T's outputs are complete: store it, refill the buffer of chunk
+  // T-1 (stored at the previous boundary) with chunk T+kNBuf-1.
+  __device__ __forceinline__ void flush(int T) {
+    if (leader) bulk_wait_read0();  // chunk T-1's stores have left smem
+    fence_async_smem();             // this thread's slot writes -> async proxy
     __syncthreads();
     if (leader) {
-      if (rel >= 2) {  // output chunk (rel-2)/2 complete: cells c-2, c-1
-        const int q = (rel - 2) / kChunk;
-        const uint8_t* src = base + (2 + (q & 1)) * kChunkBytes;
+      if (T >= 1) {
+        const int col = ka - 4 + T * kChunk - 1 + kColOff;
 #pragma unroll
-        for (int v = 0; v < 4; ++v)
-          tma_store(store_map, src + v * kVarBytes, ka + q * kChunk - 1 + kColOff, v, i0 + 1);
+        for (int v = 0; v < 4; ++v) tma_store(store_map, buf(T) + v * kVarBytes, col, v, i0 + 1);
         bulk_commit();
       }
-      // input chunk rel/2 + 1 fully consumed: refill its buffer two ahead
-      issue(rel / kChunk + 3);
+      issue(T + kNBuf - 1);
     }
   }
 };
 
-__global__ void __launch_bounds__(128, HB_Y_MINB) sweep_y_kernel(SweepArgs a,
+__global__ void __launch_bounds__(kRowsPerCta, HB_Y_MINB) sweep_y_kernel(SweepArgs a,
                                                        const __grid_constant__ CUtensorMap load_map,
                                                        const __grid_constant__ CUtensorMap store_map) {
   extern __shared__ uint8_t smem_raw[];
@@ -378,21 +382,19 @@ __global__ void __launch_bounds__(128, HB_Y_MINB) sweep_y_kernel(SweepArgs a,
   t.load_map = &load_map;
   t.store_map = &store_map;
   t.base = smem;
-  t.full = (uint64_t*)(smem + 4 * kChunkBytes);
+  t.full = (uint64_t*)(smem + kNBuf * kChunkBytes);
   t.row = threadIdx.x;
   t.i0 = i0;
   t.ka = j_lo + 1;
   t.kb = j_hi + 1;
-  t.kfirst = t.ka - 2;
-  t.nin = (t.kb + 2 - t.kfirst + kChunk) / kChunk;
+  t.nq = (t.kb + 2 - (t.ka - 4) + kChunk) / kChunk;
+  t.ready = -1;
   t.leader = threadIdx.x == 0;
   t.active = active;
   if (t.leader) {
-    mbar_init(&t.full[0], 1);
-    mbar_init(&t.full[1], 1);
+    for (int q = 0; q < kNBuf; ++q) mbar_init(&t.full[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    t.issue(0);
-    t.issue(1);
+    for (int q = 0; q < kNBuf - 1; ++q) t.issue(q);
   }
   __syncthreads();
 
@@ -438,8 +440,9 @@ __global__ void __launch_bounds__(128, HB_Y_MINB) sweep_y_kernel(SweepArgs a,
     walk_strip<true>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, active, a.err, base, 0);
   else
     walk_strip<false>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, active, a.err, base, 0);
-  // an odd-length final segment leaves one output chunk unflushed
-  if (((t.kb + 1 - t.ka) & 1) != 0) t.flush(t.kb + 2);
+  // a final segment shorter than whole chunks leaves one chunk unstored
+  const int seg = t.kb + 1 - t.ka;
+  if (seg % kChunk != 0) t.flush(seg / kChunk + 1);
   if (t.leader) bulk_wait0();
   if (a.want_limit) {
     const unsigned long long m = warp_min_u64((unsigned long long)__double_as_longlong(lim_min));
@@ -644,7 +647,7 @@ int query_geometry(Geometry* g) {
   cudaFuncSetAttribute(sweep_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
   int ox = 0, oy = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, sweep_x_kernel, 128, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy, sweep_y_kernel, 128, kYSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy, sweep_y_kernel, kRowsPerCta, kYSmemBytes);
   g->ctas_x_per_sm = ox > 0 ? ox : 1;
   g->ctas_y_per_sm = oy > 0 ? oy : 1;
   return cudaGetLastError() == cudaSuccess ? 0 : 1;

@@ -19,11 +19,12 @@ namespace hb {
 constexpr int kColOff = 3;
 
 // Row-sweep tiling: a CTA owns kRowsPerCta rows; TMA stages kChunk columns
-// of all four variables per chunk (two input and two output buffers).
-constexpr int kRowsPerCta = 128;
-constexpr int kChunk = 2;
+// of all four variables per chunk into a ring of kNBuf buffers.
+constexpr int kRowsPerCta = 64;
+constexpr int kChunk = 4;
+constexpr int kNBuf = 3;
 constexpr int kChunkBytes = kRowsPerCta * 4 * kChunk * 8;  // 8 KB
-constexpr int kYSmemBytes = 4 * kChunkBytes + 128 + 64;     // + alignment, mbarriers
+constexpr int kYSmemBytes = kNBuf * kChunkBytes + 128 + 8 * kNBuf;  // + alignment, mbarriers
 
 __host__ __device__ __forceinline__ size_t cell_index(size_t pitch, int v, int i, int j) {
   return ((size_t)(i + 1) * 4 + (size_t)v) * pitch + (size_t)(j + kColOff);
