@@ -33,7 +33,8 @@ struct hydro_gpu_ctx {
   double* B = nullptr;  // column-sweep output
   size_t pitch = 0;
   size_t count = 0;     // doubles per state buffer
-  unsigned long long* slots = nullptr;  // [0],[1] dt limits, [2] error, [3] dt error
+  // [0],[1] dt limits, [2] error, [3] dt error, [4] x / y work counters (2 x u32)
+  unsigned long long* slots = nullptr;
   hydro_gpu_error last{};
   int seg_x = 0, seg_y = 0, block = 128;
   hb::Geometry geo{};
@@ -51,6 +52,8 @@ namespace {
 
 constexpr int kSlotErr = 2;
 constexpr int kSlotDtErr = 3;
+constexpr int kSlotCounters = 4;
+constexpr int kSlots = 5;
 
 const char* kFieldName[3] = {"rho", "pres", "internal energy"};
 
@@ -166,6 +169,8 @@ hb::SweepArgs sweep_args(hydro_gpu_ctx* c, int axis, int step) {
   a.limit_out = c->slots + ((step + 1) & 1);
   a.err = c->slots + kSlotErr;
   a.dt_err = c->slots + kSlotDtErr;
+  a.counter = reinterpret_cast<unsigned*>(c->slots + kSlotCounters) + axis;
+  a.counter_next = reinterpret_cast<unsigned*>(c->slots + kSlotCounters) + (1 - axis);
   a.step = step;
   if (axis == 0) {
     a.src = c->A;
@@ -244,6 +249,7 @@ void enqueue_finish(hydro_gpu_ctx* c) {
 
 int reset_slots(hydro_gpu_ctx* c) {
   CUDA_TRY(c, cudaMemsetAsync(c->slots, 0xff, 4 * sizeof(unsigned long long), c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->slots + kSlotCounters, 0, sizeof(unsigned long long), c->stream));
   return 0;
 }
 
@@ -343,7 +349,7 @@ int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out) {
   const size_t bytes = ctx->count * sizeof(double);
   if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&ctx->A, bytes) != cudaSuccess || cudaMalloc(&ctx->B, bytes) != cudaSuccess ||
-      cudaMalloc(&ctx->slots, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+      cudaMalloc(&ctx->slots, kSlots * sizeof(unsigned long long)) != cudaSuccess) {
     hydro_gpu_destroy(ctx);
     cudaGetLastError();
     return HYDRO_GPU_ERR_CUDA;
@@ -358,6 +364,7 @@ int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out) {
   cudaMemsetAsync(ctx->A, 0, bytes, ctx->stream);
   cudaMemsetAsync(ctx->B, 0, bytes, ctx->stream);
   cudaMemsetAsync(ctx->slots, 0xff, 4 * sizeof(unsigned long long), ctx->stream);
+  cudaMemsetAsync(ctx->slots + kSlotCounters, 0, sizeof(unsigned long long), ctx->stream);
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
     hydro_gpu_destroy(ctx);
     return HYDRO_GPU_ERR_CUDA;

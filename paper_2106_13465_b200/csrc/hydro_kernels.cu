@@ -57,7 +57,7 @@ struct Window {
 struct StepOut {
   Prim wC;          // primitive of the incoming cell c+1
   int fC;           // its positivity failure (-1 none)
-  Face fr;          // right face of cell c
+  Face fl, fr;      // faces of cell c
   Flux F;           // flux through interface c-1 | c
   Cons un;          // cell c-1 after the conservative update
   int fU;
@@ -65,18 +65,45 @@ struct StepOut {
   int fD;
 };
 
-template <bool WANT_DT, class M>
+// One walker iteration at cell c.  STAGE 0: primitive + faces only (the
+// first halo iteration); STAGE 1: + flux (second halo iteration);
+// STAGE 2: + conservative update (+ dt limit).
+template <int STAGE, bool WANT_DT, class M>
 __device__ __forceinline__ void step_cell(M& m, const Window& w, const Cons& uC, double half,
                                           double dtdx, double spacing, const Gas& g,
                                           StepOut& o) {
   o.fC = to_prim(m, uC, g, o.wC);
-  Face fl;
-  predict_faces(m, w.wA, w.wB, o.wC, half, g, fl, o.fr);
-  o.F = hllc(m, w.frPrev, fl, g);
-  o.un = w.uA;
-  Recip rn;
-  o.fU = update_cell(m, o.un, w.fluxPrev, o.F, dtdx, rn);
-  if (WANT_DT) o.fD = dt_limit(m, o.un, rn, spacing, g, o.lim);
+  predict_faces(m, w.wA, w.wB, o.wC, half, g, o.fl, o.fr);
+  if (STAGE >= 1) o.F = hllc(m, w.frPrev, o.fl, g);
+  if (STAGE >= 2) {
+    o.un = w.uA;
+    Recip rn;
+    o.fU = update_cell(m, o.un, w.fluxPrev, o.F, dtdx, rn);
+    if (WANT_DT) o.fD = dt_limit(m, o.un, rn, spacing, g, o.lim);
+  }
+}
+
+// FastMath first; if any fast path left its proven range, redo the cell
+// with the compiler's IEEE operations.
+template <int STAGE, bool WANT_DT>
+__device__ __forceinline__ void step_any(const Window& w, const Cons& uC, double half,
+                                         double dtdx, double spacing, const Gas& g, StepOut& o) {
+  FastMath fm;
+  step_cell<STAGE, WANT_DT>(fm, w, uC, half, dtdx, spacing, g, o);
+  if (!fm.ok) {
+    ExactMath em;
+    step_cell<STAGE, WANT_DT>(em, w, uC, half, dtdx, spacing, g, o);
+  }
+}
+
+__device__ __forceinline__ int prim_any(const Cons& u, const Gas& g, Prim& w) {
+  FastMath fm;
+  int f = to_prim(fm, u, g, w);
+  if (!fm.ok) {
+    ExactMath em;
+    f = to_prim(em, u, g, w);
+  }
+  return f;
 }
 
 __device__ __forceinline__ void record(unsigned long long* err, unsigned long long key) {
@@ -88,6 +115,8 @@ __device__ __forceinline__ void record(unsigned long long* err, unsigned long lo
 // k = ka-2 .. kb+2 in order), sink(k, out) receives updated cells ka..kb,
 // src.boundary(c) is called after every iteration (chunk bookkeeping).
 // kg converts a local strip cell to the global index used in error keys.
+// The two halo iterations are peeled, so a segment costs its cells plus
+// two primitive conversions, two face reconstructions and one flux.
 template <bool WANT_DT, class Src, class Sink>
 __device__ __forceinline__ void walk_strip(int ka, int kb, Src& src, Sink& sink, const Gas& g,
                                            double dtdx, double spacing, bool active,
@@ -95,37 +124,47 @@ __device__ __forceinline__ void walk_strip(int ka, int kb, Src& src, Sink& sink,
                                            unsigned long long key_base, int kg) {
   const double half = 0.5 * dtdx;
   Window w;
-  {
-    ExactMath em;
-    w.uA = src.load(ka - 2);
-    int f = to_prim(em, w.uA, g, w.wA);
-    if (active && f >= 0) record(err, key_base | ((unsigned long long)(ka - 2 + kg) << 2) | f);
-    w.uB = src.load(ka - 1);
-    f = to_prim(em, w.uB, g, w.wB);
-    if (active && f >= 0) record(err, key_base | ((unsigned long long)(ka - 1 + kg) << 2) | f);
-    // placeholders for the first two iterations, whose flux/update are
-    // discarded: a physical state keeps them on the fast path
-    w.frPrev.w = w.wA;
-    w.frPrev.rr = em.recip(w.wA.r);
-    w.fluxPrev = {0.0, 0.0, 0.0, 0.0};
+  w.uA = src.load(ka - 2);
+  int f = prim_any(w.uA, g, w.wA);
+  if (active && f >= 0) record(err, key_base | ((unsigned long long)(ka - 2 + kg) << 2) | f);
+  w.uB = src.load(ka - 1);
+  f = prim_any(w.uB, g, w.wB);
+  if (active && f >= 0) record(err, key_base | ((unsigned long long)(ka - 1 + kg) << 2) | f);
+  {  // c = ka-1: faces of the first halo cell
+    const Cons uC = src.load(ka);
+    StepOut o;
+    step_any<0, false>(w, uC, half, dtdx, spacing, g, o);
+    if (active && o.fC >= 0) record(err, key_base | ((unsigned long long)(ka + kg) << 2) | o.fC);
+    src.boundary(ka - 1);
+    w.wA = w.wB;
+    w.wB = o.wC;
+    w.uA = w.uB;
+    w.uB = uC;
+    w.frPrev = o.fr;
+  }
+  {  // c = ka: faces of cell ka and the flux through its left interface
+    const Cons uC = src.load(ka + 1);
+    StepOut o;
+    step_any<1, false>(w, uC, half, dtdx, spacing, g, o);
+    if (active && o.fC >= 0) record(err, key_base | ((unsigned long long)(ka + 1 + kg) << 2) | o.fC);
+    src.boundary(ka);
+    w.wA = w.wB;
+    w.wB = o.wC;
+    w.uA = w.uB;
+    w.uB = uC;
+    w.frPrev = o.fr;
+    w.fluxPrev = o.F;
   }
 #pragma unroll 1
-  for (int c = ka - 1; c <= kb + 1; ++c) {
+  for (int c = ka + 1; c <= kb + 1; ++c) {
     const Cons uC = src.load(c + 1);
     StepOut o;
-    FastMath fm;
-    step_cell<WANT_DT>(fm, w, uC, half, dtdx, spacing, g, o);
-    if (!fm.ok) {  // some fast path left its proven range: redo the cell exactly
-      ExactMath em;
-      step_cell<WANT_DT>(em, w, uC, half, dtdx, spacing, g, o);
-    }
+    step_any<2, WANT_DT>(w, uC, half, dtdx, spacing, g, o);
     if (active && o.fC >= 0)
       record(err, key_base | ((unsigned long long)(c + 1 + kg) << 2) | o.fC);
-    if (c > ka) {
-      if (active && o.fU >= 0)
-        record(err, key_base | (1ull << 20) | ((unsigned long long)(c - 1 + kg) << 2) | o.fU);
-      sink(c - 1, o);
-    }
+    if (active && o.fU >= 0)
+      record(err, key_base | (1ull << 20) | ((unsigned long long)(c - 1 + kg) << 2) | o.fU);
+    sink(c - 1, o);
     src.boundary(c);
     w.wA = w.wB;
     w.wB = o.wC;
@@ -144,8 +183,29 @@ __device__ __forceinline__ double step_dt(const SweepArgs& a) {
   return a.explicit_dt ? a.dt_value : a.cfl * __longlong_as_double((long long)*a.limit_in);
 }
 
+// Work distribution: a sweep is split into items of 32 strips x one segment
+// of a.seg cells; the persistent warps of the launch claim items from an
+// atomic counter (item = segment * groups + group, so neighbouring warps
+// work on neighbouring strips).  Cells whose faces differ cost several times
+// cells in uniform flow (HLLC vs the equal-state shortcut, :70-73), so
+// dynamic claiming keeps all SMs busy when the active region is localised
+// (shock tubes, blasts).  Each sweep resets the other sweep's counter for
+// the next launch on the stream.
+__device__ __forceinline__ int claim(unsigned* counter) {
+  int item = 0;
+  if ((threadIdx.x & 31) == 0) item = (int)atomicAdd(counter, 1u);
+  return __shfl_sync(0xffffffffu, item, 0);
+}
+
+#ifndef HB_X_MINB
+#define HB_X_MINB 4
+#endif
+#ifndef HB_Y_MINB
+#define HB_Y_MINB 4
+#endif
+
 // ---------------------------------------------------------------------------
-// Column sweep: thread = column j, segment of rows.
+// Column sweep: lane = column j, item = 32 columns x a segment of rows.
 
 struct ColumnSource {
   const double* __restrict__ p;  // next row to fetch (cell k = row k-1)
@@ -166,64 +226,65 @@ struct ColumnSource {
   __device__ __forceinline__ void boundary(int) {}
 };
 
-#ifndef HB_X_MINB
-#define HB_X_MINB 4
-#endif
-#ifndef HB_Y_MINB
-#define HB_Y_MINB 8
-#endif
-
 __global__ void __launch_bounds__(128, HB_X_MINB) sweep_x_kernel(SweepArgs a) {
-  const int jt = 1 + blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = jt <= a.ny;
-  const int j = active ? jt : a.ny;  // idle lanes shadow the last column, writes masked
   if (latched(a)) return;
+  const int lane = threadIdx.x & 31;
   if (*(volatile unsigned long long*)a.dt_err != kNoError) {
     // compute_dt of this step failed (detected by the previous row sweep).
-    if (active) record(a.err, *(volatile unsigned long long*)a.dt_err);
+    if (blockIdx.x == 0 && threadIdx.x == 0) record(a.err, *(volatile unsigned long long*)a.dt_err);
     return;
   }
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && a.limit_out)
-    *a.limit_out = kEmptyLimit;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (a.limit_out) *a.limit_out = kEmptyLimit;
+    *a.counter_next = 0u;
+  }
   const Gas g = make_gas(a.gamma);
   const double dtdx = step_dt(a) / a.dx;
-  const int i_lo = 1 + blockIdx.y * a.seg;
-  const int i_hi = min(a.nx, i_lo + a.seg - 1);
   const size_t pitch = a.pitch;
-  ColumnSource src{a.src + cell_index(pitch, 0, i_lo - 2, j), pitch, {}};
-  // the prefetch reads one row past the stencil (row nx+3 at most: a
-  // padding row of the allocation)
-  src.start();
-  double* __restrict__ dst = a.dst;
   const int ny = a.ny;
   const bool refl = a.bc == 0;
-  auto put = [&](double* q, const Cons& u, bool neg) {
-    q[0] = u.r;
-    q[pitch] = u.ma;
-    q[2 * pitch] = neg ? -u.mb : u.mb;
-    q[3 * pitch] = u.e;
-  };
-  double* out = dst + cell_index(pitch, 0, i_lo, j);
-  auto sink = [&](int, const StepOut& o) {
-    if (active) {
-      put(out, o.un, false);
-      // y-wall ghosts of the column-sweep output (grid.cpp:44-59)
-      if (refl) {
-        if (j <= 2) put(out + (1 - 2 * j), o.un, true);
-        if (j >= ny - 1) put(out + (2 * ny + 1 - 2 * j), o.un, true);
-      } else {
-        if (j == 1) { put(out - 1, o.un, false); put(out - 2, o.un, false); }
-        if (j == ny) { put(out + 1, o.un, false); put(out + 2, o.un, false); }
+  const int groups = (ny + 31) >> 5;
+  const int items = groups * a.nseg;
+  double* __restrict__ dst = a.dst;
+  for (int item = claim(a.counter); item < items; item = claim(a.counter)) {
+    const int grp = item % groups, sg = item / groups;
+    const int jt = (grp << 5) + lane + 1;
+    const bool active = jt <= ny;
+    const int j = active ? jt : ny;  // idle lanes shadow the last column, writes masked
+    const int i_lo = 1 + sg * a.seg;
+    const int i_hi = min(a.nx, i_lo + a.seg - 1);
+    // the prefetch reads one row past the stencil (row nx+3 at most: a
+    // padding row of the allocation)
+    ColumnSource src{a.src + cell_index(pitch, 0, i_lo - 2, j), pitch, {}};
+    src.start();
+    double* out = dst + cell_index(pitch, 0, i_lo, j);
+    auto put = [&](double* q, const Cons& u, bool neg) {
+      q[0] = u.r;
+      q[pitch] = u.ma;
+      q[2 * pitch] = neg ? -u.mb : u.mb;
+      q[3 * pitch] = u.e;
+    };
+    auto sink = [&](int, const StepOut& o) {
+      if (active) {
+        put(out, o.un, false);
+        // y-wall ghosts of the column-sweep output (grid.cpp:44-59)
+        if (refl) {
+          if (j <= 2) put(out + (1 - 2 * j), o.un, true);
+          if (j >= ny - 1) put(out + (2 * ny + 1 - 2 * j), o.un, true);
+        } else {
+          if (j == 1) { put(out - 1, o.un, false); put(out - 2, o.un, false); }
+          if (j == ny) { put(out + 1, o.un, false); put(out + 2, o.un, false); }
+        }
       }
-    }
-    out += 4 * pitch;
-  };
-  const unsigned long long base = error_key(a.step, 1, j, 0, 0, 0);
-  walk_strip<false>(i_lo + 1, i_hi + 1, src, sink, g, dtdx, 0.0, active, a.err, base, a.row0);
+      out += 4 * pitch;
+    };
+    const unsigned long long base = error_key(a.step, 1, j, 0, 0, 0);
+    walk_strip<false>(i_lo + 1, i_hi + 1, src, sink, g, dtdx, 0.0, active, a.err, base, a.row0);
+  }
 }
 
 // ---------------------------------------------------------------------------
-// Row sweep with TMA-staged tiles.
+// Row sweep with TMA-staged tiles, one independent pipeline per warp.
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -277,15 +338,16 @@ __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// Row-sweep staging: a CTA of kRowsPerCta threads (one row each) walks a
-// column segment in chunks of kChunk columns.  Chunk Q holds strip cells
-// [ka-4+4Q, ka-1+4Q] of all four variables, laid out [v][row][col] (one TMA
-// box {kChunk cols, 1 var, kRowsPerCta rows} per variable, 32-byte rows =
-// whole DRAM sectors).  A ring of kNBuf buffers is used in place: once a
-// cell has been read into registers its slot receives the updated cell
-// (2 iterations later), and a completed chunk leaves with TMA bulk-tensor
-// stores before its buffer is refilled kNBuf-1 chunks ahead.
-constexpr int kVarBytes = kRowsPerCta * kChunk * 8;
+// Row-sweep staging: a warp (one row per lane) walks a column segment in
+// chunks of kChunk columns.  Chunk Q holds strip cells [ka-4+4Q, ka-1+4Q]
+// of all four variables, laid out [v][row][col] (one TMA box {kChunk cols,
+// 1 var, 32 rows} per variable; 32-byte rows = whole DRAM sectors).  A ring
+// of kNBuf buffers is used in place: once a cell has been read into
+// registers its slot receives the updated cell (2 iterations later), and a
+// completed chunk leaves with TMA bulk-tensor stores before its buffer is
+// refilled kNBuf-1 chunks ahead.  Chunk numbering runs on across the warp's
+// items so buffer/phase bookkeeping never resets.
+constexpr int kVarBytes = 32 * kChunk * 8;
 __device__ __forceinline__ uint32_t slot(int r, int v, int c) {
   return (uint32_t)(v * kVarBytes + r * (kChunk * 8) + c * 8);
 }
@@ -293,38 +355,39 @@ __device__ __forceinline__ uint32_t slot(int r, int v, int c) {
 struct RowTiles {
   const CUtensorMap* load_map;
   const CUtensorMap* store_map;
-  uint8_t* base;        // kNBuf consecutive kChunkBytes buffers
-  uint64_t* full;       // kNBuf mbarriers
-  int row;              // this thread's row within the CTA tile
-  int i0;               // first grid row of the CTA tile
+  uint8_t* base;        // kNBuf consecutive kChunkBytes buffers of this warp
+  uint64_t* full;       // kNBuf mbarriers of this warp
+  int lane;
+  int i0;               // first grid row of the item
   int ka, kb;           // output strip cells
-  int nq;               // chunks needed (cells ka-4 .. kb+2)
-  int ready;            // highest chunk this thread has waited for
-  bool leader;
+  int nq;               // chunks of this item (cells ka-4 .. kb+2)
+  unsigned q0;          // running chunk number of this item's chunk 0
+  int ready;            // highest local chunk this lane has waited for
   bool active;
 
-  __device__ __forceinline__ uint8_t* buf(int q) { return base + (q % kNBuf) * kChunkBytes; }
+  __device__ __forceinline__ uint8_t* buf(int q) { return base + ((q0 + q) % kNBuf) * kChunkBytes; }
+  __device__ __forceinline__ uint64_t* bar(int q) { return &full[(q0 + q) % kNBuf]; }
 
-  __device__ __forceinline__ void issue(int q) {
+  __device__ __forceinline__ void issue(int q) {  // lane 0 only
     if (q >= nq) return;
-    mbar_expect_tx(&full[q % kNBuf], kChunkBytes);
+    mbar_expect_tx(bar(q), kChunkBytes);
     // strip cell k is column k-1, stored at column offset k-1+kColOff
     const int col = ka - 4 + q * kChunk - 1 + kColOff;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) tma_load(buf(q) + v * kVarBytes, load_map, &full[q % kNBuf], col, v, i0 + 1);
+    for (int v = 0; v < 4; ++v) tma_load(buf(q) + v * kVarBytes, load_map, bar(q), col, v, i0 + 1);
   }
 
   __device__ __forceinline__ Cons load(int k) {
     const int rel = k - ka + 4;
     const int q = rel / kChunk, pos = rel % kChunk;
     if (q > ready) {
-      mbar_wait(&full[q % kNBuf], (q / kNBuf) & 1);
+      mbar_wait(bar(q), ((q0 + q) / kNBuf) & 1);
       ready = q;
     }
     const uint8_t* b = buf(q);
     // sweep orientation: mom_a = mom_y (variable 2), mom_b = mom_x
-    Cons u = {*(const double*)(b + slot(row, 0, pos)), *(const double*)(b + slot(row, 2, pos)),
-              *(const double*)(b + slot(row, 1, pos)), *(const double*)(b + slot(row, 3, pos))};
+    Cons u = {*(const double*)(b + slot(lane, 0, pos)), *(const double*)(b + slot(lane, 2, pos)),
+              *(const double*)(b + slot(lane, 1, pos)), *(const double*)(b + slot(lane, 3, pos))};
     if (!active) u = {1.0, 0.0, 0.0, 1.0};  // rows past the grid: inert
     return u;
   }
@@ -333,10 +396,10 @@ struct RowTiles {
     const int rel = k - ka + 4;
     uint8_t* b = buf(rel / kChunk);
     const int pos = rel % kChunk;
-    *(double*)(b + slot(row, 0, pos)) = u.r;
-    *(double*)(b + slot(row, 2, pos)) = u.ma;
-    *(double*)(b + slot(row, 1, pos)) = u.mb;
-    *(double*)(b + slot(row, 3, pos)) = u.e;
+    *(double*)(b + slot(lane, 0, pos)) = u.r;
+    *(double*)(b + slot(lane, 2, pos)) = u.ma;
+    *(double*)(b + slot(lane, 1, pos)) = u.mb;
+    *(double*)(b + slot(lane, 3, pos)) = u.e;
   }
 
   // After iteration c: chunk boundaries fall on c - ka = 4T.
@@ -349,10 +412,10 @@ struct RowTiles {
   // Chunk T's outputs are complete: store it, refill the buffer of chunk
   // T-1 (stored at the previous boundary) with chunk T+kNBuf-1.
   __device__ __forceinline__ void flush(int T) {
-    if (leader) bulk_wait_read0();  // chunk T-1's stores have left smem
-    fence_async_smem();             // this thread's slot writes -> async proxy
-    __syncthreads();
-    if (leader) {
+    if (lane == 0) bulk_wait_read0();  // chunk T-1's stores have left smem
+    fence_async_smem();                // this lane's slot writes -> async proxy
+    __syncwarp();
+    if (lane == 0) {
       if (T >= 1) {
         const int col = ka - 4 + T * kChunk - 1 + kColOff;
 #pragma unroll
@@ -364,90 +427,102 @@ struct RowTiles {
   }
 };
 
-__global__ void __launch_bounds__(kRowsPerCta, HB_Y_MINB) sweep_y_kernel(SweepArgs a,
+__global__ void __launch_bounds__(128, HB_Y_MINB) sweep_y_kernel(SweepArgs a,
                                                        const __grid_constant__ CUtensorMap load_map,
                                                        const __grid_constant__ CUtensorMap store_map) {
   extern __shared__ uint8_t smem_raw[];
   if (latched(a)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.counter_next = 0u;
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
-  const int i0 = 1 + blockIdx.x * kRowsPerCta;
-  const int i = i0 + threadIdx.x;
-  const bool active = i <= a.nx;
-  const Gas g = make_gas(a.gamma);
-  const double dtdx = step_dt(a) / a.dx;
-  const int j_lo = 1 + blockIdx.y * a.seg;
-  const int j_hi = min(a.ny, j_lo + a.seg - 1);
-
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   RowTiles t;
   t.load_map = &load_map;
   t.store_map = &store_map;
-  t.base = smem;
-  t.full = (uint64_t*)(smem + kNBuf * kChunkBytes);
-  t.row = threadIdx.x;
-  t.i0 = i0;
-  t.ka = j_lo + 1;
-  t.kb = j_hi + 1;
-  t.nq = (t.kb + 2 - (t.ka - 4) + kChunk) / kChunk;
-  t.ready = -1;
-  t.leader = threadIdx.x == 0;
-  t.active = active;
-  if (t.leader) {
+  t.base = smem + warp * (kNBuf * kChunkBytes);
+  t.full = (uint64_t*)(smem + 4 * kNBuf * kChunkBytes) + warp * kNBuf;
+  t.lane = lane;
+  t.q0 = 0;
+  if (lane == 0) {
     for (int q = 0; q < kNBuf; ++q) mbar_init(&t.full[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int q = 0; q < kNBuf - 1; ++q) t.issue(q);
   }
-  __syncthreads();
+  __syncwarp();
 
+  const Gas g = make_gas(a.gamma);
+  const double dtdx = step_dt(a) / a.dx;
   const size_t pitch = a.pitch;
   const int nx = a.nx;
   const bool refl = a.bc == 0;
-  const bool mirror_lo = active && a.wall_lo && i <= 2;
-  const bool mirror_hi = active && a.wall_hi && i >= nx - 1;
+  const int groups = (nx + 31) >> 5;
+  const int items = groups * a.nseg;
   double* __restrict__ dst = a.dst;
   double lim_min = __longlong_as_double(0x7ff0000000000000ll);
   unsigned long long dt_key = kNoError;
-  const int gi = a.row0 + i;
-  auto put_row = [&](int ii, int j, const Cons& u, bool neg) {
-    double* q = dst + cell_index(pitch, 0, ii, j);
-    q[0] = u.r;
-    q[2 * pitch] = u.ma;
-    q[pitch] = neg ? -u.mb : u.mb;
-    q[3 * pitch] = u.e;
-  };
-  auto sink = [&](int k, const StepOut& o) {
-    t.put(k, o.un);
-    if (!active) return;
-    const int j = k - 1;
-    if (mirror_lo) {  // x-wall ghosts for the next column sweep (grid.cpp:26-42)
-      if (refl) put_row(1 - i, j, o.un, true);
-      else if (i == 1) { put_row(0, j, o.un, false); put_row(-1, j, o.un, false); }
-    }
-    if (mirror_hi) {
-      if (refl) put_row(2 * nx + 1 - i, j, o.un, true);
-      else if (i == nx) { put_row(nx + 1, j, o.un, false); put_row(nx + 2, j, o.un, false); }
-    }
-    if (a.want_limit) {
-      if (o.fD >= 0) {
-        const unsigned long long key = error_key(a.step + 1, 0, gi, 0, j, o.fD);
-        dt_key = key < dt_key ? key : dt_key;
-      } else {
-        lim_min = smin(lim_min, o.lim);
+
+  for (int item = claim(a.counter); item < items; item = claim(a.counter)) {
+    const int grp = item % groups, sg = item / groups;
+    const int i0 = (grp << 5) + 1;
+    const int i = i0 + lane;
+    const bool active = i <= nx;
+    const int j_lo = 1 + sg * a.seg;
+    const int j_hi = min(a.ny, j_lo + a.seg - 1);
+    t.i0 = i0;
+    t.ka = j_lo + 1;
+    t.kb = j_hi + 1;
+    t.nq = (t.kb + 2 - (t.ka - 4) + kChunk) / kChunk;
+    t.ready = -1;
+    t.active = active;
+    if (lane == 0)
+      for (int q = 0; q < kNBuf - 1; ++q) t.issue(q);
+
+    const bool mirror_lo = active && a.wall_lo && i <= 2;
+    const bool mirror_hi = active && a.wall_hi && i >= nx - 1;
+    const int gi = a.row0 + i;
+    auto put_row = [&](int ii, int j, const Cons& u, bool neg) {
+      double* q = dst + cell_index(pitch, 0, ii, j);
+      q[0] = u.r;
+      q[2 * pitch] = u.ma;
+      q[pitch] = neg ? -u.mb : u.mb;
+      q[3 * pitch] = u.e;
+    };
+    auto sink = [&](int k, const StepOut& o) {
+      t.put(k, o.un);
+      if (!active) return;
+      const int j = k - 1;
+      if (mirror_lo) {  // x-wall ghosts for the next column sweep (grid.cpp:26-42)
+        if (refl) put_row(1 - i, j, o.un, true);
+        else if (i == 1) { put_row(0, j, o.un, false); put_row(-1, j, o.un, false); }
       }
-    }
-  };
-  const unsigned long long base = error_key(a.step, 2, gi, 0, 0, 0);
-  if (a.want_limit)
-    walk_strip<true>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, active, a.err, base, 0);
-  else
-    walk_strip<false>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, active, a.err, base, 0);
-  // a final segment shorter than whole chunks leaves one chunk unstored
-  const int seg = t.kb + 1 - t.ka;
-  if (seg % kChunk != 0) t.flush(seg / kChunk + 1);
-  if (t.leader) bulk_wait0();
+      if (mirror_hi) {
+        if (refl) put_row(2 * nx + 1 - i, j, o.un, true);
+        else if (i == nx) { put_row(nx + 1, j, o.un, false); put_row(nx + 2, j, o.un, false); }
+      }
+      if (a.want_limit) {
+        if (o.fD >= 0) {
+          const unsigned long long key = error_key(a.step + 1, 0, gi, 0, j, o.fD);
+          dt_key = key < dt_key ? key : dt_key;
+        } else {
+          lim_min = smin(lim_min, o.lim);
+        }
+      }
+    };
+    const unsigned long long base = error_key(a.step, 2, gi, 0, 0, 0);
+    if (a.want_limit)
+      walk_strip<true>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, active, a.err, base, 0);
+    else
+      walk_strip<false>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, active, a.err, base, 0);
+    // a final segment shorter than whole chunks leaves one chunk unstored
+    const int seg = t.kb + 1 - t.ka;
+    if (seg % kChunk != 0) t.flush(seg / kChunk + 1);
+    if (lane == 0) bulk_wait_read0();  // the ring is free for the next item
+    __syncwarp();
+    t.q0 += t.nq;
+  }
+  if (lane == 0) bulk_wait0();
   if (a.want_limit) {
     const unsigned long long m = warp_min_u64((unsigned long long)__double_as_longlong(lim_min));
     const unsigned long long e = warp_min_u64(dt_key);
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
       atomicMin(a.limit_out, m);
       if (e != kNoError) atomicMin(a.dt_err, e);
     }
@@ -627,15 +702,18 @@ __global__ void math_selftest_kernel(int op, const double* a, const double* b, d
   okv[t] = fm.ok ? 1 : 0;
 }
 
-// Segments per strip: about one wave of resident CTAs; a multiple of
-// kChunk cells per segment where the row sweep needs it.
-int pick_segments(int n, int strip_blocks, int ctas_per_wave, int align) {
-  long long nseg = ctas_per_wave / (strip_blocks > 0 ? strip_blocks : 1);
-  if (nseg < 1) nseg = 1;
-  const long long max_seg = (n + 15) / 16;  // keep segments >= 16 cells
-  if (nseg > max_seg) nseg = max_seg;
-  if (nseg < 1) nseg = 1;
-  return (int)nseg;
+// Segment length for the persistent sweeps: about kItemsPerWarp work items
+// per resident warp (dynamic balance), 16..128 cells, whole row-sweep chunks.
+constexpr int kItemsPerWarp = 8;
+int pick_seg(int n, int strips, int warps) {
+  const long long groups = (strips + 31) / 32;
+  long long segs = (long long)warps * kItemsPerWarp / (groups > 0 ? groups : 1);
+  if (segs < 1) segs = 1;
+  long long seg = (n + segs - 1) / segs;
+  if (seg < 16) seg = 16;
+  if (seg > 128) seg = 128;
+  seg = (seg + kChunk - 1) / kChunk * kChunk;
+  return (int)seg;
 }
 
 }  // namespace
@@ -647,7 +725,7 @@ int query_geometry(Geometry* g) {
   cudaFuncSetAttribute(sweep_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
   int ox = 0, oy = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, sweep_x_kernel, 128, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy, sweep_y_kernel, kRowsPerCta, kYSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy, sweep_y_kernel, 128, kYSmemBytes);
   g->ctas_x_per_sm = ox > 0 ? ox : 1;
   g->ctas_y_per_sm = oy > 0 ? oy : 1;
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
@@ -665,7 +743,7 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
     encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
   }
   const cuuint64_t strides[2] = {pitch * 8, 4 * pitch * 8};
-  const cuuint32_t box[3] = {(cuuint32_t)kChunk, 1, (cuuint32_t)kRowsPerCta};
+  const cuuint32_t box[3] = {(cuuint32_t)kChunk, 1, 32};
   const cuuint32_t estr[3] = {1, 1, 1};
   // load: all of U_b (ghost rows/columns included)
   const cuuint64_t dim_load[3] = {pitch, 4, (cuuint64_t)nx + 4};
@@ -683,27 +761,20 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
 
 void launch_sweep_x(const SweepArgs& a0, const Geometry& geo, cudaStream_t s) {
   SweepArgs a = a0;
-  const int blocks = (a.ny + 127) / 128;
-  int nseg = a.seg > 0 ? (a.nx + a.seg - 1) / a.seg
-                       : pick_segments(a.nx, blocks, geo.sms * geo.ctas_x_per_sm, 1);
-  a.seg = (a.nx + nseg - 1) / nseg;
-  nseg = (a.nx + a.seg - 1) / a.seg;
-  a.nseg = nseg;
-  sweep_x_kernel<<<dim3(blocks, nseg), 128, 0, s>>>(a);
+  const int ctas = geo.sms * geo.ctas_x_per_sm;
+  if (a.seg <= 0) a.seg = pick_seg(a.nx, a.ny, ctas * 4);
+  a.nseg = (a.nx + a.seg - 1) / a.seg;
+  sweep_x_kernel<<<ctas, 128, 0, s>>>(a);
 }
 
 void launch_sweep_y(const SweepArgs& a0, const TmaMaps& maps, const Geometry& geo,
                     cudaStream_t s) {
   SweepArgs a = a0;
-  const int blocks = (a.nx + kRowsPerCta - 1) / kRowsPerCta;
-  int nseg = a.seg > 0 ? (a.ny + a.seg - 1) / a.seg
-                       : pick_segments(a.ny, blocks, geo.sms * geo.ctas_y_per_sm, kChunk);
-  int seg = (a.ny + nseg - 1) / nseg;
-  seg = (seg + kChunk - 1) / kChunk * kChunk;  // whole output chunks per segment
-  a.seg = seg;
-  a.nseg = (a.ny + seg - 1) / seg;
-  sweep_y_kernel<<<dim3(blocks, a.nseg), kRowsPerCta, kYSmemBytes, s>>>(a, maps.y_load,
-                                                                        maps.y_store);
+  const int ctas = geo.sms * geo.ctas_y_per_sm;
+  if (a.seg <= 0) a.seg = pick_seg(a.ny, a.nx, ctas * 4);
+  a.seg = (a.seg + kChunk - 1) / kChunk * kChunk;  // chunks never straddle segments
+  a.nseg = (a.ny + a.seg - 1) / a.seg;
+  sweep_y_kernel<<<ctas, 128, kYSmemBytes, s>>>(a, maps.y_load, maps.y_store);
 }
 
 void launch_prologue(const PrologueArgs& a, cudaStream_t s) {

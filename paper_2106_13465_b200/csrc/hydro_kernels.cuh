@@ -18,13 +18,12 @@ namespace hb {
 // doubles -- a slab halo is a single contiguous send/recv.
 constexpr int kColOff = 3;
 
-// Row-sweep tiling: a CTA owns kRowsPerCta rows; TMA stages kChunk columns
-// of all four variables per chunk into a ring of kNBuf buffers.
-constexpr int kRowsPerCta = 64;
+// Row-sweep tiling: every warp stages kChunk columns x 32 rows x 4 variables
+// per chunk into its own ring of kNBuf buffers (4 warps per CTA).
 constexpr int kChunk = 4;
 constexpr int kNBuf = 3;
-constexpr int kChunkBytes = kRowsPerCta * 4 * kChunk * 8;  // 8 KB
-constexpr int kYSmemBytes = kNBuf * kChunkBytes + 128 + 8 * kNBuf;  // + alignment, mbarriers
+constexpr int kChunkBytes = 32 * 4 * kChunk * 8;                         // 4 KB
+constexpr int kYSmemBytes = 4 * kNBuf * kChunkBytes + 128 + 4 * kNBuf * 8;  // + align, mbarriers
 
 __host__ __device__ __forceinline__ size_t cell_index(size_t pitch, int v, int i, int j) {
   return ((size_t)(i + 1) * 4 + (size_t)v) * pitch + (size_t)(j + kColOff);
@@ -56,10 +55,12 @@ struct SweepArgs {
   int explicit_dt;            // 1: use dt_value instead of cfl*limit_in
   double dt_value;
   int want_limit;             // row sweep: produce limit_out
+  unsigned* counter;          // work-item counter of this sweep (starts at 0)
+  unsigned* counter_next;     // the other sweep's counter, reset for its launch
 };
 
 struct TmaMaps {
-  CUtensorMap y_load;         // U_b, box {kChunk cols, 1 var, kRowsPerCta rows}
+  CUtensorMap y_load;         // U_b, box {kChunk cols, 1 var, 32 rows}
   CUtensorMap y_store;        // U_a interior rows/cols only (clips ghosts)
 };
 

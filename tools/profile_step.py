@@ -19,12 +19,13 @@ ap.add_argument("--case", default="sod_x")
 ap.add_argument("--bc", default="transmit")
 ap.add_argument("--seed", type=int, default=0)
 ap.add_argument("--seg", type=int, nargs=3, default=[0, 0, 0])
+ap.add_argument("--pre", type=int, default=2, help="untimed steps before the timed ones")
 a = ap.parse_args()
 ny = a.ny or a.nx
 with P.GpuGrid(a.nx, ny, 1.0 / a.nx, 1.0 / ny, P.GasModel(), a.bc, device=0) as g:
     g.tune(*a.seg)
     g.init_case(a.case, a.seed)
-    g.run(2)  # warm-up: init, prologue, 2 x (sweep_x, sweep_y), finish
+    g.run(a.pre)  # warm-up / advance the flow: init, prologue, sweeps, finish
     g.set_timing(True)
     g.run(a.steps)
     t = g.kernel_times()
