@@ -102,33 +102,39 @@ def dist_env():
     return rank, world, local
 
 
-def cpu_reference_sample(steps_per_sample: int, threads: int):
-    """Times the reference's own CPU path (oracle/_ref coarse_grain) -- or the C
-    port if the compiled reference is absent -- on `steps_per_sample` time
-    steps of the workload.  Returns (cell-steps/s, kind, seconds)."""
+def cpu_reference_sample(steps_per_chunk: int, threads: int, min_seconds: float = 0.0):
+    """Times the reference's own CPU path (oracle/_ref coarse_grain over
+    `threads` host threads) -- or the C port if the compiled reference is
+    absent -- on chunks of `steps_per_chunk` time steps of the workload,
+    continuing the same flow until at least `min_seconds` of stepping was
+    timed.  Returns (cell-steps/s, kind, seconds, threads, steps)."""
     from oracle import oracle as O
     g = O.make_case(CASE, NX, NY)
-    if O.ref_available():
-        warm = g.copy()
-        O.ref_run(warm, 1, BC, "coarse_grain", threads)
-        secs = O.ref_run(g, steps_per_sample, BC, "coarse_grain", threads)
-        kind = "reference"
+    kind = "reference" if O.ref_available() else "port"
+    if kind == "reference":
+        O.ref_run(g.copy(), 1, BC, "coarse_grain", threads)  # warm-up (bench.cpp:112-117)
     else:
-        t0 = time.perf_counter()
-        O.run_sequential(g, steps_per_sample, BC)
-        secs = time.perf_counter() - t0
-        kind, threads = "port", 1
-    return NX * NY * steps_per_sample / secs, kind, secs, threads
+        threads = 1
+    secs, steps = 0.0, 0
+    while steps == 0 or secs < min_seconds:
+        if kind == "reference":
+            secs += O.ref_run(g, steps_per_chunk, BC, "coarse_grain", threads)
+        else:
+            t0 = time.perf_counter()
+            O.run_sequential(g, steps_per_chunk, BC)
+            secs += time.perf_counter() - t0
+        steps += steps_per_chunk
+    return NX * NY * steps / secs, kind, secs, threads, steps
 
 
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    sample_steps = 5
+    sample_steps = 20
     vals, kind = [], None
     for k in range(args.warmup + args.steps):
-        v, kind, secs, used = cpu_reference_sample(sample_steps, threads)
+        v, kind, secs, used, _ = cpu_reference_sample(sample_steps, threads)
         if k >= args.warmup:
             vals.append(v)
     value = statistics.median(vals)
@@ -292,9 +298,9 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        v, kind, secs, used = cpu_reference_sample(10, threads)
+        v, kind, secs, used, nsteps = cpu_reference_sample(10, threads, min_seconds=10.0)
         cpu = {"value": v, "unit": UNIT, "cores": used, "kind": kind,
-               "sample": f"10 time steps of the {NX}x{NY} config-1 grid ({secs:.1f}s), "
+               "sample": f"{nsteps} time steps of the {NX}x{NY} config-1 grid ({secs:.1f}s timed), "
                          f"reference coarse_grain over {used} host threads"}
 
     if rank == 0:

@@ -1,0 +1,154 @@
+// gpu_strategy.hpp -- header-only C++ adaptor that plugs libhydro_b200.so into
+// the reference hydro2d as one more execution strategy.
+//
+// It is written against the reference's own types (include it from a tree
+// that has proj/include on the include path) and the C-ABI in hydro_gpu.h:
+//
+//   reference                                        this adaptor
+//   run_sequential(Grid2D&, const GasModel&, int)    run_gpu(grid, model, steps)
+//     (proj/include/hydro/schedulers.hpp:24)
+//   advance_sequential(Grid2D&, GasModel, double)    advance_gpu(grid, model, dt)
+//     (schedulers.hpp:21)
+//   run_until(Grid2D&, const GasModel&, double)      run_until_gpu(grid, model, t_end)
+//     (schedulers.hpp:28)
+//   compute_dt(const Grid2D&, const GasModel&)       compute_dt_gpu(grid, model)
+//     (euler_kernel.hpp:75)
+//
+// Same argument meaning, same in-place mutation of the caller-owned Grid2D
+// (every plane, ghosts included, ends bitwise equal to the reference's), and
+// the same error behaviour: a positivity failure throws hydro::Error with
+// ErrorCategory::Positivity and the reference's message, e.g.
+// "step 3: column sweep strip 17: rho non-positive at strip cell -2"
+// (schedulers.cpp:23-26,80-91); configuration problems throw ConfigError; a
+// CUDA failure (no reference counterpart) throws std::runtime_error, which
+// hydrobench reports as "error: internal: ..." (tools/hydrobench.cpp:156-159).
+// See INTEGRATION.md for the run_strategy hook.
+#pragma once
+
+#include <stdexcept>
+#include <string>
+
+#include "hydro/errors.hpp"
+#include "hydro/grid.hpp"
+#include "hydro/types.hpp"
+#include "hydro_gpu.h"
+
+namespace hydro {
+
+struct GpuOptions {
+  int device = -1;                    // CUDA device; -1 = current
+  int bc = HYDRO_GPU_BC_REFLECT;      // the reference's walls; TRANSMIT for BASELINE configs
+};
+
+namespace gpu_detail {
+
+[[noreturn]] inline void raise(int status, const std::string& message) {
+  switch (status) {
+    case HYDRO_GPU_ERR_CONFIG: throw ConfigError(message);
+    case HYDRO_GPU_ERR_POSITIVITY: throw Error(ErrorCategory::Positivity, message);
+    case HYDRO_GPU_ERR_CUDA: throw std::runtime_error(message);
+    default: throw Error(static_cast<ErrorCategory>(status - 1), message);
+  }
+}
+
+// One device-resident copy of a Grid2D for the duration of a call.
+class Context {
+ public:
+  Context(const Grid2D& g, const GasModel& m, const GpuOptions& o) {
+    hydro_gpu_cfg cfg{};
+    cfg.nx = g.nx();
+    cfg.ny = g.ny();
+    cfg.dx = g.dx();
+    cfg.dy = g.dy();
+    cfg.gamma = m.gamma;
+    cfg.cfl = m.cfl;
+    cfg.bc = o.bc;
+    cfg.flux = HYDRO_GPU_FLUX_HLLC;
+    cfg.device = o.device;
+    cfg.row0 = 0;
+    cfg.global_nx = g.nx();
+    cfg.wall_lo = cfg.wall_hi = 1;
+    const int rc = hydro_gpu_create(&cfg, &ctx_);
+    if (rc != HYDRO_GPU_OK)
+      raise(rc, std::string("hydro_gpu_create: ") + hydro_gpu_status_string(rc));
+  }
+  ~Context() { hydro_gpu_destroy(ctx_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+
+  void download(Grid2D& g) {
+    double* planes[4];
+    for (int v = 0; v < kNumVars; ++v) planes[v] = &g.at(Var(v), -1, -1);
+    check(hydro_gpu_download(ctx_, planes, g.ny() + 2 * kGhost));
+  }
+  void check(int rc) {
+    if (rc == HYDRO_GPU_OK) return;
+    hydro_gpu_error e{};
+    hydro_gpu_last_error(ctx_, &e);
+    raise(rc, e.message);
+  }
+  hydro_gpu_ctx* get() { return ctx_; }
+
+ private:
+  hydro_gpu_ctx* ctx_ = nullptr;
+};
+
+// Grid2D::at(...) const returns by value; the planes are contiguous vectors,
+// so the address of cell (-1,-1) is taken through a non-const view.
+inline const double* plane(const Grid2D& g, int v) {
+  return &const_cast<Grid2D&>(g).at(Var(v), -1, -1);
+}
+
+}  // namespace gpu_detail
+
+// run_sequential on the GPU: `steps` steps of BC -> dt -> column sweep ->
+// BC -> row sweep, bitwise equal to the reference; returns the last dt.
+inline double run_gpu(Grid2D& grid, const GasModel& model, int steps,
+                      const GpuOptions& opt = {}) {
+  gpu_detail::Context ctx(grid, model, opt);
+  const double* planes[4];
+  for (int v = 0; v < kNumVars; ++v) planes[v] = gpu_detail::plane(grid, v);
+  ctx.check(hydro_gpu_upload(ctx.get(), planes, grid.ny() + 2 * kGhost));
+  double last_dt = 0.0;
+  const int rc = hydro_gpu_run(ctx.get(), steps, &last_dt);
+  ctx.download(grid);
+  ctx.check(rc);
+  return last_dt;
+}
+
+inline void advance_gpu(Grid2D& grid, const GasModel& model, double dt,
+                        const GpuOptions& opt = {}) {
+  gpu_detail::Context ctx(grid, model, opt);
+  const double* planes[4];
+  for (int v = 0; v < kNumVars; ++v) planes[v] = gpu_detail::plane(grid, v);
+  ctx.check(hydro_gpu_upload(ctx.get(), planes, grid.ny() + 2 * kGhost));
+  const int rc = hydro_gpu_advance(ctx.get(), dt);
+  ctx.download(grid);
+  ctx.check(rc);
+}
+
+inline int run_until_gpu(Grid2D& grid, const GasModel& model, double t_end,
+                         const GpuOptions& opt = {}) {
+  gpu_detail::Context ctx(grid, model, opt);
+  const double* planes[4];
+  for (int v = 0; v < kNumVars; ++v) planes[v] = gpu_detail::plane(grid, v);
+  ctx.check(hydro_gpu_upload(ctx.get(), planes, grid.ny() + 2 * kGhost));
+  int steps = 0;
+  const int rc = hydro_gpu_run_until(ctx.get(), t_end, &steps);
+  ctx.download(grid);
+  ctx.check(rc);
+  return steps;
+}
+
+inline double compute_dt_gpu(const Grid2D& grid, const GasModel& model,
+                             const GpuOptions& opt = {}) {
+  gpu_detail::Context ctx(grid, model, opt);
+  const double* planes[4];
+  for (int v = 0; v < kNumVars; ++v) planes[v] = gpu_detail::plane(grid, v);
+  ctx.check(hydro_gpu_upload(ctx.get(), planes, grid.ny() + 2 * kGhost));
+  double dt = 0.0;
+  ctx.check(hydro_gpu_compute_dt(ctx.get(), &dt));
+  return dt;
+}
+
+}  // namespace hydro

@@ -1,0 +1,67 @@
+"""The drop-in: the reference's own command surface (RunConfig, make_case,
+grid_checksum/format_checksum, error convention) with a "gpu" strategy that
+goes through include/hydro/gpu_strategy.hpp and the C-ABI
+(integration/hydrobench_gpu.cpp)."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "integration", "_build", "hydrobench_gpu")
+README_LINE = ("checksum b4593af8ee8e4e25  rho=2304 mom_x=0 mom_y=-3.4208746946262636e-15 "
+               "ener=2304.0230000000001")  # proj/README.md:98-101
+
+needs_bin = pytest.mark.skipif(not os.path.exists(BIN), reason="integration driver not built")
+
+
+def run(*args):
+    return subprocess.run([BIN, *args], capture_output=True, text=True, timeout=600)
+
+
+@needs_bin
+def test_reference_strategy_reproduces_readme_line():
+    out = run("run", "--case", "blast", "--nx", "48", "--ny", "48", "--steps", "5",
+              "--strategy", "task_graph", "--workers", "4")
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.splitlines()[1] == README_LINE
+
+
+@needs_bin
+def test_error_convention_for_bad_flags():
+    out = run("run", "--case", "nope", "--strategy", "gpu")
+    assert out.returncode == 1
+    assert out.stderr.startswith("error: config: unknown case")
+
+
+@needs_bin
+@pytest.mark.gpu
+def test_gpu_strategy_reproduces_readme_line():
+    out = run("run", "--case", "blast", "--nx", "48", "--ny", "48", "--steps", "5",
+              "--strategy", "gpu")
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.splitlines()[0].startswith("case=blast 48x48 steps=5 strategy=gpu")
+    assert out.stdout.splitlines()[1] == README_LINE
+
+
+@needs_bin
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,n,steps,strategy", [("blast", 64, 10, "coarse_grain"),
+                                                   ("sod", 128, 40, "sequential")])
+def test_gpu_strategy_equals_cpu_strategy(case, n, steps, strategy):
+    args = ["--case", case, "--nx", str(n), "--ny", str(n), "--steps", str(steps)]
+    cpu = run("run", *args, "--strategy", strategy, "--workers", "4" if strategy != "sequential" else "1")
+    gpu = run("run", *args, "--strategy", "gpu")
+    assert cpu.returncode == 0 and gpu.returncode == 0, (cpu.stderr, gpu.stderr)
+    assert cpu.stdout.splitlines()[1] == gpu.stdout.splitlines()[1]
+
+
+@needs_bin
+@pytest.mark.gpu
+def test_gpu_positivity_error_line_matches_reference():
+    args = ["--case", "blast", "--nx", "64", "--ny", "64", "--steps", "5", "--cfl", "25"]
+    cpu = run("run", *args, "--strategy", "sequential")
+    gpu = run("run", *args, "--strategy", "gpu")
+    assert cpu.returncode == gpu.returncode == 1
+    assert cpu.stderr == gpu.stderr
+    assert cpu.stderr.startswith("error: positivity: step ")
