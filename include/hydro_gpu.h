@@ -174,9 +174,10 @@ int hydro_gpu_reset_counters(hydro_gpu_ctx* ctx);
 /* Launch-geometry override (0 = default): strip segment length along the
  * column and row sweeps; block must be 0 or 128. */
 int hydro_gpu_tune(hydro_gpu_ctx* ctx, int seg_x, int seg_y, int block);
-/* Self-test of the device fp64 division (op 0) and square root (op 1)
- * fast paths against the compiler's IEEE operations on n operand pairs
- * (b ignored for sqrt).  in_range[k] = 1 where the fast path applied. */
+/* Self-test of the device fp64 division (op 0), square root (op 1) and
+ * signed-zero-safe division (op 2) fast paths against the compiler's IEEE
+ * operations on n operand pairs (b ignored for sqrt).  in_range[k] = 1 where
+ * the fast path applied. */
 int hydro_gpu_math_selftest(int op, const double* a, const double* b, double* fast,
                             double* exact, int* in_range, size_t n);
 /* Device pointer to plane-interleaved storage and its pitch (doubles). */

@@ -83,58 +83,48 @@ __device__ __forceinline__ void step_cell(M& m, const Window& w, const Cons& uC,
   }
 }
 
-// FastMath first; if any fast path left its proven range, redo the cell
-// with the compiler's IEEE operations.
-template <int STAGE, bool WANT_DT>
-__device__ __forceinline__ void step_any(const Window& w, const Cons& uC, double half,
-                                         double dtdx, double spacing, const Gas& g, StepOut& o) {
-  FastMath fm;
-  step_cell<STAGE, WANT_DT>(fm, w, uC, half, dtdx, spacing, g, o);
-  if (!fm.ok) {
-    ExactMath em;
-    step_cell<STAGE, WANT_DT>(em, w, uC, half, dtdx, spacing, g, o);
-  }
-}
-
-__device__ __forceinline__ int prim_any(const Cons& u, const Gas& g, Prim& w) {
-  FastMath fm;
-  int f = to_prim(fm, u, g, w);
-  if (!fm.ok) {
-    ExactMath em;
-    f = to_prim(em, u, g, w);
-  }
-  return f;
-}
-
 __device__ __forceinline__ void record(unsigned long long* err, unsigned long long key) {
   atomicMin(err, key);
 }
 
+struct OkKey {
+  bool ok;
+  unsigned long long key;
+};
+__device__ __forceinline__ OkKey make_pair_ok(bool ok, unsigned long long key) { return {ok, key}; }
+
+__device__ __forceinline__ void keep_min(unsigned long long& k, unsigned long long v) {
+  k = v < k ? v : k;
+}
+
 // Walks strip cells [ka, kb] (strip coordinates: cell k holds grid index
-// k-1).  src.load(k) returns cell k in sweep orientation (called for
-// k = ka-2 .. kb+2 in order), sink(k, out) receives updated cells ka..kb,
-// src.boundary(c) is called after every iteration (chunk bookkeeping).
-// kg converts a local strip cell to the global index used in error keys.
-// The two halo iterations are peeled, so a segment costs its cells plus
-// two primitive conversions, two face reconstructions and one flux.
-template <bool WANT_DT, class Src, class Sink>
-__device__ __forceinline__ void walk_strip(int ka, int kb, Src& src, Sink& sink, const Gas& g,
-                                           double dtdx, double spacing, bool active,
-                                           unsigned long long* err,
-                                           unsigned long long key_base, int kg) {
+// k-1) with math policy M.  src.load(k) returns cell k in sweep orientation
+// (called for k = ka-2 .. kb+2 in order), sink(k, out) receives updated
+// cells ka..kb, src.boundary(c) is called after every iteration (chunk
+// bookkeeping).  Positivity failures are folded into `ekey` (kg converts a
+// local strip cell to the global index used in error keys).  The two halo
+// iterations are peeled, so a segment costs its cells plus two primitive
+// conversions, two face reconstructions and one flux.  Returns false if a
+// FastMath operation left its proven range somewhere in the segment.
+template <class M, bool WANT_DT, class Src, class Sink>
+__device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink, const Gas& g,
+                                           double dtdx, double spacing,
+                                           unsigned long long key_base, int kg,
+                                           unsigned long long& ekey) {
+  M m;
   const double half = 0.5 * dtdx;
   Window w;
   w.uA = src.load(ka - 2);
-  int f = prim_any(w.uA, g, w.wA);
-  if (active && f >= 0) record(err, key_base | ((unsigned long long)(ka - 2 + kg) << 2) | f);
+  int f = to_prim(m, w.uA, g, w.wA);
+  if (f >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka - 2 + kg) << 2) | f);
   w.uB = src.load(ka - 1);
-  f = prim_any(w.uB, g, w.wB);
-  if (active && f >= 0) record(err, key_base | ((unsigned long long)(ka - 1 + kg) << 2) | f);
+  f = to_prim(m, w.uB, g, w.wB);
+  if (f >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka - 1 + kg) << 2) | f);
   {  // c = ka-1: faces of the first halo cell
     const Cons uC = src.load(ka);
     StepOut o;
-    step_any<0, false>(w, uC, half, dtdx, spacing, g, o);
-    if (active && o.fC >= 0) record(err, key_base | ((unsigned long long)(ka + kg) << 2) | o.fC);
+    step_cell<0, false>(m, w, uC, half, dtdx, spacing, g, o);
+    if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka + kg) << 2) | o.fC);
     src.boundary(ka - 1);
     w.wA = w.wB;
     w.wB = o.wC;
@@ -145,8 +135,8 @@ __device__ __forceinline__ void walk_strip(int ka, int kb, Src& src, Sink& sink,
   {  // c = ka: faces of cell ka and the flux through its left interface
     const Cons uC = src.load(ka + 1);
     StepOut o;
-    step_any<1, false>(w, uC, half, dtdx, spacing, g, o);
-    if (active && o.fC >= 0) record(err, key_base | ((unsigned long long)(ka + 1 + kg) << 2) | o.fC);
+    step_cell<1, false>(m, w, uC, half, dtdx, spacing, g, o);
+    if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka + 1 + kg) << 2) | o.fC);
     src.boundary(ka);
     w.wA = w.wB;
     w.wB = o.wC;
@@ -159,11 +149,10 @@ __device__ __forceinline__ void walk_strip(int ka, int kb, Src& src, Sink& sink,
   for (int c = ka + 1; c <= kb + 1; ++c) {
     const Cons uC = src.load(c + 1);
     StepOut o;
-    step_any<2, WANT_DT>(w, uC, half, dtdx, spacing, g, o);
-    if (active && o.fC >= 0)
-      record(err, key_base | ((unsigned long long)(c + 1 + kg) << 2) | o.fC);
-    if (active && o.fU >= 0)
-      record(err, key_base | (1ull << 20) | ((unsigned long long)(c - 1 + kg) << 2) | o.fU);
+    step_cell<2, WANT_DT>(m, w, uC, half, dtdx, spacing, g, o);
+    if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(c + 1 + kg) << 2) | o.fC);
+    if (o.fU >= 0)
+      keep_min(ekey, key_base | (1ull << 20) | ((unsigned long long)(c - 1 + kg) << 2) | o.fU);
     sink(c - 1, o);
     src.boundary(c);
     w.wA = w.wB;
@@ -173,6 +162,7 @@ __device__ __forceinline__ void walk_strip(int ka, int kb, Src& src, Sink& sink,
     w.frPrev = o.fr;
     w.fluxPrev = o.F;
   }
+  return m.ok;
 }
 
 __device__ __forceinline__ bool latched(const SweepArgs& a) {
@@ -253,33 +243,47 @@ __global__ void __launch_bounds__(128, HB_X_MINB) sweep_x_kernel(SweepArgs a) {
     const int j = active ? jt : ny;  // idle lanes shadow the last column, writes masked
     const int i_lo = 1 + sg * a.seg;
     const int i_hi = min(a.nx, i_lo + a.seg - 1);
-    // the prefetch reads one row past the stencil (row nx+3 at most: a
-    // padding row of the allocation)
-    ColumnSource src{a.src + cell_index(pitch, 0, i_lo - 2, j), pitch, {}};
-    src.start();
-    double* out = dst + cell_index(pitch, 0, i_lo, j);
-    auto put = [&](double* q, const Cons& u, bool neg) {
-      q[0] = u.r;
-      q[pitch] = u.ma;
-      q[2 * pitch] = neg ? -u.mb : u.mb;
-      q[3 * pitch] = u.e;
-    };
-    auto sink = [&](int, const StepOut& o) {
-      if (active) {
-        put(out, o.un, false);
-        // y-wall ghosts of the column-sweep output (grid.cpp:44-59)
-        if (refl) {
-          if (j <= 2) put(out + (1 - 2 * j), o.un, true);
-          if (j >= ny - 1) put(out + (2 * ny + 1 - 2 * j), o.un, true);
-        } else {
-          if (j == 1) { put(out - 1, o.un, false); put(out - 2, o.un, false); }
-          if (j == ny) { put(out + 1, o.un, false); put(out + 2, o.un, false); }
-        }
-      }
-      out += 4 * pitch;
-    };
+    // warps holding a y-wall column (1, 2, ny-1 or ny; the last two may sit in
+    // different groups)
+    const bool edge = grp == 0 || (grp << 5) + 32 >= ny - 1;
     const unsigned long long base = error_key(a.step, 1, j, 0, 0, 0);
-    walk_strip<false>(i_lo + 1, i_hi + 1, src, sink, g, dtdx, 0.0, active, a.err, base, a.row0);
+    // One pass over the item with math policy M; returns (in range, error key).
+    auto pass = [&](auto math) {
+      using M = decltype(math);
+      // the prefetch reads one row past the stencil (row nx+3 at most: a
+      // padding row of the allocation)
+      ColumnSource src{a.src + cell_index(pitch, 0, i_lo - 2, j), pitch, {}};
+      src.start();
+      double* out = dst + cell_index(pitch, 0, i_lo, j);
+      auto put = [&](double* q, const Cons& u, bool neg) {
+        q[0] = u.r;
+        q[pitch] = u.ma;
+        q[2 * pitch] = neg ? -u.mb : u.mb;
+        q[3 * pitch] = u.e;
+      };
+      auto sink = [&](int, const StepOut& o) {
+        if (active) put(out, o.un, false);
+        if (edge && active) {  // y-wall ghosts of the column-sweep output (grid.cpp:44-59)
+          if (refl) {
+            if (j <= 2) put(out + (1 - 2 * j), o.un, true);
+            if (j >= ny - 1) put(out + (2 * ny + 1 - 2 * j), o.un, true);
+          } else {
+            if (j == 1) { put(out - 1, o.un, false); put(out - 2, o.un, false); }
+            if (j == ny) { put(out + 1, o.un, false); put(out + 2, o.un, false); }
+          }
+        }
+        out += 4 * pitch;
+      };
+      unsigned long long ek = kNoError;
+      const bool ok = walk_strip<M, false>(i_lo + 1, i_hi + 1, src, sink, g, dtdx, 0.0, base,
+                                           a.row0, ek);
+      return make_pair_ok(ok, ek);
+    };
+    OkKey r = pass(FastMath{});
+    // a fast path left its proven range somewhere: the warp redoes the item
+    // with the compiler's IEEE division/sqrt (overwriting every output)
+    if (!__all_sync(0xffffffffu, r.ok || !active)) r = pass(ExactMath{});
+    if (active && r.key != kNoError) record(a.err, r.key);
   }
 }
 
@@ -470,14 +474,12 @@ __global__ void __launch_bounds__(128, HB_Y_MINB) sweep_y_kernel(SweepArgs a,
     t.ka = j_lo + 1;
     t.kb = j_hi + 1;
     t.nq = (t.kb + 2 - (t.ka - 4) + kChunk) / kChunk;
-    t.ready = -1;
     t.active = active;
-    if (lane == 0)
-      for (int q = 0; q < kNBuf - 1; ++q) t.issue(q);
-
-    const bool mirror_lo = active && a.wall_lo && i <= 2;
-    const bool mirror_hi = active && a.wall_hi && i >= nx - 1;
+    // warps holding x-wall rows write the ghost rows of the next step
+    const bool mirror_lo = a.wall_lo && grp == 0;
+    const bool mirror_hi = a.wall_hi && (grp << 5) + 32 >= nx - 1;  // rows nx-1, nx
     const int gi = a.row0 + i;
+    const unsigned long long base = error_key(a.step, 2, gi, 0, 0, 0);
     auto put_row = [&](int ii, int j, const Cons& u, bool neg) {
       double* q = dst + cell_index(pitch, 0, ii, j);
       q[0] = u.r;
@@ -485,38 +487,58 @@ __global__ void __launch_bounds__(128, HB_Y_MINB) sweep_y_kernel(SweepArgs a,
       q[pitch] = neg ? -u.mb : u.mb;
       q[3 * pitch] = u.e;
     };
-    auto sink = [&](int k, const StepOut& o) {
-      t.put(k, o.un);
-      if (!active) return;
-      const int j = k - 1;
-      if (mirror_lo) {  // x-wall ghosts for the next column sweep (grid.cpp:26-42)
-        if (refl) put_row(1 - i, j, o.un, true);
-        else if (i == 1) { put_row(0, j, o.un, false); put_row(-1, j, o.un, false); }
-      }
-      if (mirror_hi) {
-        if (refl) put_row(2 * nx + 1 - i, j, o.un, true);
-        else if (i == nx) { put_row(nx + 1, j, o.un, false); put_row(nx + 2, j, o.un, false); }
-      }
-      if (a.want_limit) {
-        if (o.fD >= 0) {
-          const unsigned long long key = error_key(a.step + 1, 0, gi, 0, j, o.fD);
-          dt_key = key < dt_key ? key : dt_key;
-        } else {
-          lim_min = smin(lim_min, o.lim);
+    double lim_item;
+    unsigned long long dt_item;
+    // One pass over the item with math policy M (tiles restaged from U_b).
+    auto pass = [&](auto math) {
+      using M = decltype(math);
+      lim_item = __longlong_as_double(0x7ff0000000000000ll);
+      dt_item = kNoError;
+      t.ready = -1;
+      if (lane == 0)
+        for (int q = 0; q < kNBuf - 1; ++q) t.issue(q);
+      auto sink = [&](int k, const StepOut& o) {
+        t.put(k, o.un);
+        const int j = k - 1;
+        if (mirror_lo && active && i <= 2) {  // x-wall ghosts for the next column sweep (grid.cpp:26-42)
+          if (refl) put_row(1 - i, j, o.un, true);
+          else if (i == 1) { put_row(0, j, o.un, false); put_row(-1, j, o.un, false); }
         }
-      }
+        if (mirror_hi && active && i >= nx - 1) {
+          if (refl) put_row(2 * nx + 1 - i, j, o.un, true);
+          else if (i == nx) { put_row(nx + 1, j, o.un, false); put_row(nx + 2, j, o.un, false); }
+        }
+        if (a.want_limit) {
+          if (o.fD >= 0) keep_min(dt_item, error_key(a.step + 1, 0, gi, 0, j, o.fD));
+          else lim_item = smin(lim_item, o.lim);
+        }
+      };
+      unsigned long long ek = kNoError;
+      const bool ok =
+          a.want_limit
+              ? walk_strip<M, true>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, base, 0, ek)
+              : walk_strip<M, false>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, base, 0, ek);
+      // a final segment shorter than whole chunks leaves one chunk unstored
+      const int seg = t.kb + 1 - t.ka;
+      if (seg % kChunk != 0) t.flush(seg / kChunk + 1);
+      if (lane == 0) bulk_wait_read0();  // the ring is free again
+      __syncwarp();
+      t.q0 += t.nq;
+      return make_pair_ok(ok, ek);
     };
-    const unsigned long long base = error_key(a.step, 2, gi, 0, 0, 0);
-    if (a.want_limit)
-      walk_strip<true>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, active, a.err, base, 0);
-    else
-      walk_strip<false>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, active, a.err, base, 0);
-    // a final segment shorter than whole chunks leaves one chunk unstored
-    const int seg = t.kb + 1 - t.ka;
-    if (seg % kChunk != 0) t.flush(seg / kChunk + 1);
-    if (lane == 0) bulk_wait_read0();  // the ring is free for the next item
-    __syncwarp();
-    t.q0 += t.nq;
+    OkKey r = pass(FastMath{});
+    // a fast path left its proven range somewhere: the warp redoes the item
+    // with the compiler's IEEE division/sqrt (restaging and overwriting all)
+    if (!__all_sync(0xffffffffu, r.ok || !active)) {
+      if (lane == 0) bulk_wait0();  // the fast pass's stores have landed
+      __syncwarp();
+      r = pass(ExactMath{});
+    }
+    if (active) {
+      if (r.key != kNoError) record(a.err, r.key);
+      keep_min(dt_key, dt_item);
+      lim_min = smin(lim_min, lim_item);
+    }
   }
   if (lane == 0) bulk_wait0();
   if (a.want_limit) {
@@ -694,6 +716,9 @@ __global__ void math_selftest_kernel(int op, const double* a, const double* b, d
   FastMath fm;
   if (op == 0) {
     fast[t] = fm.divf(a[t], b[t]);
+    ref[t] = a[t] / b[t];
+  } else if (op == 2) {
+    fast[t] = fm.divz(a[t], b[t]);
     ref[t] = a[t] / b[t];
   } else {
     fast[t] = fm.sqrt(a[t]);

@@ -94,3 +94,18 @@ def test_division_zero_numerator_fast_and_signed():
     # negative or non-normal denominators leave the fast path (exact recompute)
     _, _, ok = run(0, np.array([-0.0, 0.0, 0.0, 0.0]), np.array([-2.0, 0.0, 5e-324, np.inf]))
     assert not ok.any()
+
+
+def test_signed_zero_division_any_denominator_sign():
+    """op 2: the star-speed division (divz) -- +-0 over a negative normal
+    denominator stays fast with the IEEE sign."""
+    rng = np.random.default_rng(3)
+    b = np.concatenate([-rng.uniform(1e-6, 1e6, 4096), rng.uniform(1e-6, 1e6, 4096)])
+    for zero in (0.0, -0.0):
+        a = np.full(b.size, zero)
+        fast, exact, ok = run(2, a, b)
+        assert ok.all()
+        assert np.array_equal(bits(fast), bits(exact))
+    a = rng.uniform(-5, 5, b.size)
+    fast, exact, ok = run(2, a, b)
+    assert ok.all() and np.array_equal(bits(fast), bits(exact))

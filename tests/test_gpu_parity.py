@@ -58,6 +58,9 @@ def test_golden_digest(gpu, name):
     ("random", 33, 70, 8, "reflect", 4),
     ("blast", 4, 4, 5, "reflect", 0),
     ("corner_blast", 4, 9, 6, "transmit", 0),
+    ("random", 33, 33, 7, "reflect", 2),     # rows/cols nx-1, nx in different warp groups
+    ("random", 65, 97, 6, "transmit", 8),
+    ("corner_blast", 97, 65, 9, "reflect", 0),
 ])
 def test_every_plane_and_ghost_matches_oracle(gpu, case, nx, ny, steps, bc, seed):
     grid, dt = gpu_run(case, nx, ny, steps, bc, seed)
@@ -237,3 +240,24 @@ def test_full_size_golden(gpu, name):
         g.download(planes)
     grid = P.Grid2D(nx, ny, dx, dy, planes)
     assert f"{P.grid_digest(grid):016x}" == rec["digest"], rec["provenance"]
+
+
+@pytest.mark.parametrize("scale,bc", [(1e-310, "reflect"), (1e-300, "transmit"), (1e200, "transmit")])
+def test_exact_redo_path_is_bitwise(gpu, scale, bc):
+    """Denormal / tiny / huge momenta push FastMath out of its proven range, so
+    warps redo their work items with IEEE division -- still bitwise."""
+    grid = P.make_case("random", 72, 40, MODEL, seed=17)
+    grid.planes[1:3, 10:40, :] *= scale  # momenta of a band of rows
+    ref = O.Grid(grid.nx, grid.ny, grid.dx, grid.dy, grid.planes.copy())
+    msg_ref = msg_gpu = None
+    try:
+        O.run_sequential(ref, 6, bc)
+    except O.CheckerError as e:
+        msg_ref = str(e)
+    try:
+        P.run_gpu(grid, MODEL, 6, bc)
+    except P.PositivityError as e:
+        msg_gpu = str(e)
+    assert msg_gpu == msg_ref
+    if msg_ref is None:
+        assert np.array_equal(grid.planes, ref.u)
