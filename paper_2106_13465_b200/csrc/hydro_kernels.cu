@@ -47,9 +47,11 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
 // ---------------------------------------------------------------------------
 // The strip walker.
 
+// Carried from one cell to the next.  The conserved cells themselves are
+// not carried: the update re-reads cell c-1 from L1 / shared memory, which
+// costs 4 loads instead of 16 register moves and 16 live registers per cell.
 struct Window {
   Prim wA, wB;      // primitives of cells c-1, c
-  Cons uA, uB;      // conserved cells c-1, c
   Face frPrev;      // right face of cell c-1
   Flux fluxPrev;    // flux through interface c-2 | c-1
 };
@@ -68,15 +70,21 @@ struct StepOut {
 // One walker iteration at cell c.  STAGE 0: primitive + faces only (the
 // first halo iteration); STAGE 1: + flux (second halo iteration);
 // STAGE 2: + conservative update (+ dt limit).
-template <int STAGE, bool WANT_DT, class M>
+template <int STAGE, bool WANT_DT, class M, class Old>
 __device__ __forceinline__ void step_cell(M& m, const Window& w, const Cons& uC, double half,
                                           double dtdx, double spacing, const Gas& g,
-                                          StepOut& o) {
+                                          const Old& old, StepOut& o) {
   o.fC = to_prim(m, uC, g, o.wC);
-  predict_faces(m, w.wA, w.wB, o.wC, half, g, o.fl, o.fr);
+  Cons el, er;
+  predict_evolved(m, w.wA, w.wB, o.wC, half, g, el, er);
+  // left face first: it meets the previous right face in this iteration's
+  // Riemann problem, after which that face is dead and the new right face
+  // can take its registers
+  o.fl = face_prim(m, el, w.wB, g);
   if (STAGE >= 1) o.F = hllc(m, w.frPrev, o.fl, g);
+  o.fr = face_prim(m, er, w.wB, g);
   if (STAGE >= 2) {
-    o.un = w.uA;
+    o.un = old();
     Recip rn;
     o.fU = update_cell(m, o.un, w.fluxPrev, o.F, dtdx, rn);
     if (WANT_DT) o.fD = dt_limit(m, o.un, rn, spacing, g, o.lim);
@@ -114,34 +122,29 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
   M m;
   const double half = 0.5 * dtdx;
   Window w;
-  w.uA = src.load(ka - 2);
-  int f = to_prim(m, w.uA, g, w.wA);
+  auto none = [] { return Cons{}; };
+  int f = to_prim(m, src.load(ka - 2), g, w.wA);
   if (f >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka - 2 + kg) << 2) | f);
-  w.uB = src.load(ka - 1);
-  f = to_prim(m, w.uB, g, w.wB);
+  f = to_prim(m, src.load(ka - 1), g, w.wB);
   if (f >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka - 1 + kg) << 2) | f);
   {  // c = ka-1: faces of the first halo cell
     const Cons uC = src.load(ka);
     StepOut o;
-    step_cell<0, false>(m, w, uC, half, dtdx, spacing, g, o);
+    step_cell<0, false>(m, w, uC, half, dtdx, spacing, g, none, o);
     if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka + kg) << 2) | o.fC);
     src.boundary(ka - 1);
     w.wA = w.wB;
     w.wB = o.wC;
-    w.uA = w.uB;
-    w.uB = uC;
     w.frPrev = o.fr;
   }
   {  // c = ka: faces of cell ka and the flux through its left interface
     const Cons uC = src.load(ka + 1);
     StepOut o;
-    step_cell<1, false>(m, w, uC, half, dtdx, spacing, g, o);
+    step_cell<1, false>(m, w, uC, half, dtdx, spacing, g, none, o);
     if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka + 1 + kg) << 2) | o.fC);
     src.boundary(ka);
     w.wA = w.wB;
     w.wB = o.wC;
-    w.uA = w.uB;
-    w.uB = uC;
     w.frPrev = o.fr;
     w.fluxPrev = o.F;
   }
@@ -149,7 +152,7 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
   for (int c = ka + 1; c <= kb + 1; ++c) {
     const Cons uC = src.load(c + 1);
     StepOut o;
-    step_cell<2, WANT_DT>(m, w, uC, half, dtdx, spacing, g, o);
+    step_cell<2, WANT_DT>(m, w, uC, half, dtdx, spacing, g, [&] { return src.reload(c - 1); }, o);
     if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(c + 1 + kg) << 2) | o.fC);
     if (o.fU >= 0)
       keep_min(ekey, key_base | (1ull << 20) | ((unsigned long long)(c - 1 + kg) << 2) | o.fU);
@@ -157,8 +160,6 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
     src.boundary(c);
     w.wA = w.wB;
     w.wB = o.wC;
-    w.uA = w.uB;
-    w.uB = uC;
     w.frPrev = o.fr;
     w.fluxPrev = o.F;
   }
@@ -212,6 +213,11 @@ struct ColumnSource {
     const Cons u = next;
     next = fetch();
     return u;
+  }
+  // Cell c-1 during iteration c (after load(c+1) the cursor is at c+3).
+  __device__ __forceinline__ Cons reload(int) const {
+    const double* q = p - 16 * pitch;
+    return {__ldg(q), __ldg(q + pitch), __ldg(q + 2 * pitch), __ldg(q + 3 * pitch)};
   }
   __device__ __forceinline__ void boundary(int) {}
 };
@@ -394,6 +400,15 @@ struct RowTiles {
               *(const double*)(b + slot(lane, 1, pos)), *(const double*)(b + slot(lane, 3, pos))};
     if (!active) u = {1.0, 0.0, 0.0, 1.0};  // rows past the grid: inert
     return u;
+  }
+
+  // Cell k again (already staged; its slot is overwritten only by put(k)).
+  __device__ __forceinline__ Cons reload(int k) {
+    const int rel = k - ka + 4;
+    const uint8_t* b = buf(rel / kChunk);
+    const int pos = rel % kChunk;
+    return {*(const double*)(b + slot(lane, 0, pos)), *(const double*)(b + slot(lane, 2, pos)),
+            *(const double*)(b + slot(lane, 1, pos)), *(const double*)(b + slot(lane, 3, pos))};
   }
 
   __device__ __forceinline__ void put(int k, const Cons& u) {
