@@ -46,6 +46,19 @@ struct hydro_gpu_ctx {
   size_t ev_next = 0;
   double ms[3] = {0, 0, 0};
   long long n[3] = {0, 0, 0};
+  // CUDA graphs of whole run_sequential calls, one per (steps, timing):
+  // the 2*steps+3 launches replay without per-launch CPU and queue gaps.
+  struct GraphEntry {
+    int steps;
+    bool timing;
+    cudaGraphExec_t exec;
+    std::vector<Pending> events;  // event pairs recorded inside the graph
+  };
+  std::vector<GraphEntry> graphs;
+  bool use_graphs = true;
+  bool capturing = false;         // ev_begin/ev_end use dedicated graph events
+  std::vector<cudaEvent_t> graph_events;
+  size_t graph_next = 0;
 };
 
 namespace {
@@ -122,6 +135,11 @@ double as_double(unsigned long long bits) {
 // Event bracket for one launch (timing mode only).
 void ev_begin(hydro_gpu_ctx* c, cudaEvent_t* a) {
   if (!c->timing) return;
+  if (c->capturing) {  // events pre-created by launch_graph
+    *a = c->graph_events[c->graph_next++];
+    cudaEventRecordWithFlags(*a, c->stream, cudaEventRecordExternal);  // a graph node
+    return;
+  }
   if (c->ev_next + 2 > c->ev_pool.size()) {
     for (int k = 0; k < 64; ++k) {
       cudaEvent_t e;
@@ -135,6 +153,12 @@ void ev_begin(hydro_gpu_ctx* c, cudaEvent_t* a) {
 
 void ev_end(hydro_gpu_ctx* c, cudaEvent_t a, int kind) {
   if (!c->timing) return;
+  if (c->capturing) {
+    cudaEvent_t b = c->graph_events[c->graph_next++];
+    cudaEventRecordWithFlags(b, c->stream, cudaEventRecordExternal);
+    c->pending.push_back({a, b, kind});
+    return;
+  }
   cudaEvent_t b = c->ev_pool[c->ev_next++];
   cudaEventRecord(b, c->stream);
   c->pending.push_back({a, b, kind});
@@ -146,6 +170,8 @@ void harvest(hydro_gpu_ctx* c) {
     if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
       c->ms[p.kind] += ms;
       c->n[p.kind] += 1;
+    } else {
+      cudaGetLastError();  // not recorded (e.g. an aborted capture): skip
     }
   }
   c->pending.clear();
@@ -307,6 +333,89 @@ struct DeviceGuard {
 
 }  // namespace
 
+namespace {
+
+int enqueue_run(hydro_gpu_ctx* c, int steps) {
+  int rc = reset_slots(c);
+  if (rc) return rc;
+  enqueue_prologue(c, 1, 0, 0);
+  for (int s = 0; s < steps; ++s) {
+    enqueue_x(c, s, 0, 0.0);
+    enqueue_y(c, s, 0, 0.0, s + 1 < steps);
+  }
+  enqueue_finish(c);
+  return HYDRO_GPU_OK;
+}
+
+void drop_graphs(hydro_gpu_ctx* c) {
+  for (auto& e : c->graphs) cudaGraphExecDestroy(e.exec);
+  c->graphs.clear();
+  for (auto ev : c->graph_events) cudaEventDestroy(ev);
+  c->graph_events.clear();
+}
+
+// Captures (once) and launches the whole run as a CUDA graph.  Returns
+// false if graphs cannot be used (legacy default stream, capture failure).
+bool launch_graph(hydro_gpu_ctx* c, int steps) {
+  if (!c->use_graphs || c->stream == nullptr || c->stream == cudaStreamLegacy) return false;
+  if (c->timing && !c->pending.empty()) {  // the graph re-records its events
+    cudaStreamSynchronize(c->stream);
+    harvest(c);
+  }
+  hydro_gpu_ctx::GraphEntry* entry = nullptr;
+  for (auto& e : c->graphs)
+    if (e.steps == steps && e.timing == c->timing) entry = &e;
+  if (!entry) {
+    std::vector<hydro_gpu_ctx::Pending> saved;
+    saved.swap(c->pending);
+    if (c->timing) {  // two events per launch: prologue, 2 per step, finish
+      const size_t need = c->graph_events.size() + 2 * (2 * (size_t)steps + 2);
+      c->graph_next = c->graph_events.size();
+      while (c->graph_events.size() < need) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c->graph_events.push_back(e);
+      }
+    }
+    if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+      cudaGetLastError();
+      c->pending.swap(saved);
+      return false;
+    }
+    c->capturing = true;
+    const int rc = enqueue_run(c, steps);
+    c->capturing = false;
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(c->stream, &graph);
+    cudaGraphExec_t exec = nullptr;
+    if (rc != 0 || ec != cudaSuccess || !graph ||
+        cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      c->pending.swap(saved);
+      c->use_graphs = false;
+      return false;
+    }
+    cudaGraphDestroy(graph);
+    if (c->graphs.size() >= 8) {  // bounded cache: forget the oldest run length
+      cudaGraphExecDestroy(c->graphs.front().exec);
+      c->graphs.erase(c->graphs.begin());
+    }
+    c->graphs.push_back({steps, c->timing, exec, {}});
+    entry = &c->graphs.back();
+    entry->events.swap(c->pending);
+    c->pending.swap(saved);
+  }
+  if (cudaGraphLaunch(entry->exec, c->stream) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (c->timing) c->pending.insert(c->pending.end(), entry->events.begin(), entry->events.end());
+  return true;
+}
+
+}  // namespace
+
 extern "C" {
 
 int hydro_gpu_abi_version(void) { return HYDRO_GPU_ABI_VERSION; }
@@ -377,6 +486,8 @@ int hydro_gpu_destroy(hydro_gpu_ctx* ctx) {
   if (!ctx) return HYDRO_GPU_OK;
   DeviceGuard g(ctx->device);
   if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  drop_graphs(ctx);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->A) cudaFree(ctx->A);
   if (ctx->B) cudaFree(ctx->B);
@@ -459,18 +570,17 @@ int hydro_gpu_init_case(hydro_gpu_ctx* c, int case_id, uint64_t seed) {
   return HYDRO_GPU_OK;
 }
 
+
 int hydro_gpu_run_async(hydro_gpu_ctx* c, int steps) {
   if (!c) return HYDRO_GPU_ERR_CONFIG;
   if (steps <= 0) return HYDRO_GPU_OK;
   DeviceGuard g(c->device);
-  int rc = reset_slots(c);
-  if (rc) return rc;
-  enqueue_prologue(c, 1, 0, 0);
-  for (int s = 0; s < steps; ++s) {
-    enqueue_x(c, s, 0, 0.0);
-    enqueue_y(c, s, 0, 0.0, s + 1 < steps);
+  if (steps >= 2 && launch_graph(c, steps)) {
+    CUDA_TRY(c, cudaGetLastError());
+    return HYDRO_GPU_OK;
   }
-  enqueue_finish(c);
+  int rc = enqueue_run(c, steps);
+  if (rc) return rc;
   CUDA_TRY(c, cudaGetLastError());
   return HYDRO_GPU_OK;
 }
@@ -681,6 +791,7 @@ int hydro_gpu_tune(hydro_gpu_ctx* c, int seg_x, int seg_y, int block) {
     return set_err(c, HYDRO_GPU_ERR_CONFIG, "bad launch geometry");
   c->seg_x = seg_x;
   c->seg_y = seg_y;
+  drop_graphs(c);  // launch geometry is baked into captured graphs
   return HYDRO_GPU_OK;
 }
 
