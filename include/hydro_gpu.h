@@ -60,8 +60,13 @@ enum hydro_gpu_status {
  * copy the adjacent interior cell), needed by BASELINE configs 1, 2, 4. */
 enum hydro_gpu_bc { HYDRO_GPU_BC_REFLECT = 0, HYDRO_GPU_BC_TRANSMIT = 1 };
 
-/* Riemann flux: HLLC is the reference hot path (euler_kernel.cpp:59-109). */
-enum hydro_gpu_flux { HYDRO_GPU_FLUX_HLLC = 0 };
+/* Riemann flux: HLLC is the reference hot path (euler_kernel.cpp:59-109);
+ * EXACT10 is BASELINE's "exact Riemann solver with 10 Newton iterations": the
+ * reference's exact solver (exact_riemann.cpp) sampled at x/t = 0, with a
+ * portable log/exp in place of std::pow (bitwise equal to the C oracle,
+ * floored-relative 1e-12 against std::pow).  A vacuum-generating state pair
+ * is a Validation error, as in exact_riemann.cpp:55-57. */
+enum hydro_gpu_flux { HYDRO_GPU_FLUX_HLLC = 0, HYDRO_GPU_FLUX_EXACT10 = 1 };
 
 /* Case ids for the initialisers (cases.cpp:11-69 + BASELINE configs). */
 enum hydro_gpu_case {
@@ -93,9 +98,9 @@ typedef struct hydro_gpu_error {
   int step;            /* step index within the failing call */
   int phase;           /* 0 = compute_dt, 1 = column sweep, 2 = row sweep */
   int strip;           /* 1-based strip (column j or row i); grid row for phase 0 */
-  int loop;            /* 0 = primitive conversion, 1 = conservative update */
+  int loop;            /* 0 = primitive conversion, 1 = Riemann, 2 = conservative update */
   int cell;            /* strip-local index k - kGhost as printed by the reference */
-  int field;           /* 0 = rho, 1 = pres, 2 = internal energy */
+  int field;           /* 0 = rho, 1 = pres, 2 = internal energy, 3 = vacuum */
   char message[256];   /* the reference's what() text, context included */
 } hydro_gpu_error;
 

@@ -117,6 +117,178 @@ static double minmod(double a, double b, double c) {
   return 0.0;
 }
 
+/* ---- exact-10 flux mode (BASELINE "exact Riemann, 10 Newton iterations") --
+ * Restates the reference's exact solver (proj/src/exact_riemann.cpp:17-95,
+ * 139-241) as an interface flux: Newton on the pressure function for exactly
+ * 10 iterations from initial_guess with the p_min floor (closed-form root when
+ * both waves are rarefactions), the wave structure sampled at x/t = 0, then
+ * physical_flux.  std::pow is replaced by or_pow = or_exp(y * or_log(x)),
+ * fdlibm-style argument reduction + polynomials in plain IEEE arithmetic --
+ * the same operation sequence as csrc/hydro_exact.cuh, so CPU and GPU agree
+ * bitwise.  tests/test_exact_flux.py pins it against the reference's own
+ * exact_riemann/sample_riemann (tolerance: pow). */
+
+static int g_flux = 0; /* 0 = HLLC (the reference hot path), 1 = exact-10 */
+
+void oracle_set_flux(int flux) { g_flux = flux; }
+
+static double or_from_bits(uint64_t b) { double d; memcpy(&d, &b, 8); return d; }
+static uint64_t or_to_bits(double x) { uint64_t b; memcpy(&b, &x, 8); return b; }
+
+static double or_log(double x) {
+  const uint64_t bits = or_to_bits(x);
+  uint32_t hx = (uint32_t)(bits >> 32);
+  int k = (int)(hx >> 20) - 1023;
+  hx &= 0x000fffffu;
+  const uint32_t i = (hx + 0x95f64u) & 0x100000u;
+  const double m = or_from_bits(((uint64_t)(hx | (i ^ 0x3ff00000u)) << 32) | (bits & 0xffffffffull));
+  k += (int)(i >> 20);
+  const double f = m - 1.0;
+  const double s = f / (2.0 + f);
+  const double z = s * s;
+  const double w = z * z;
+  const double t1 = w * (3.999999999940941908e-01 + w * (2.222219843214978396e-01 + w * 1.531383769920937332e-01));
+  const double t2 = z * (6.666666666666735130e-01 + w * (2.857142874366239149e-01 +
+                         w * (1.818357216161805012e-01 + w * 1.479819860511658591e-01)));
+  const double R = t2 + t1;
+  const double hfsq = 0.5 * f * f;
+  const double dk = (double)k;
+  return dk * 6.93147180369123816490e-01 - ((hfsq - (s * (hfsq + R) + dk * 1.90821492927058770002e-10)) - f);
+}
+
+static double or_exp(double x) {
+  const double half = (x < 0.0) ? -0.5 : 0.5;
+  const int k = (int)(1.44269504088896338700e+00 * x + half);
+  const double t = (double)k;
+  const double hi = x - t * 6.93147180369123816490e-01;
+  const double lo = t * 1.90821492927058770002e-10;
+  const double r = hi - lo;
+  const double r2 = r * r;
+  const double c = r - r2 * (1.66666666666666019037e-01 + r2 * (-2.77777777770155933842e-03 +
+                   r2 * (6.61375632143793436117e-05 + r2 * (-1.65339022054652515390e-06 +
+                   r2 * 4.13813679705723846039e-08))));
+  const double y = 1.0 - ((lo - (r * c) / (2.0 - c)) - hi);
+  return or_from_bits(or_to_bits(y) + ((uint64_t)(int64_t)k << 52));
+}
+
+static double or_pow(double x, double y) { return or_exp(y * or_log(x)); }
+
+typedef struct { double rho, u, p, c; } xside;
+
+static double side_f(double p, const xside* s, double g) { /* side_fn :26-35 */
+  if (p > s->p) {
+    const double a = 2.0 / ((g + 1.0) * s->rho);
+    const double b = (g - 1.0) / (g + 1.0) * s->p;
+    return (p - s->p) * sqrt(a / (p + b));
+  }
+  return 2.0 * s->c / (g - 1.0) * (or_pow(p / s->p, (g - 1.0) / (2.0 * g)) - 1.0);
+}
+
+static void side_fdf(double p, const xside* s, double g, double* f, double* df) { /* :26-45 */
+  if (p > s->p) {
+    const double a = 2.0 / ((g + 1.0) * s->rho);
+    const double b = (g - 1.0) / (g + 1.0) * s->p;
+    const double root = sqrt(a / (p + b));
+    *f = (p - s->p) * root;
+    *df = root * (1.0 - 0.5 * (p - s->p) / (p + b));
+  } else {
+    const double l = or_log(p / s->p);
+    *f = 2.0 * s->c / (g - 1.0) * (or_exp((g - 1.0) / (2.0 * g) * l) - 1.0);
+    *df = 1.0 / (s->rho * s->c) * or_exp(-(g + 1.0) / (2.0 * g) * l);
+  }
+}
+
+/* State at x/t = 0 of the Riemann problem (wl, wr); 0 on vacuum (:52-59). */
+static int sample_xi0(oprim wl, oprim wr, double g, oprim* out) {
+  const xside l = {wl.r, wl.va, wl.p, sqrt(g * wl.p / wl.r)}; /* make_side :17-22 */
+  const xside r = {wr.r, wr.va, wr.p, sqrt(g * wr.p / wr.r)};
+  const double du = wr.va - wl.va;
+  if (2.0 * (l.c + r.c) / (g - 1.0) <= du) return 0;
+  const double p_min = smin(l.p, r.p);
+  double p;
+  if (side_f(p_min, &l, g) + side_f(p_min, &r, g) + du >= 0.0) { /* :63-69 */
+    const double z = (g - 1.0) / (2.0 * g);
+    const double numer = l.c + r.c - 0.5 * (g - 1.0) * du;
+    const double denom = l.c / or_pow(l.p, z) + r.c / or_pow(r.p, z);
+    p = or_pow(numer / denom, 1.0 / z);
+  } else { /* newton_root :80-95, exactly 10 iterations */
+    const double guess = 0.5 * (l.p + r.p) - 0.125 * du * (l.rho + r.rho) * (l.c + r.c);
+    p = smax(guess, p_min);
+    for (int it = 0; it < 10; ++it) {
+      double fl, dfl, fr, dfr;
+      side_fdf(p, &l, g, &fl, &dfl);
+      side_fdf(p, &r, g, &fr, &dfr);
+      const double f = fl + fr + du;
+      const double df = dfl + dfr;
+      double next = p - f / df;
+      if (next < p_min) next = p_min;
+      p = next;
+    }
+  }
+  const double u_star = 0.5 * (wl.va + wr.va) + 0.5 * (side_f(p, &r, g) - side_f(p, &l, g));
+  const double gm = (g - 1.0) / (g + 1.0);
+  const double xi = 0.0;
+  if (xi <= u_star) { /* sample_riemann :208-223 */
+    if (p > l.p) {
+      const double ratio = p / l.p;
+      const double head = l.u - l.c * sqrt((g + 1.0) / (2.0 * g) * ratio + (g - 1.0) / (2.0 * g));
+      if (xi <= head) { *out = wl; return 1; }
+      out->r = l.rho * (ratio + gm) / (gm * ratio + 1.0); out->va = u_star; out->vb = wl.vb; out->p = p;
+      return 1;
+    }
+    const double head = l.u - l.c;
+    if (xi <= head) { *out = wl; return 1; }
+    const double c_star = l.c * or_pow(p / l.p, (g - 1.0) / (2.0 * g));
+    const double tail = u_star - c_star;
+    if (xi >= tail) {
+      out->r = l.rho * or_pow(p / l.p, 1.0 / g); out->va = u_star; out->vb = wl.vb; out->p = p;
+      return 1;
+    }
+    const double u = 2.0 / (g + 1.0) * (l.c + 0.5 * (g - 1.0) * l.u + xi);
+    const double c = 2.0 / (g + 1.0) * (l.c + 0.5 * (g - 1.0) * (l.u - xi));
+    out->r = l.rho * or_pow(c / l.c, 2.0 / (g - 1.0)); out->va = u; out->vb = wl.vb;
+    out->p = l.p * or_pow(c / l.c, 2.0 * g / (g - 1.0));
+    return 1;
+  }
+  if (p > r.p) { /* :225-240 */
+    const double ratio = p / r.p;
+    const double head = r.u + r.c * sqrt((g + 1.0) / (2.0 * g) * ratio + (g - 1.0) / (2.0 * g));
+    if (xi >= head) { *out = wr; return 1; }
+    out->r = r.rho * (ratio + gm) / (gm * ratio + 1.0); out->va = u_star; out->vb = wr.vb; out->p = p;
+    return 1;
+  }
+  const double head = r.u + r.c;
+  if (xi >= head) { *out = wr; return 1; }
+  const double c_star = r.c * or_pow(p / r.p, (g - 1.0) / (2.0 * g));
+  const double tail = u_star + c_star;
+  if (xi <= tail) {
+    out->r = r.rho * or_pow(p / r.p, 1.0 / g); out->va = u_star; out->vb = wr.vb; out->p = p;
+    return 1;
+  }
+  const double u = 2.0 / (g + 1.0) * (-r.c + 0.5 * (g - 1.0) * r.u + xi);
+  const double c = 2.0 / (g + 1.0) * (r.c - 0.5 * (g - 1.0) * (r.u - xi));
+  out->r = r.rho * or_pow(c / r.c, 2.0 / (g - 1.0)); out->va = u; out->vb = wr.vb;
+  out->p = r.p * or_pow(c / r.c, 2.0 * g / (g - 1.0));
+  return 1;
+}
+
+/* 1 on success, 0 on vacuum. */
+static int exact10(oprim wl, oprim wr, double gamma, oflux* out) {
+  oprim w;
+  if (!sample_xi0(wl, wr, gamma, &w)) return 0;
+  *out = phys_flux(w, gamma);
+  return 1;
+}
+
+int oracle_exact10_flux(const double* wl, const double* wr, double gamma, double* flux) {
+  oprim a = {wl[0], wl[1], wl[2], wl[3]};
+  oprim b = {wr[0], wr[1], wr[2], wr[3]};
+  oflux f;
+  if (!exact10(a, b, gamma, &f)) return OR_ERR_VALIDATION;
+  flux[0] = f.m; flux[1] = f.ma; flux[2] = f.mb; flux[3] = f.e;
+  return OR_OK;
+}
+
 /* HLLC, euler_kernel.cpp:59-109.  Returns 0 on a positivity failure. */
 static int hllc(oprim wl, oprim wr, double gamma, oflux* out, int* field) {
   if (!(wl.r > 0.0)) { *field = 0; return 0; }
@@ -254,7 +426,14 @@ static int strip_update(ocons* c, int n, double dx, double dt, double gamma,
   /* loop 3: one Riemann problem per interface (:195-198) */
   for (int k = 1; k <= n + 1; ++k) {
     int field = 0;
-    if (!hllc(s->fr[k], s->fl[k + 1], gamma, &s->f[k], &field)) {
+    if (g_flux == 1) {
+      if (!exact10(s->fr[k], s->fl[k + 1], gamma, &s->f[k])) {
+        /* exact_riemann.cpp:55-57 */
+        set_error(err, OR_ERR_VALIDATION, "vacuum-generating Riemann states are out of scope");
+        if (err) { err->loop = 1; err->cell = k - KGHOST; err->field = 3; }
+        return OR_ERR_VALIDATION;
+      }
+    } else if (!hllc(s->fr[k], s->fl[k + 1], gamma, &s->f[k], &field)) {
       set_positivity(err, 0, 0, 0, k - KGHOST, field, "riemann state");
       return OR_ERR_POSITIVITY;
     }
@@ -271,13 +450,13 @@ static int strip_update(ocons* c, int n, double dx, double dt, double gamma,
     u->e -= dtdx * (fr.e - fl.e);
     if (!(u->r > 0.0)) {
       snprintf(where, sizeof(where), "updated strip cell %d", k - KGHOST);
-      set_positivity(err, 0, 0, 1, k - KGHOST, 0, where);
+      set_positivity(err, 0, 0, 2, k - KGHOST, 0, where);
       return OR_ERR_POSITIVITY;
     }
     const double eint = u->e - 0.5 * (u->ma * u->ma + u->mb * u->mb) / u->r;
     if (!(eint > 0.0)) {
       snprintf(where, sizeof(where), "updated strip cell %d", k - KGHOST);
-      set_positivity(err, 0, 0, 1, k - KGHOST, 2, where);
+      set_positivity(err, 0, 0, 2, k - KGHOST, 2, where);
       return OR_ERR_POSITIVITY;
     }
   }

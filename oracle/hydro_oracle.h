@@ -40,10 +40,10 @@ enum {
   OR_ERR_VALIDATION = 7
 };
 
-/* Positivity error location: phase 0 = compute_dt, 1 = column sweep,
- * 2 = row sweep; loop 0 = primitive conversion (euler_kernel.cpp:124-139),
- * 1 = conservative update (euler_kernel.cpp:200-220); field 0 = rho,
- * 1 = pres, 2 = internal energy. */
+/* Error location: phase 0 = compute_dt, 1 = column sweep, 2 = row sweep;
+ * loop 0 = primitive conversion (euler_kernel.cpp:124-139), 1 = Riemann
+ * problem, 2 = conservative update (euler_kernel.cpp:200-220); field 0 = rho,
+ * 1 = pres, 2 = internal energy, 3 = vacuum (exact-10 mode). */
 typedef struct {
   int category;
   int step;
@@ -105,6 +105,11 @@ int oracle_run_until(double* u, int nx, int ny, double dx, double dy,
  * (euler_kernel.cpp:111-223).  first/last receive the boundary fluxes. */
 int oracle_sweep_strip(double* cells, int n, double dx, double dt, double gamma,
                        double* first, double* last, oracle_error* err);
+
+/* Interface flux used by every sweep: 0 = HLLC (default, the reference hot
+ * path), 1 = exact-10 (exact Riemann solver, 10 Newton iterations). */
+void oracle_set_flux(int flux);
+int oracle_exact10_flux(const double* wl, const double* wr, double gamma, double* flux);
 
 /* riemann_flux (euler_kernel.cpp:59-109) on primitive states. */
 int oracle_riemann_flux(const double* wl, const double* wr, double gamma,

@@ -79,6 +79,9 @@ def lib():
         L.oracle_sums.restype = None
         L.oracle_compare_tolerance.argtypes = [_dp, _dp, i, i, _dp, _dp]
         L.oracle_compare_tolerance.restype = None
+        L.oracle_set_flux.argtypes = [i]
+        L.oracle_set_flux.restype = None
+        L.oracle_exact10_flux.argtypes = [_dp, _dp, d, _dp]
         L.oracle_splitmix64.argtypes = [u64]
         L.oracle_splitmix64.restype = u64
         _lib = L
@@ -109,6 +112,7 @@ def ref():
         R.ref_sweep_strip.argtypes = [_dp, i, d, d, d, _dp, _dp, C.c_char_p, i]
         R.ref_riemann_flux.argtypes = [_dp, _dp, d, _dp]
         R.ref_hardware_concurrency.restype = i
+        R.ref_exact_flux.argtypes = [_dp, _dp, d, _dp]
         _ref = R
     return _ref
 
@@ -211,6 +215,38 @@ def riemann_flux(wl, wr, gamma=1.4) -> np.ndarray:
     return f
 
 
+FLUXES = {"hllc": 0, "exact10": 1}
+
+
+def set_flux(flux: str) -> None:
+    """Interface flux of every oracle sweep: "hllc" (the reference hot path) or
+    "exact10" (exact Riemann solver, 10 Newton iterations)."""
+    lib().oracle_set_flux(FLUXES[flux])
+
+
+class flux_mode:
+    """Context manager: run oracle calls with the given flux, restore HLLC."""
+
+    def __init__(self, flux: str):
+        self.flux = flux
+
+    def __enter__(self):
+        set_flux(self.flux)
+
+    def __exit__(self, *exc):
+        set_flux("hllc")
+
+
+def exact10_flux(wl, wr, gamma=1.4) -> np.ndarray:
+    a = np.ascontiguousarray(wl, dtype=np.float64)
+    b = np.ascontiguousarray(wr, dtype=np.float64)
+    f = np.zeros(4)
+    rc = lib().oracle_exact10_flux(_ptr(a), _ptr(b), gamma, _ptr(f))
+    if rc:
+        raise CheckerError(rc, "vacuum-generating Riemann states are out of scope")
+    return f
+
+
 def digest(g: Grid) -> int:
     return int(lib().oracle_digest(_ptr(g.u), g.nx, g.ny))
 
@@ -287,6 +323,17 @@ def ref_sweep_strip(cells: np.ndarray, n: int, dx: float, dt: float, gamma=1.4):
     if rc:
         raise CheckerError(rc, msg.value.decode())
     return first, last
+
+
+def ref_exact_flux(wl, wr, gamma=1.4):
+    """(flux, newton iterations) of the reference's exact solver at x/t = 0."""
+    a = np.ascontiguousarray(wl, dtype=np.float64)
+    b = np.ascontiguousarray(wr, dtype=np.float64)
+    f = np.zeros(4)
+    rc = ref().ref_exact_flux(_ptr(a), _ptr(b), gamma, _ptr(f))
+    if rc >= 100:
+        raise CheckerError(rc - 100, "reference exact solver error")
+    return f, rc
 
 
 def ref_riemann_flux(wl, wr, gamma=1.4) -> np.ndarray:

@@ -22,6 +22,7 @@
 #include "hydro/cases.hpp"
 #include "hydro/errors.hpp"
 #include "hydro/euler_kernel.hpp"
+#include "hydro/exact_riemann.hpp"
 #include "hydro/grid.hpp"
 #include "hydro/schedulers.hpp"
 
@@ -213,6 +214,25 @@ int ref_riemann_flux(const double* wl, const double* wr, double gamma,
     return 0;
   } catch (const Error& e) {
     return report(e, nullptr, 0);
+  }
+}
+
+// The reference's exact Riemann solution sampled at x/t = 0 and its
+// physical flux (exact_riemann.cpp:136-241, euler_kernel.cpp:34-39): the
+// ground truth for the exact-10 flux mode.  Returns the Newton iterations
+// used (-1 = closed-form two-rarefaction root) or throws' category + 100.
+int ref_exact_flux(const double* wl, const double* wr, double gamma, double* flux) {
+  try {
+    const GasModel m{gamma, 0.8};
+    const PrimitiveState a{wl[0], wl[1], wl[2], wl[3]};
+    const PrimitiveState b{wr[0], wr[1], wr[2], wr[3]};
+    const WaveStructure ws = exact_riemann(a, b, m);
+    const PrimitiveState w = sample_riemann(ws, a, b, 0.0, m);
+    const FluxVector f = physical_flux(w, m);
+    std::memcpy(flux, &f, sizeof f);
+    return ws.iterations;
+  } catch (const Error& e) {
+    return 100 + static_cast<int>(e.category()) + 1;
   }
 }
 

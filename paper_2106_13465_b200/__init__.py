@@ -7,6 +7,7 @@ reference's stepping interface (hydro.py) and the multi-GPU slab driver
 (slab.py).
 """
 from .hydro import (  # noqa: F401
-    BC, CASES, ConfigError, DeviceError, ErrorCategory, GasModel, GpuGrid, Grid2D, HydroError,
-    PositivityError, advance_gpu, compute_dt_gpu, grid_digest, make_case, run_gpu, run_until_gpu,
+    BC, CASES, FLUX, ConfigError, DeviceError, ErrorCategory, GasModel, GpuGrid, Grid2D, HydroError,
+    PositivityError, ValidationError, advance_gpu, compute_dt_gpu, grid_digest, make_case, run_gpu,
+    run_until_gpu,
 )

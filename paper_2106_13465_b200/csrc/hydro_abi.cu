@@ -110,7 +110,7 @@ bool valid_cfg(const hydro_gpu_cfg* c, char* why, size_t n) {
     std::snprintf(why, n, "unknown boundary kind %d", c->bc);
     return false;
   }
-  if (c->flux != HYDRO_GPU_FLUX_HLLC) {
+  if (c->flux != HYDRO_GPU_FLUX_HLLC && c->flux != HYDRO_GPU_FLUX_EXACT10) {
     std::snprintf(why, n, "unknown flux kind %d", c->flux);
     return false;
   }
@@ -188,6 +188,7 @@ hb::SweepArgs sweep_args(hydro_gpu_ctx* c, int axis, int step) {
   a.gamma = c->cfg.gamma;
   a.cfl = c->cfg.cfl;
   a.bc = c->cfg.bc;
+  a.flux = c->cfg.flux;
   a.wall_lo = c->cfg.wall_lo;
   a.wall_hi = c->cfg.wall_hi;
   a.row0 = c->cfg.row0;
@@ -281,23 +282,29 @@ int reset_slots(hydro_gpu_ctx* c) {
 
 void decode(unsigned long long key, hydro_gpu_error* e, bool with_step) {
   *e = hydro_gpu_error{};
-  e->category = HYDRO_GPU_ERR_POSITIVITY;
-  e->step = (int)(key >> 41);
-  e->phase = (int)((key >> 39) & 3);
-  e->strip = (int)((key >> 21) & 0x3ffff);
-  e->loop = (int)((key >> 20) & 1);
+  e->step = (int)(key >> 42);
+  e->phase = (int)((key >> 40) & 3);
+  e->strip = (int)((key >> 22) & 0x3ffff);
+  e->loop = (int)((key >> 20) & 3);
   const int k = (int)((key >> 2) & 0x3ffff);
   e->field = (int)(key & 3);
+  e->category = e->field == 3 ? HYDRO_GPU_ERR_VALIDATION : HYDRO_GPU_ERR_POSITIVITY;
   char body[200];
-  const char* fname = kFieldName[e->field < 3 ? e->field : 0];
   if (e->phase == 0) {
     e->cell = k;  // column j of the failing cell; compute_dt has no strip context
-    std::snprintf(body, sizeof body, "%s non-positive at cons_to_prim input", fname);
+    std::snprintf(body, sizeof body, "%s non-positive at cons_to_prim input",
+                  kFieldName[e->field < 3 ? e->field : 0]);
   } else {
     e->cell = k - 2;  // k - kGhost
-    std::snprintf(body, sizeof body, "%s sweep strip %d: %s non-positive at %sstrip cell %d",
-                  e->phase == 1 ? "column" : "row", e->strip, fname, e->loop ? "updated " : "",
-                  e->cell);
+    const char* sweep = e->phase == 1 ? "column" : "row";
+    if (e->field == 3)  // exact-10 mode (exact_riemann.cpp:55-57)
+      std::snprintf(body, sizeof body,
+                    "%s sweep strip %d: vacuum-generating Riemann states are out of scope", sweep,
+                    e->strip);
+    else
+      std::snprintf(body, sizeof body, "%s sweep strip %d: %s non-positive at %sstrip cell %d",
+                    sweep, e->strip, kFieldName[e->field], e->loop == 2 ? "updated " : "",
+                    e->cell);
   }
   if (with_step)
     std::snprintf(e->message, sizeof e->message, "step %d: %s", e->step, body);
@@ -317,7 +324,7 @@ int finish_status(hydro_gpu_ctx* c, bool with_step) {
     return HYDRO_GPU_OK;
   }
   decode(key, &c->last, with_step);
-  return HYDRO_GPU_ERR_POSITIVITY;
+  return c->last.category;
 }
 
 struct DeviceGuard {
@@ -655,7 +662,7 @@ int hydro_gpu_run_until(hydro_gpu_ctx* c, double t_end, int* steps_out) {
     if (key != hb::kNoError) {
       *steps_out = steps;
       decode(key, &c->last, true);
-      return HYDRO_GPU_ERR_POSITIVITY;
+      return c->last.category;
     }
     double dt = c->cfg.cfl * as_double(sl[steps & 1]);
     if (t + dt > t_end) dt = t_end - t;
@@ -746,7 +753,7 @@ int hydro_gpu_decode_error(hydro_gpu_ctx* c, uint64_t key, hydro_gpu_error* out)
   }
   decode(key, out, true);
   c->last = *out;
-  return HYDRO_GPU_ERR_POSITIVITY;
+  return out->category;
 }
 
 // ---- instrumentation ---------------------------------------------------------

@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include "hydro_exact.cuh"
 #include "hydro_kernels.cuh"
 
 namespace hb {
@@ -61,6 +62,7 @@ struct StepOut {
   int fC;           // its positivity failure (-1 none)
   Face fl, fr;      // faces of cell c
   Flux F;           // flux through interface c-1 | c
+  int fR;           // Riemann failure (exact-10: 3 = vacuum), -1 none
   Cons un;          // cell c-1 after the conservative update
   int fU;
   double lim;       // cell_dt_limit of the updated cell (row sweep)
@@ -70,7 +72,25 @@ struct StepOut {
 // One walker iteration at cell c.  STAGE 0: primitive + faces only (the
 // first halo iteration); STAGE 1: + flux (second halo iteration);
 // STAGE 2: + conservative update (+ dt limit).
-template <int STAGE, bool WANT_DT, class M, class Old>
+// FLUX 0: HLLC (euler_kernel.cpp:59-109); FLUX 1: exact Riemann, 10 Newton
+// iterations (hydro_exact.cuh).
+template <int FLUX, class M>
+__device__ __forceinline__ Flux riemann(M& m, const Face& L, const Face& R, const Gas& g, int& fail) {
+  fail = -1;
+  if constexpr (FLUX == 0) {
+    return hllc(m, L, R, g);
+  } else {
+    bool vacuum;
+    const Flux f = exact10_flux(L.w, R.w, g, vacuum);
+    if (vacuum) {
+      if constexpr (M::kFast) m.fallback();  // reported by the exact pass
+      else fail = 3;
+    }
+    return f;
+  }
+}
+
+template <int STAGE, bool WANT_DT, int FLUX, class M, class Old>
 __device__ __forceinline__ void step_cell(M& m, const Window& w, const Cons& uC, double half,
                                           double dtdx, double spacing, const Gas& g,
                                           const Old& old, StepOut& o) {
@@ -81,7 +101,8 @@ __device__ __forceinline__ void step_cell(M& m, const Window& w, const Cons& uC,
   // Riemann problem, after which that face is dead and the new right face
   // can take its registers
   o.fl = face_prim(m, el, w.wB, g);
-  if (STAGE >= 1) o.F = hllc(m, w.frPrev, o.fl, g);
+  o.fR = -1;
+  if (STAGE >= 1) o.F = riemann<FLUX>(m, w.frPrev, o.fl, g, o.fR);
   o.fr = face_prim(m, er, w.wB, g);
   if (STAGE >= 2) {
     o.un = old();
@@ -114,7 +135,7 @@ __device__ __forceinline__ void keep_min(unsigned long long& k, unsigned long lo
 // iterations are peeled, so a segment costs its cells plus two primitive
 // conversions, two face reconstructions and one flux.  Returns false if a
 // FastMath operation left its proven range somewhere in the segment.
-template <class M, bool WANT_DT, class Src, class Sink>
+template <class M, bool WANT_DT, int FLUX, class Src, class Sink>
 __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink, const Gas& g,
                                            double dtdx, double spacing,
                                            unsigned long long key_base, int kg,
@@ -130,7 +151,7 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
   {  // c = ka-1: faces of the first halo cell
     const Cons uC = src.load(ka);
     StepOut o;
-    step_cell<0, false>(m, w, uC, half, dtdx, spacing, g, none, o);
+    step_cell<0, false, FLUX>(m, w, uC, half, dtdx, spacing, g, none, o);
     if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka + kg) << 2) | o.fC);
     src.boundary(ka - 1);
     w.wA = w.wB;
@@ -140,8 +161,10 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
   {  // c = ka: faces of cell ka and the flux through its left interface
     const Cons uC = src.load(ka + 1);
     StepOut o;
-    step_cell<1, false>(m, w, uC, half, dtdx, spacing, g, none, o);
+    step_cell<1, false, FLUX>(m, w, uC, half, dtdx, spacing, g, none, o);
     if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka + 1 + kg) << 2) | o.fC);
+    if (o.fR >= 0)
+      keep_min(ekey, key_base | (1ull << 20) | ((unsigned long long)(ka - 1 + kg) << 2) | o.fR);
     src.boundary(ka);
     w.wA = w.wB;
     w.wB = o.wC;
@@ -152,10 +175,13 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
   for (int c = ka + 1; c <= kb + 1; ++c) {
     const Cons uC = src.load(c + 1);
     StepOut o;
-    step_cell<2, WANT_DT>(m, w, uC, half, dtdx, spacing, g, [&] { return src.reload(c - 1); }, o);
+    step_cell<2, WANT_DT, FLUX>(m, w, uC, half, dtdx, spacing, g,
+                                [&] { return src.reload(c - 1); }, o);
     if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(c + 1 + kg) << 2) | o.fC);
+    if (o.fR >= 0)
+      keep_min(ekey, key_base | (1ull << 20) | ((unsigned long long)(c - 1 + kg) << 2) | o.fR);
     if (o.fU >= 0)
-      keep_min(ekey, key_base | (1ull << 20) | ((unsigned long long)(c - 1 + kg) << 2) | o.fU);
+      keep_min(ekey, key_base | (2ull << 20) | ((unsigned long long)(c - 1 + kg) << 2) | o.fU);
     sink(c - 1, o);
     src.boundary(c);
     w.wA = w.wB;
@@ -222,7 +248,10 @@ struct ColumnSource {
   __device__ __forceinline__ void boundary(int) {}
 };
 
-__global__ void __launch_bounds__(128, HB_X_MINB) sweep_x_kernel(SweepArgs a) {
+// The exact-10 flux needs far more live state than HLLC: it gets the
+// register file of 2 CTAs/SM instead of a spilling 128-register cap.
+template <int FLUX>
+__global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : 2) sweep_x_kernel(SweepArgs a) {
   if (latched(a)) return;
   const int lane = threadIdx.x & 31;
   if (*(volatile unsigned long long*)a.dt_err != kNoError) {
@@ -281,8 +310,8 @@ __global__ void __launch_bounds__(128, HB_X_MINB) sweep_x_kernel(SweepArgs a) {
         out += 4 * pitch;
       };
       unsigned long long ek = kNoError;
-      const bool ok = walk_strip<M, false>(i_lo + 1, i_hi + 1, src, sink, g, dtdx, 0.0, base,
-                                           a.row0, ek);
+      const bool ok = walk_strip<M, false, FLUX>(i_lo + 1, i_hi + 1, src, sink, g, dtdx, 0.0,
+                                                 base, a.row0, ek);
       return make_pair_ok(ok, ek);
     };
     OkKey r = pass(FastMath{});
@@ -446,7 +475,8 @@ struct RowTiles {
   }
 };
 
-__global__ void __launch_bounds__(128, HB_Y_MINB) sweep_y_kernel(SweepArgs a,
+template <int FLUX>
+__global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel(SweepArgs a,
                                                        const __grid_constant__ CUtensorMap load_map,
                                                        const __grid_constant__ CUtensorMap store_map) {
   extern __shared__ uint8_t smem_raw[];
@@ -531,8 +561,8 @@ __global__ void __launch_bounds__(128, HB_Y_MINB) sweep_y_kernel(SweepArgs a,
       unsigned long long ek = kNoError;
       const bool ok =
           a.want_limit
-              ? walk_strip<M, true>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, base, 0, ek)
-              : walk_strip<M, false>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, base, 0, ek);
+              ? walk_strip<M, true, FLUX>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, base, 0, ek)
+              : walk_strip<M, false, FLUX>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, base, 0, ek);
       // a final segment shorter than whole chunks leaves one chunk unstored
       const int seg = t.kb + 1 - t.ka;
       if (seg % kChunk != 0) t.flush(seg / kChunk + 1);
@@ -762,12 +792,17 @@ int query_geometry(Geometry* g) {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(sweep_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
-  int ox = 0, oy = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, sweep_x_kernel, 128, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy, sweep_y_kernel, 128, kYSmemBytes);
+  cudaFuncSetAttribute(sweep_y_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
+  cudaFuncSetAttribute(sweep_y_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
+  int ox = 0, oy = 0, ox1 = 0, oy1 = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, sweep_x_kernel<0>, 128, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy, sweep_y_kernel<0>, 128, kYSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox1, sweep_x_kernel<1>, 128, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy1, sweep_y_kernel<1>, 128, kYSmemBytes);
   g->ctas_x_per_sm = ox > 0 ? ox : 1;
   g->ctas_y_per_sm = oy > 0 ? oy : 1;
+  g->ctas_x_exact = ox1 > 0 ? ox1 : 1;
+  g->ctas_y_exact = oy1 > 0 ? oy1 : 1;
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -801,20 +836,26 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
 
 void launch_sweep_x(const SweepArgs& a0, const Geometry& geo, cudaStream_t s) {
   SweepArgs a = a0;
-  const int ctas = geo.sms * geo.ctas_x_per_sm;
+  const int ctas = geo.sms * (a.flux == 1 ? geo.ctas_x_exact : geo.ctas_x_per_sm);
   if (a.seg <= 0) a.seg = pick_seg(a.nx, a.ny, ctas * 4);
   a.nseg = (a.nx + a.seg - 1) / a.seg;
-  sweep_x_kernel<<<ctas, 128, 0, s>>>(a);
+  if (a.flux == 1)
+    sweep_x_kernel<1><<<ctas, 128, 0, s>>>(a);
+  else
+    sweep_x_kernel<0><<<ctas, 128, 0, s>>>(a);
 }
 
 void launch_sweep_y(const SweepArgs& a0, const TmaMaps& maps, const Geometry& geo,
                     cudaStream_t s) {
   SweepArgs a = a0;
-  const int ctas = geo.sms * geo.ctas_y_per_sm;
+  const int ctas = geo.sms * (a.flux == 1 ? geo.ctas_y_exact : geo.ctas_y_per_sm);
   if (a.seg <= 0) a.seg = pick_seg(a.ny, a.nx, ctas * 4);
   a.seg = (a.seg + kChunk - 1) / kChunk * kChunk;  // chunks never straddle segments
   a.nseg = (a.ny + a.seg - 1) / a.seg;
-  sweep_y_kernel<<<ctas, 128, kYSmemBytes, s>>>(a, maps.y_load, maps.y_store);
+  if (a.flux == 1)
+    sweep_y_kernel<1><<<ctas, 128, kYSmemBytes, s>>>(a, maps.y_load, maps.y_store);
+  else
+    sweep_y_kernel<0><<<ctas, 128, kYSmemBytes, s>>>(a, maps.y_load, maps.y_store);
 }
 
 void launch_prologue(const PrologueArgs& a, cudaStream_t s) {

@@ -45,6 +45,7 @@ struct SweepArgs {
   double spacing;             // min(dx, dy) for the dt limit
   double gamma, cfl;
   int bc;                     // 0 reflect, 1 transmit
+  int flux;                   // 0 HLLC, 1 exact Riemann (10 Newton iterations)
   int wall_lo, wall_hi;       // physical walls on the i sides of this slab
   int row0;                   // global row of local row 1, minus 1
   unsigned long long* limit_in;   // dt limit consumed by this step
@@ -96,6 +97,8 @@ struct InitArgs {
 struct Geometry {
   int ctas_x_per_sm;          // resident CTAs per SM (from the occupancy API)
   int ctas_y_per_sm;
+  int ctas_x_exact;           // the same for the exact-10 flux instantiations
+  int ctas_y_exact;
   int sms;
 };
 

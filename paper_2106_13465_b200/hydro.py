@@ -78,6 +78,11 @@ class DeviceError(HydroError):
     pass
 
 
+class ValidationError(HydroError):
+    """ErrorCategory::Validation, e.g. a vacuum-generating Riemann problem in
+    the exact-10 flux mode (exact_riemann.cpp:55-57)."""
+
+
 def _raise_for(status: int, info: L.ErrorInfo | None = None, message: str | None = None):
     if status == 0:
         return
@@ -87,6 +92,8 @@ def _raise_for(status: int, info: L.ErrorInfo | None = None, message: str | None
         details = {k: getattr(info, k) for k in ("step", "phase", "strip", "loop", "cell", "field")}
     if status == ErrorCategory.POSITIVITY:
         raise PositivityError(status, msg, details)
+    if status == ErrorCategory.VALIDATION:
+        raise ValidationError(status, msg, details)
     if status == ErrorCategory.CONFIG:
         raise ConfigError(msg or "invalid configuration")
     if status == ErrorCategory.CUDA:
@@ -101,6 +108,7 @@ class GasModel:
 
 
 BC = {"reflect": 0, "transmit": 1}
+FLUX = {"hllc": 0, "exact10": 1}
 CASES = {"uniform": 0, "blast": 1, "sod": 2, "corner_blast": 3, "sod_x": 4, "random": 5}
 RHO, MOM_X, MOM_Y, ENER = 0, 1, 2, 3
 
@@ -159,14 +167,17 @@ class GpuGrid:
 
     def __init__(self, nx: int, ny: int, dx: float, dy: float, model: GasModel = GasModel(),
                  bc: str = "reflect", device: int = -1, row0: int = 0, global_nx: int | None = None,
-                 wall_lo: bool = True, wall_hi: bool = True):
+                 wall_lo: bool = True, wall_hi: bool = True, flux: str = "hllc"):
         if bc not in BC:
             raise ConfigError(f"unknown boundary '{bc}' (expected reflect or transmit)")
+        if flux not in FLUX:
+            raise ConfigError(f"unknown flux '{flux}' (expected hllc or exact10)")
+        self.flux = flux
         self.nx, self.ny, self.dx, self.dy = nx, ny, dx, dy
         self.model, self.bc = model, bc
         self.row0 = row0
         self.global_nx = global_nx if global_nx is not None else nx
-        cfg = L.Cfg(nx, ny, dx, dy, model.gamma, model.cfl, BC[bc], 0, device, row0,
+        cfg = L.Cfg(nx, ny, dx, dy, model.gamma, model.cfl, BC[bc], FLUX[flux], device, row0,
                     self.global_nx, int(wall_lo), int(wall_hi))
         self._lib = L.lib()
         self._ctx = C.c_void_p()
@@ -316,15 +327,16 @@ class GpuGrid:
         return C.cast(p, C.c_void_p).value, pitch.value
 
 
-def _context_for(grid: Grid2D, model: GasModel, bc: str) -> GpuGrid:
-    g = GpuGrid(grid.nx, grid.ny, grid.dx, grid.dy, model, bc)
+def _context_for(grid: Grid2D, model: GasModel, bc: str, flux: str = "hllc") -> GpuGrid:
+    g = GpuGrid(grid.nx, grid.ny, grid.dx, grid.dy, model, bc, flux=flux)
     g.upload(grid.planes)
     return g
 
 
-def run_gpu(grid: Grid2D, model: GasModel = GasModel(), steps: int = 1, bc: str = "reflect") -> float:
+def run_gpu(grid: Grid2D, model: GasModel = GasModel(), steps: int = 1, bc: str = "reflect",
+            flux: str = "hllc") -> float:
     """run_sequential(grid, model, steps) on the GPU, in place; returns the last dt."""
-    with _context_for(grid, model, bc) as g:
+    with _context_for(grid, model, bc, flux) as g:
         try:
             last = g.run(steps)
         finally:
@@ -341,9 +353,10 @@ def advance_gpu(grid: Grid2D, model: GasModel, dt: float, bc: str = "reflect") -
             g.download(grid.planes)
 
 
-def run_until_gpu(grid: Grid2D, model: GasModel, t_end: float, bc: str = "reflect") -> int:
+def run_until_gpu(grid: Grid2D, model: GasModel, t_end: float, bc: str = "reflect",
+                  flux: str = "hllc") -> int:
     """run_until(grid, model, t_end) on the GPU, in place; returns steps taken."""
-    with _context_for(grid, model, bc) as g:
+    with _context_for(grid, model, bc, flux) as g:
         try:
             steps = g.run_until(t_end)
         finally:
