@@ -141,6 +141,9 @@ __device__ __forceinline__ bool sample0(const Prim& wl, const Prim& wr, double g
     const double guess =
         0.5 * (l.p + r.p) - 0.125 * du * (l.rho + r.rho) * (l.c + r.c);  // :72-74
     p = smax(guess, p_min);
+    // Once a step reproduces p exactly, every remaining step does too (same
+    // inputs, same arithmetic), so leaving the loop there is bitwise
+    // identical to running all 10 iterations -- typically after 4-5.
 #pragma unroll 1
     for (int it = 0; it < 10; ++it) {
       double fl, dfl, fr, dfr;
@@ -150,6 +153,7 @@ __device__ __forceinline__ bool sample0(const Prim& wl, const Prim& wr, double g
       const double df = dfl + dfr;
       double next = p - f / df;
       if (next < p_min) next = p_min;
+      if (next == p) break;
       p = next;
     }
   }
