@@ -30,9 +30,20 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# BASELINE.json configs: name -> (case, nx per GPU, ny, bc,
+# time steps per bench step, seed, scaling when --gpus > 1)
+WORKLOADS = {
+    "cfg0": ("corner_blast", 256, 256, "reflect", 100, 0, "weak"),
+    "cfg1": ("sod_x", 2048, 2048, "transmit", 200, 0, "weak"),
+    "cfg2": ("random", 8192, 8192, "transmit", 50, 2106, "weak"),
+    "cfg3": ("corner_blast", 16384, 16384, "reflect", 50, 0, "strong"),
+    "cfg4": ("random", 16384, 16384, "transmit", 20, 13465, "weak"),
+}
 NX = NY = 2048
 TSTEPS = 200
 CASE, BC = "sod_x", "transmit"
+SEED = 0
+SCALING = "weak"
 METRIC = "cell-updates/s (both sweeps, fp64)"
 UNIT = "cell-updates/s"
 ALG_BYTES_PER_CELL_SWEEP = 64  # 32 B read + 32 B write of 4 fp64 fields
@@ -109,7 +120,7 @@ def cpu_reference_sample(steps_per_chunk: int, threads: int, min_seconds: float 
     continuing the same flow until at least `min_seconds` of stepping was
     timed.  Returns (cell-steps/s, kind, seconds, threads, steps)."""
     from oracle import oracle as O
-    g = O.make_case(CASE, NX, NY)
+    g = O.make_case(CASE, NX, NY, seed=SEED)
     kind = "reference" if O.ref_available() else "port"
     if kind == "reference":
         O.ref_run(g.copy(), 1, BC, "coarse_grain", threads)  # warm-up (bench.cpp:112-117)
@@ -162,7 +173,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="cfg1", choices=sorted(WORKLOADS),
+                    help="BASELINE config (default cfg1, the metric's config)")
+    ap.add_argument("--flux", default="hllc", choices=["hllc", "exact10"],
+                    help="interface flux (hllc = the reference hot path)")
     args = ap.parse_args()
+    global NX, NY, TSTEPS, CASE, BC, SEED, SCALING
+    CASE, NX, NY, BC, TSTEPS, SEED, SCALING = WORKLOADS[args.workload]
     rank, world, local = dist_env()
 
     if args.impl == "reference":
@@ -182,24 +199,26 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     model = P.GasModel()
-    global_nx = NX * world
+    # weak scaling grows the slab axis i by the GPU count;
+    # strong scaling splits one grid
+    global_nx = NX * world if SCALING == "weak" else NX
     dx, dy = 1.0 / global_nx, 1.0 / NY
     stream = torch.cuda.Stream()  # a real stream: library kernels, NCCL and events share it
     torch.cuda.set_stream(stream)
 
     geo = S.SlabGeometry(global_nx, NY, rank, world)
     if world == 1:
-        grid = P.GpuGrid(NX, NY, dx, dy, model, BC, device=local)
+        grid = P.GpuGrid(NX, NY, dx, dy, model, BC, device=local, flux=args.flux)
         grid.set_stream(stream.cuda_stream)
         slab = None
     else:
-        slab = S.GpuSlab(geo, dx, dy, model, BC, local)
+        slab = S.GpuSlab(geo, dx, dy, model, BC, local, flux=args.flux)
         slab.bind_stream(stream)
         grid = slab.grid
         comm = S.TorchComm()
 
     def one_step():
-        grid.init_case(CASE, 0)
+        grid.init_case(CASE, SEED)
         if world == 1:
             grid.run_async(TSTEPS)
         else:
@@ -256,11 +275,11 @@ def main():
     # ---- end-to-end through the C-ABI with pinned host buffers --------------
     host0 = torch.zeros((4, geo.nx + 4, NY + 4), dtype=torch.float64).pin_memory()
     host = torch.zeros_like(host0).pin_memory()
-    init = P.make_case(CASE, global_nx, NY, model) if world == 1 else None
+    init = P.make_case(CASE, global_nx, NY, model, seed=SEED) if world == 1 else None
     if init is not None:
         host0.copy_(torch.from_numpy(init.planes))
     else:
-        full = P.make_case(CASE, global_nx, NY, model)
+        full = P.make_case(CASE, global_nx, NY, model, seed=SEED)
         host0.copy_(torch.from_numpy(S.slab_planes(full.planes, global_nx, world, rank)))
         del full
     ptrs0 = [host0[v].data_ptr() for v in range(4)]
@@ -317,14 +336,15 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (analytic Sod initial condition, no dataset)",
-            "config": {"workload": f"BASELINE config 1: {global_nx}x{NY} {CASE} {BC}, HLLC, "
-                                   f"{TSTEPS} time steps per bench step",
+            "higher_is_better": True, "scaling": SCALING, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (analytic or seeded initial condition, no dataset)",
+            "config": {"workload": f"BASELINE {args.workload}: {global_nx}x{NY} {CASE} {BC}, "
+                                   f"{args.flux}, {TSTEPS} time steps per bench step",
                        "global_batch": cells, "seq_len": TSTEPS,
                        "parallelism": f"row slabs x{world}" if world > 1 else "single GPU",
-                       "l2": "inputs larger than L2 (2 x 134 MB state per GPU)",
-                       "flux": "hllc"},
+                       "l2": "inputs larger than L2 (2 x %.0f MB state per GPU)"
+                             % (4 * (geo.nx + 4) * (NY + 4) * 8 / 1e6),
+                       "flux": args.flux, "seed": SEED},
             "roofline": {"bound": "hbm", "kernel": f"sweep_{which}", "achieved": achieved,
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
