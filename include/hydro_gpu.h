@@ -188,10 +188,30 @@ int hydro_gpu_math_selftest(int op, const double* a, const double* b, double* fa
 /* Device pointer to plane-interleaved storage and its pitch (doubles). */
 int hydro_gpu_state(hydro_gpu_ctx* ctx, double** dev_ptr, size_t* pitch);
 
+/* ---- device-side audit (no grid download) ------------------------------ */
+/* Per (variable, interior row) FNV-1a hash and plain sum of the current
+ * state, 4*nx entries each (variable-major, rows in order); either pointer
+ * may be NULL. */
+int hydro_gpu_row_audit(hydro_gpu_ctx* ctx, uint64_t* row_hashes, double* row_sums);
+/* Composable state hash: FNV-1a over the row hashes in (variable, global row)
+ * order.  Equal to hydro_grid_state_hash of the downloaded planes; for row
+ * slabs, the row hashes of all ranks in global order combine to the hash of
+ * the whole grid (hydro_combine_row_hashes). */
+int hydro_gpu_state_hash(hydro_gpu_ctx* ctx, uint64_t* out);
+/* Volume-weighted interior totals (conservation_totals, audit.cpp:16-51):
+ * per-row sums on the device, pairwise over rows on the host. */
+int hydro_gpu_totals(hydro_gpu_ctx* ctx, double out[4]);
+
 /* ---- host utilities (no device needed) --------------------------------- */
 /* FNV-1a digest of the interior bytes (proj/src/audit.cpp:53-76). */
 uint64_t hydro_grid_digest(const double* const planes[4], size_t row_stride,
                            int nx, int ny);
+/* The state hash of host Grid2D planes, and its combining step. */
+uint64_t hydro_grid_state_hash(const double* const planes[4], size_t row_stride, int nx,
+                               int ny);
+uint64_t hydro_combine_row_hashes(const uint64_t* row_hashes, size_t n);
+/* pairwise_sum of audit.cpp:16-25. */
+double hydro_pairwise_sum(const double* v, size_t n);
 /* Host initialiser for the case ids above; fills 4 planes (zeroing first,
  * like Grid2D's constructor) and the spacings. */
 int hydro_init_case_host(int case_id, int nx, int ny, double gamma,

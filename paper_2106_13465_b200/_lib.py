@@ -86,6 +86,12 @@ def lib() -> C.CDLL:
         "hydro_gpu_state": ([_ctx, P(_dp), P(sz)], i),
         "hydro_gpu_math_selftest": ([i, _dp, _dp, _dp, _dp, P(i), sz], i),
         "hydro_grid_digest": ([_planes, sz, i, i], u64),
+        "hydro_grid_state_hash": ([_planes, sz, i, i], u64),
+        "hydro_combine_row_hashes": ([P(u64), sz], u64),
+        "hydro_pairwise_sum": ([_dp, sz], d),
+        "hydro_gpu_row_audit": ([_ctx, P(u64), _dp], i),
+        "hydro_gpu_state_hash": ([_ctx, P(u64)], i),
+        "hydro_gpu_totals": ([_ctx, _dp], i),
         "hydro_init_case_host": ([i, i, i, d, u64, _planes, sz, _dp, _dp], i),
     }
     for name, (args, res) in sig.items():

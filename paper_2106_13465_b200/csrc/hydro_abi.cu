@@ -802,6 +802,48 @@ int hydro_gpu_tune(hydro_gpu_ctx* c, int seg_x, int seg_y, int block) {
   return HYDRO_GPU_OK;
 }
 
+int hydro_gpu_row_audit(hydro_gpu_ctx* c, uint64_t* row_hashes, double* row_sums) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  const size_t n = 4 * (size_t)c->cfg.nx;
+  unsigned long long* dh = nullptr;
+  double* ds = nullptr;
+  CUDA_TRY(c, cudaMallocAsync(&dh, n * sizeof(unsigned long long), c->stream));
+  CUDA_TRY(c, cudaMallocAsync(&ds, n * sizeof(double), c->stream));
+  hb::launch_row_audit(c->A, c->pitch, c->cfg.nx, c->cfg.ny, dh, ds, c->stream);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && row_hashes)
+    e = cudaMemcpyAsync(row_hashes, dh, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                        c->stream);
+  if (e == cudaSuccess && row_sums)
+    e = cudaMemcpyAsync(row_sums, ds, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+  cudaFreeAsync(dh, c->stream);
+  cudaFreeAsync(ds, c->stream);
+  CUDA_TRY(c, e);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_state_hash(hydro_gpu_ctx* c, uint64_t* out) {
+  if (!c || !out) return HYDRO_GPU_ERR_CONFIG;
+  std::vector<uint64_t> h(4 * (size_t)c->cfg.nx);
+  const int rc = hydro_gpu_row_audit(c, h.data(), nullptr);
+  if (rc) return rc;
+  *out = hydro_combine_row_hashes(h.data(), h.size());
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_totals(hydro_gpu_ctx* c, double out[4]) {
+  if (!c || !out) return HYDRO_GPU_ERR_CONFIG;
+  const int nx = c->cfg.nx;
+  std::vector<double> s(4 * (size_t)nx);
+  const int rc = hydro_gpu_row_audit(c, nullptr, s.data());
+  if (rc) return rc;
+  const double vol = c->cfg.dx * c->cfg.dy;
+  for (int v = 0; v < 4; ++v) out[v] = vol * hydro_pairwise_sum(s.data() + (size_t)v * nx, nx);
+  return HYDRO_GPU_OK;
+}
+
 int hydro_gpu_math_selftest(int op, const double* a, const double* b, double* fast,
                             double* exact, int* in_range, size_t n) {
   if (op < 0 || op > 2 || !a || !fast || !exact || !in_range) return HYDRO_GPU_ERR_CONFIG;

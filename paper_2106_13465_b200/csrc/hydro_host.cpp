@@ -10,6 +10,7 @@
 // Built with -ffp-contract=off like the reference (proj/CMakeLists.txt:10-14).
 #include <cstdint>
 #include <cstring>
+#include <vector>
 
 #include "../../include/hydro_gpu.h"
 
@@ -58,6 +59,46 @@ uint64_t hydro_grid_digest(const double* const planes[4], size_t stride, int nx,
     }
   }
   return h;
+}
+
+uint64_t hydro_combine_row_hashes(const uint64_t* row_hashes, size_t n) {
+  uint64_t h = 14695981039346656037ull;
+  for (size_t k = 0; k < n; ++k)
+    for (int b = 0; b < 8; ++b) {
+      h ^= (row_hashes[k] >> (8 * b)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  return h;
+}
+
+uint64_t hydro_grid_state_hash(const double* const planes[4], size_t stride, int nx, int ny) {
+  std::vector<uint64_t> rows(4 * (size_t)nx);
+  for (int v = 0; v < 4; ++v)
+    for (int i = 1; i <= nx; ++i) {
+      const double* row = planes[v] + (size_t)(i + 1) * stride + 2;
+      uint64_t h = 14695981039346656037ull;
+      for (int j = 0; j < ny; ++j) {
+        uint64_t bits;
+        std::memcpy(&bits, row + j, 8);
+        for (int b = 0; b < 8; ++b) {
+          h ^= (bits >> (8 * b)) & 0xffu;
+          h *= 1099511628211ull;
+        }
+      }
+      rows[(size_t)v * nx + (i - 1)] = h;
+    }
+  return hydro_combine_row_hashes(rows.data(), rows.size());
+}
+
+// pairwise_sum (audit.cpp:16-25): halve until blocks of <= 8.
+double hydro_pairwise_sum(const double* v, size_t n) {
+  if (n <= 8) {
+    double s = 0.0;
+    for (size_t k = 0; k < n; ++k) s += v[k];
+    return s;
+  }
+  const size_t h = n / 2;
+  return hydro_pairwise_sum(v, h) + hydro_pairwise_sum(v + h, n - h);
 }
 
 int hydro_init_case_host(int case_id, int nx, int ny, double gamma, uint64_t seed,

@@ -753,6 +753,35 @@ __global__ void init_kernel(InitArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Device-side audit: per-row FNV-1a hashes (the building block of the
+// composable state hash, see hydro_gpu_state_hash) and per-row sums of one
+// variable (fixed serial order: deterministic), one thread per (variable,
+// row).  The reference's digest (audit.cpp:53-76) is byte-serial over the
+// whole grid and stays a host step.
+__global__ void row_audit_kernel(const double* __restrict__ u, size_t pitch, int nx, int ny,
+                                 unsigned long long* __restrict__ hashes,
+                                 double* __restrict__ sums) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 4 * nx) return;
+  const int v = t / nx, i = t % nx + 1;
+  const double* row = u + cell_index(pitch, v, i, 1);
+  unsigned long long h = 14695981039346656037ull;
+  double sum = 0.0;
+  for (int j = 0; j < ny; ++j) {
+    const double x = __ldg(row + j);
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      h ^= (bits >> (8 * b)) & 0xffull;
+      h *= 1099511628211ull;
+    }
+    sum += x;
+  }
+  hashes[t] = h;
+  sums[t] = sum;
+}
+
 // FastMath against the compiler's IEEE operations (tests/test_gpu_math.py).
 __global__ void math_selftest_kernel(int op, const double* a, const double* b, double* fast,
                                      double* ref, int* okv, size_t n) {
@@ -871,6 +900,12 @@ void launch_finish(const FinishArgs& a, cudaStream_t s) {
 void launch_init(const InitArgs& a, cudaStream_t s) {
   dim3 grid((a.ny + 255) / 256, a.nx < 4096 ? a.nx : 4096);
   init_kernel<<<grid, 256, 0, s>>>(a);
+}
+
+void launch_row_audit(const double* u, size_t pitch, int nx, int ny, unsigned long long* hashes,
+                      double* sums, cudaStream_t s) {
+  const int n = 4 * nx;
+  row_audit_kernel<<<(n + 127) / 128, 128, 0, s>>>(u, pitch, nx, ny, hashes, sums);
 }
 
 void launch_math_selftest(int op, const double* a, const double* b, double* fast, double* ref,

@@ -109,6 +109,8 @@ void launch_sweep_y(const SweepArgs& a, const TmaMaps& maps, const Geometry& geo
 void launch_prologue(const PrologueArgs& a, cudaStream_t s);
 void launch_finish(const FinishArgs& a, cudaStream_t s);
 void launch_init(const InitArgs& a, cudaStream_t s);
+void launch_row_audit(const double* u, size_t pitch, int nx, int ny, unsigned long long* hashes,
+                      double* sums, cudaStream_t s);
 void launch_math_selftest(int op, const double* a, const double* b, double* fast, double* ref,
                           int* ok, size_t n, cudaStream_t s);
 

@@ -162,6 +162,17 @@ def grid_digest(grid: Grid2D) -> int:
     return int(L.lib().hydro_grid_digest(L.planes_of(grid.planes), grid.ny + 4, grid.nx, grid.ny))
 
 
+def grid_state_hash(grid: Grid2D) -> int:
+    """Composable state hash (FNV-1a over per-row FNV-1a hashes) of host planes;
+    equals GpuGrid.state_hash() of the same state."""
+    return int(L.lib().hydro_grid_state_hash(L.planes_of(grid.planes), grid.ny + 4, grid.nx, grid.ny))
+
+
+def combine_row_hashes(rows) -> int:
+    arr = np.ascontiguousarray(rows, dtype=np.uint64)
+    return int(L.lib().hydro_combine_row_hashes(arr.ctypes.data_as(C.POINTER(C.c_uint64)), arr.size))
+
+
 class GpuGrid:
     """One device-resident grid (or row slab): a hydro_gpu_ctx."""
 
@@ -301,6 +312,25 @@ class GpuGrid:
         info = L.ErrorInfo()
         rc = self._lib.hydro_gpu_decode_error(self._ctx, key, C.byref(info))
         _raise_for(rc, info)
+
+    # -- device-side audit -------------------------------------------------
+    def row_audit(self) -> tuple[np.ndarray, np.ndarray]:
+        """(row hashes, row sums), shape (4, nx) each, without downloading the grid."""
+        h = np.zeros(4 * self.nx, dtype=np.uint64)
+        s = np.zeros(4 * self.nx)
+        self._check(self._lib.hydro_gpu_row_audit(self._ctx, h.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                                  s.ctypes.data_as(L._dp)))
+        return h.reshape(4, self.nx), s.reshape(4, self.nx)
+
+    def state_hash(self) -> int:
+        out = C.c_uint64()
+        self._check(self._lib.hydro_gpu_state_hash(self._ctx, C.byref(out)))
+        return out.value
+
+    def totals(self) -> np.ndarray:
+        out = np.zeros(4)
+        self._check(self._lib.hydro_gpu_totals(self._ctx, out.ctypes.data_as(L._dp)))
+        return out
 
     # -- instrumentation ----------------------------------------------------
     def set_timing(self, on: bool):
