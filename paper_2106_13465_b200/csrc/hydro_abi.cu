@@ -217,7 +217,7 @@ void enqueue_x(hydro_gpu_ctx* c, int step, int explicit_dt, double dt) {
   a.dt_value = dt;
   cudaEvent_t e0{};
   ev_begin(c, &e0);
-  hb::launch_sweep_x(a, c->geo, c->stream);
+  hb::launch_sweep_x(a, c->maps, c->geo, c->stream);
   ev_end(c, e0, 0);
 }
 

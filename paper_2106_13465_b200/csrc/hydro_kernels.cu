@@ -217,10 +217,14 @@ __device__ __forceinline__ int claim(unsigned* counter) {
 #ifndef HB_X_MINB
 #define HB_X_MINB 4
 #endif
+#ifndef HB_X_TMA
+#define HB_X_TMA 1
+#endif
 #ifndef HB_Y_MINB
 #define HB_Y_MINB 4
 #endif
 
+#if !HB_X_TMA  // the register-prefetch column sweep (A/B reference)
 // ---------------------------------------------------------------------------
 // Column sweep: lane = column j, item = 32 columns x a segment of rows.
 
@@ -322,6 +326,8 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : 2) sweep_x_kernel
   }
 }
 
+#endif  // !HB_X_TMA
+
 // ---------------------------------------------------------------------------
 // Row sweep with TMA-staged tiles, one independent pipeline per warp.
 
@@ -377,27 +383,29 @@ __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// Row-sweep staging: a warp (one row per lane) walks a column segment in
-// chunks of kChunk columns.  Chunk Q holds strip cells [ka-4+4Q, ka-1+4Q]
-// of all four variables, laid out [v][row][col] (one TMA box {kChunk cols,
-// 1 var, 32 rows} per variable; 32-byte rows = whole DRAM sectors).  A ring
-// of kNBuf buffers is used in place: once a cell has been read into
-// registers its slot receives the updated cell (2 iterations later), and a
-// completed chunk leaves with TMA bulk-tensor stores before its buffer is
-// refilled kNBuf-1 chunks ahead.  Chunk numbering runs on across the warp's
-// items so buffer/phase bookkeeping never resets.
+// TMA staging (both sweeps): a warp (one strip per lane) walks a segment in
+// chunks of kChunk cells.  Chunk Q holds strip cells [ka-4+4Q, ka-1+4Q] of
+// all four variables, laid out [v][...] with one TMA box per variable:
+//   AXIS 1 (row sweep):    box {kChunk cols, 1 var, 32 rows}, slot [row][col]
+//   AXIS 0 (column sweep): box {32 cols, 1 var, kChunk rows}, slot [row][col]
+// so a lane's cell is 8 bytes at stride 32 B (row sweep) or consecutive
+// lanes read consecutive 8-byte words (column sweep).  Box rows are 32 or
+// 256 bytes: whole DRAM sectors.  A ring of kNBuf buffers is used in place:
+// once a cell has been read into registers its slot receives the updated
+// cell (2 iterations later), and a completed chunk leaves with TMA
+// bulk-tensor stores before its buffer is refilled kNBuf-1 chunks ahead.
+// Chunk numbering runs on across the warp's items so buffer/phase
+// bookkeeping never resets.
 constexpr int kVarBytes = 32 * kChunk * 8;
-__device__ __forceinline__ uint32_t slot(int r, int v, int c) {
-  return (uint32_t)(v * kVarBytes + r * (kChunk * 8) + c * 8);
-}
 
-struct RowTiles {
+template <int AXIS>
+struct Tiles {
   const CUtensorMap* load_map;
   const CUtensorMap* store_map;
   uint8_t* base;        // kNBuf consecutive kChunkBytes buffers of this warp
   uint64_t* full;       // kNBuf mbarriers of this warp
   int lane;
-  int i0;               // first grid row of the item
+  int s0;               // first strip of the item: column j0 (AXIS 0) or row i0 (AXIS 1)
   int ka, kb;           // output strip cells
   int nq;               // chunks of this item (cells ka-4 .. kb+2)
   unsigned q0;          // running chunk number of this item's chunk 0
@@ -406,14 +414,28 @@ struct RowTiles {
 
   __device__ __forceinline__ uint8_t* buf(int q) { return base + ((q0 + q) % kNBuf) * kChunkBytes; }
   __device__ __forceinline__ uint64_t* bar(int q) { return &full[(q0 + q) % kNBuf]; }
+  __device__ __forceinline__ uint32_t slot(int pos, int v) const {
+    return AXIS == 0 ? (uint32_t)(v * kVarBytes + pos * (32 * 8) + lane * 8)
+                     : (uint32_t)(v * kVarBytes + lane * (kChunk * 8) + pos * 8);
+  }
+  // Tensor coordinates {column offset, variable, plane row} of the chunk
+  // whose first strip cell is k (cell k is grid index k-1 along the strip).
+  __device__ __forceinline__ int c0(int k) const { return AXIS == 0 ? s0 + kColOff : k - 1 + kColOff; }
+  __device__ __forceinline__ int c2(int k) const { return AXIS == 0 ? k : s0 + 1; }
 
   __device__ __forceinline__ void issue(int q) {  // lane 0 only
     if (q >= nq) return;
     mbar_expect_tx(bar(q), kChunkBytes);
-    // strip cell k is column k-1, stored at column offset k-1+kColOff
-    const int col = ka - 4 + q * kChunk - 1 + kColOff;
+    const int k = ka - 4 + q * kChunk;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) tma_load(buf(q) + v * kVarBytes, load_map, bar(q), col, v, i0 + 1);
+    for (int v = 0; v < 4; ++v) tma_load(buf(q) + v * kVarBytes, load_map, bar(q), c0(k), v, c2(k));
+  }
+
+  // sweep orientation: mom_a is the momentum along the strip
+  __device__ __forceinline__ Cons get(const uint8_t* b, int pos) const {
+    constexpr int va = AXIS == 0 ? 1 : 2, vb = AXIS == 0 ? 2 : 1;
+    return {*(const double*)(b + slot(pos, 0)), *(const double*)(b + slot(pos, va)),
+            *(const double*)(b + slot(pos, vb)), *(const double*)(b + slot(pos, 3))};
   }
 
   __device__ __forceinline__ Cons load(int k) {
@@ -423,31 +445,29 @@ struct RowTiles {
       mbar_wait(bar(q), ((q0 + q) / kNBuf) & 1);
       ready = q;
     }
-    const uint8_t* b = buf(q);
-    // sweep orientation: mom_a = mom_y (variable 2), mom_b = mom_x
-    Cons u = {*(const double*)(b + slot(lane, 0, pos)), *(const double*)(b + slot(lane, 2, pos)),
-              *(const double*)(b + slot(lane, 1, pos)), *(const double*)(b + slot(lane, 3, pos))};
-    if (!active) u = {1.0, 0.0, 0.0, 1.0};  // rows past the grid: inert
+    Cons u = get(buf(q), pos);
+    if (!active) u = {1.0, 0.0, 0.0, 1.0};  // strips past the grid: inert
     return u;
   }
 
   // Cell k again (already staged; its slot is overwritten only by put(k)).
   __device__ __forceinline__ Cons reload(int k) {
     const int rel = k - ka + 4;
-    const uint8_t* b = buf(rel / kChunk);
-    const int pos = rel % kChunk;
-    return {*(const double*)(b + slot(lane, 0, pos)), *(const double*)(b + slot(lane, 2, pos)),
-            *(const double*)(b + slot(lane, 1, pos)), *(const double*)(b + slot(lane, 3, pos))};
+    return get(buf(rel / kChunk), rel % kChunk);
   }
 
-  __device__ __forceinline__ void put(int k, const Cons& u) {
+  // Cell k of strip `ln` (default: this lane's) receives u.
+  __device__ __forceinline__ void put(int k, const Cons& u, int ln = -1) {
+    constexpr int va = AXIS == 0 ? 1 : 2, vb = AXIS == 0 ? 2 : 1;
     const int rel = k - ka + 4;
     uint8_t* b = buf(rel / kChunk);
     const int pos = rel % kChunk;
-    *(double*)(b + slot(lane, 0, pos)) = u.r;
-    *(double*)(b + slot(lane, 2, pos)) = u.ma;
-    *(double*)(b + slot(lane, 1, pos)) = u.mb;
-    *(double*)(b + slot(lane, 3, pos)) = u.e;
+    const int sh = ln < 0 ? 0 : (ln - lane) * (AXIS == 0 ? 8 : kChunk * 8);
+    b += sh;
+    *(double*)(b + slot(pos, 0)) = u.r;
+    *(double*)(b + slot(pos, va)) = u.ma;
+    *(double*)(b + slot(pos, vb)) = u.mb;
+    *(double*)(b + slot(pos, 3)) = u.e;
   }
 
   // After iteration c: chunk boundaries fall on c - ka = 4T.
@@ -465,28 +485,40 @@ struct RowTiles {
     __syncwarp();
     if (lane == 0) {
       if (T >= 1) {
-        const int col = ka - 4 + T * kChunk - 1 + kColOff;
+        const int k = ka - 4 + T * kChunk;
 #pragma unroll
-        for (int v = 0; v < 4; ++v) tma_store(store_map, buf(T) + v * kVarBytes, col, v, i0 + 1);
+        for (int v = 0; v < 4; ++v) tma_store(store_map, buf(T) + v * kVarBytes, c0(k), v, c2(k));
         bulk_commit();
       }
       issue(T + kNBuf - 1);
     }
   }
+
+  // Stage the first chunks of an item / drain it.
+  __device__ __forceinline__ void begin() {
+    ready = -1;
+    if (lane == 0)
+      for (int q = 0; q < kNBuf - 1; ++q) issue(q);
+  }
+  __device__ __forceinline__ void end() {
+    const int seg = kb + 1 - ka;
+    if (seg % kChunk != 0) flush(seg / kChunk + 1);  // a short final chunk
+    if (lane == 0) bulk_wait_read0();                // the ring is free again
+    __syncwarp();
+    q0 += nq;
+  }
 };
 
-template <int FLUX>
-__global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel(SweepArgs a,
-                                                       const __grid_constant__ CUtensorMap load_map,
-                                                       const __grid_constant__ CUtensorMap store_map) {
-  extern __shared__ uint8_t smem_raw[];
-  if (latched(a)) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *a.counter_next = 0u;
+// Shared-memory carve-up of the staged sweeps: 4 warps x kNBuf chunk
+// buffers, then 4 x kNBuf mbarriers.
+template <int AXIS>
+__device__ __forceinline__ Tiles<AXIS> make_tiles(uint8_t* smem_raw, const CUtensorMap* load_map,
+                                                  const CUtensorMap* store_map) {
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  RowTiles t;
-  t.load_map = &load_map;
-  t.store_map = &store_map;
+  Tiles<AXIS> t;
+  t.load_map = load_map;
+  t.store_map = store_map;
   t.base = smem + warp * (kNBuf * kChunkBytes);
   t.full = (uint64_t*)(smem + 4 * kNBuf * kChunkBytes) + warp * kNBuf;
   t.lane = lane;
@@ -496,7 +528,107 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
+  return t;
+}
 
+// Column sweep with TMA-staged tiles (same pipeline as the row sweep).
+template <int FLUX>
+__global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : 2)
+    sweep_x_tma_kernel(SweepArgs a, const __grid_constant__ CUtensorMap load_map,
+                       const __grid_constant__ CUtensorMap store_map) {
+  extern __shared__ uint8_t smem_raw[];
+  if (latched(a)) return;
+  if (*(volatile unsigned long long*)a.dt_err != kNoError) {
+    // compute_dt of this step failed (detected by the previous row sweep).
+    if (blockIdx.x == 0 && threadIdx.x == 0) record(a.err, *(volatile unsigned long long*)a.dt_err);
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (a.limit_out) *a.limit_out = kEmptyLimit;
+    *a.counter_next = 0u;
+  }
+  Tiles<0> t = make_tiles<0>(smem_raw, &load_map, &store_map);
+  const int lane = t.lane;
+  const Gas g = make_gas(a.gamma);
+  const double dtdx = step_dt(a) / a.dx;
+  const size_t pitch = a.pitch;
+  const int ny = a.ny;
+  const bool refl = a.bc == 0;
+  const int groups = (ny + 31) >> 5;
+  const int items = groups * a.nseg;
+  double* __restrict__ dst = a.dst;
+  for (int item = claim(a.counter); item < items; item = claim(a.counter)) {
+    const int grp = item % groups, sg = item / groups;
+    const int j0 = (grp << 5) + 1;
+    const int j = j0 + lane;
+    const bool active = j <= ny;
+    const int i_lo = 1 + sg * a.seg;
+    const int i_hi = min(a.nx, i_lo + a.seg - 1);
+    t.s0 = j0;
+    t.ka = i_lo + 1;
+    t.kb = i_hi + 1;
+    t.nq = (t.kb + 2 - (t.ka - 4) + kChunk) / kChunk;
+    t.active = active;
+    // warps holding a y-wall column (1, 2, ny-1 or ny) write the ghost columns
+    const bool edge = grp == 0 || (grp << 5) + 32 >= ny - 1;
+    const unsigned long long base = error_key(a.step, 1, j, 0, 0, 0);
+    auto pass = [&](auto math) {
+      using M = decltype(math);
+      t.begin();
+      auto put = [&](int i, int jj, const Cons& u, bool neg) {
+        double* q = dst + cell_index(pitch, 0, i, jj);
+        q[0] = u.r;
+        q[pitch] = u.ma;
+        q[2 * pitch] = neg ? -u.mb : u.mb;
+        q[3 * pitch] = u.e;
+      };
+      auto sink = [&](int k, const StepOut& o) {
+        if (active) t.put(k, o.un);
+        if (edge && active) {  // y-wall ghosts of the column-sweep output (grid.cpp:44-59)
+          const int i = k - 1;
+          if (refl) {
+            if (j <= 2) put(i, 1 - j, o.un, true);
+            if (j >= ny - 1) put(i, 2 * ny + 1 - j, o.un, true);
+          } else {
+            if (j == 1) { put(i, 0, o.un, false); put(i, -1, o.un, false); }
+            if (j == ny) { put(i, ny + 1, o.un, false); put(i, ny + 2, o.un, false); }
+          }
+          // For odd ny the store box's last 16-byte unit (TMA clips stores at
+          // that granularity along the inner dimension) also covers ghost
+          // column ny+1: its slot gets the same ghost value the direct store
+          // above writes, so both writes agree.
+          if ((ny & 1) && j == ny) {
+            Cons gh = o.un;
+            if (refl) gh.mb = -gh.mb;
+            t.put(k, gh, lane + 1);
+          }
+        }
+      };
+      unsigned long long ek = kNoError;
+      const bool ok = walk_strip<M, false, FLUX>(t.ka, t.kb, t, sink, g, dtdx, 0.0, base, a.row0, ek);
+      t.end();
+      return make_pair_ok(ok, ek);
+    };
+    OkKey r = pass(FastMath{});
+    if (!__all_sync(0xffffffffu, r.ok || !active)) {
+      if (lane == 0) bulk_wait0();  // the fast pass's stores have landed
+      __syncwarp();
+      r = pass(ExactMath{});
+    }
+    if (active && r.key != kNoError) record(a.err, r.key);
+  }
+  if (lane == 0) bulk_wait0();
+}
+
+template <int FLUX>
+__global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel(SweepArgs a,
+                                                       const __grid_constant__ CUtensorMap load_map,
+                                                       const __grid_constant__ CUtensorMap store_map) {
+  extern __shared__ uint8_t smem_raw[];
+  if (latched(a)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.counter_next = 0u;
+  Tiles<1> t = make_tiles<1>(smem_raw, &load_map, &store_map);
+  const int lane = t.lane;
   const Gas g = make_gas(a.gamma);
   const double dtdx = step_dt(a) / a.dx;
   const size_t pitch = a.pitch;
@@ -515,7 +647,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
     const bool active = i <= nx;
     const int j_lo = 1 + sg * a.seg;
     const int j_hi = min(a.ny, j_lo + a.seg - 1);
-    t.i0 = i0;
+    t.s0 = i0;
     t.ka = j_lo + 1;
     t.kb = j_hi + 1;
     t.nq = (t.kb + 2 - (t.ka - 4) + kChunk) / kChunk;
@@ -539,9 +671,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
       using M = decltype(math);
       lim_item = __longlong_as_double(0x7ff0000000000000ll);
       dt_item = kNoError;
-      t.ready = -1;
-      if (lane == 0)
-        for (int q = 0; q < kNBuf - 1; ++q) t.issue(q);
+      t.begin();
       auto sink = [&](int k, const StepOut& o) {
         t.put(k, o.un);
         const int j = k - 1;
@@ -563,12 +693,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
           a.want_limit
               ? walk_strip<M, true, FLUX>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, base, 0, ek)
               : walk_strip<M, false, FLUX>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, base, 0, ek);
-      // a final segment shorter than whole chunks leaves one chunk unstored
-      const int seg = t.kb + 1 - t.ka;
-      if (seg % kChunk != 0) t.flush(seg / kChunk + 1);
-      if (lane == 0) bulk_wait_read0();  // the ring is free again
-      __syncwarp();
-      t.q0 += t.nq;
+      t.end();
       return make_pair_ok(ok, ek);
     };
     OkKey r = pass(FastMath{});
@@ -824,9 +949,16 @@ int query_geometry(Geometry* g) {
   cudaFuncSetAttribute(sweep_y_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
   cudaFuncSetAttribute(sweep_y_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
   int ox = 0, oy = 0, ox1 = 0, oy1 = 0;
+#if HB_X_TMA
+  cudaFuncSetAttribute(sweep_x_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
+  cudaFuncSetAttribute(sweep_x_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, sweep_x_tma_kernel<0>, 128, kYSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox1, sweep_x_tma_kernel<1>, 128, kYSmemBytes);
+#else
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, sweep_x_kernel<0>, 128, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy, sweep_y_kernel<0>, 128, kYSmemBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox1, sweep_x_kernel<1>, 128, 0);
+#endif
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy, sweep_y_kernel<0>, 128, kYSmemBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy1, sweep_y_kernel<1>, 128, kYSmemBytes);
   g->ctas_x_per_sm = ox > 0 ? ox : 1;
   g->ctas_y_per_sm = oy > 0 ? oy : 1;
@@ -847,31 +979,50 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
     encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
   }
   const cuuint64_t strides[2] = {pitch * 8, 4 * pitch * 8};
-  const cuuint32_t box[3] = {(cuuint32_t)kChunk, 1, 32};
   const cuuint32_t estr[3] = {1, 1, 1};
-  // load: all of U_b (ghost rows/columns included)
+  // loads: the whole state buffer (ghost rows/columns included; boxes
+  // reaching past it are zero-filled)
   const cuuint64_t dim_load[3] = {pitch, 4, (cuuint64_t)nx + 4};
-  CUresult r1 = encode(&maps->y_load, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, B, dim_load, strides,
-                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  // store: rows -1..nx (the tail CTA's rows past nx are clipped) and
-  // column offsets up to j = ny (a short final segment is clipped)
+  // stores: interior only -- rows up to nx and column offsets up to j = ny,
+  // so tail items past the grid are clipped (ghosts are written separately)
   const cuuint64_t dim_store[3] = {(cuuint64_t)ny + 1 + kColOff, 4, (cuuint64_t)nx + 2};
-  CUresult r2 = encode(&maps->y_store, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, A, dim_store, strides,
-                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r1 == CUDA_SUCCESS && r2 == CUDA_SUCCESS;
+  // column-sweep stores: the inner extent rounded up to whole 16-byte units,
+  // which is what TMA writes; the odd ghost column ny+1 this adds carries the
+  // ghost value (sweep_x_tma_kernel)
+  const cuuint64_t dim_xstore[3] = {((cuuint64_t)ny + 2 + kColOff) & ~(cuuint64_t)1, 4,
+                                    (cuuint64_t)nx + 2};
+  auto enc = [&](CUtensorMap* m, double* base, const cuuint64_t* dim, const cuuint32_t* box) {
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dim, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+  };
+  const cuuint32_t box_y[3] = {(cuuint32_t)kChunk, 1, 32};  // row sweep: 4 cols x 32 rows
+  const cuuint32_t box_x[3] = {32, 1, (cuuint32_t)kChunk};  // column sweep: 32 cols x 4 rows
+  return enc(&maps->y_load, B, dim_load, box_y) && enc(&maps->y_store, A, dim_store, box_y) &&
+         enc(&maps->x_load, A, dim_load, box_x) && enc(&maps->x_store, B, dim_xstore, box_x);
 }
 
-void launch_sweep_x(const SweepArgs& a0, const Geometry& geo, cudaStream_t s) {
+void launch_sweep_x(const SweepArgs& a0, const TmaMaps& maps, const Geometry& geo,
+                    cudaStream_t s) {
   SweepArgs a = a0;
   const int ctas = geo.sms * (a.flux == 1 ? geo.ctas_x_exact : geo.ctas_x_per_sm);
   if (a.seg <= 0) a.seg = pick_seg(a.nx, a.ny, ctas * 4);
+#if HB_X_TMA
+  a.seg = (a.seg + kChunk - 1) / kChunk * kChunk;  // chunks never straddle segments
+#endif
   a.nseg = (a.nx + a.seg - 1) / a.seg;
+#if HB_X_TMA
+  if (a.flux == 1)
+    sweep_x_tma_kernel<1><<<ctas, 128, kYSmemBytes, s>>>(a, maps.x_load, maps.x_store);
+  else
+    sweep_x_tma_kernel<0><<<ctas, 128, kYSmemBytes, s>>>(a, maps.x_load, maps.x_store);
+#else
   if (a.flux == 1)
     sweep_x_kernel<1><<<ctas, 128, 0, s>>>(a);
   else
     sweep_x_kernel<0><<<ctas, 128, 0, s>>>(a);
+#endif
 }
 
 void launch_sweep_y(const SweepArgs& a0, const TmaMaps& maps, const Geometry& geo,

@@ -63,6 +63,8 @@ struct SweepArgs {
 struct TmaMaps {
   CUtensorMap y_load;         // U_b, box {kChunk cols, 1 var, 32 rows}
   CUtensorMap y_store;        // U_a interior rows/cols only (clips ghosts)
+  CUtensorMap x_load;         // U_a, box {32 cols, 1 var, kChunk rows}
+  CUtensorMap x_store;        // U_b interior only
 };
 
 struct PrologueArgs {
@@ -104,7 +106,7 @@ struct Geometry {
 
 bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, int ny);
 int query_geometry(Geometry* g);
-void launch_sweep_x(const SweepArgs& a, const Geometry& geo, cudaStream_t s);
+void launch_sweep_x(const SweepArgs& a, const TmaMaps& maps, const Geometry& geo, cudaStream_t s);
 void launch_sweep_y(const SweepArgs& a, const TmaMaps& maps, const Geometry& geo, cudaStream_t s);
 void launch_prologue(const PrologueArgs& a, cudaStream_t s);
 void launch_finish(const FinishArgs& a, cudaStream_t s);

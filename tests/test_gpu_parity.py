@@ -71,6 +71,17 @@ def test_every_plane_and_ghost_matches_oracle(gpu, case, nx, ny, steps, bc, seed
     assert dt == dt_ref
 
 
+@pytest.mark.parametrize("ny", [35, 45, 63, 65])
+@pytest.mark.parametrize("bc", ["transmit", "reflect"])
+def test_odd_width_wall_ghosts(gpu, ny, bc):
+    """Odd ny: the column sweep's last TMA store unit straddles the y-wall
+    ghost column ny+1 (stores clip at 16-byte granularity), which must still
+    carry the ghost value."""
+    a, _ = gpu_run("random", 24, ny, 3, bc, 9)
+    ref, _ = oracle_run("random", 24, ny, 3, bc, 9)
+    assert np.array_equal(a.planes, ref.u)
+
+
 @pytest.mark.parametrize("seg", [(1, 2, 0), (3, 4, 0), (7, 1000, 128), (1000, 6, 0), (5, 1, 0)])
 def test_launch_geometry_does_not_change_bits(gpu, seg):
     """Strip segmentation is an execution detail: any split is bitwise equal
