@@ -398,12 +398,17 @@ __device__ __forceinline__ void fence_async_smem() {
 // bookkeeping never resets.
 constexpr int kVarBytes = 32 * kChunk * 8;
 
+// The staged sweeps' dynamic shared memory.  Addressing it as hb_smem +
+// offset (rather than through generic pointers) lets the compiler emit
+// LDS/STS with 32-bit addresses.
+extern __shared__ __align__(128) uint8_t hb_smem[];
+
 template <int AXIS>
 struct Tiles {
   const CUtensorMap* load_map;
   const CUtensorMap* store_map;
-  uint8_t* base;        // kNBuf consecutive kChunkBytes buffers of this warp
-  uint64_t* full;       // kNBuf mbarriers of this warp
+  uint32_t base;        // offset of this warp's kNBuf consecutive kChunkBytes buffers
+  uint32_t full;        // offset of this warp's kNBuf mbarriers
   int lane;
   int s0;               // first strip of the item: column j0 (AXIS 0) or row i0 (AXIS 1)
   int ka, kb;           // output strip cells
@@ -412,8 +417,12 @@ struct Tiles {
   int ready;            // highest local chunk this lane has waited for
   bool active;
 
-  __device__ __forceinline__ uint8_t* buf(int q) { return base + ((q0 + q) % kNBuf) * kChunkBytes; }
-  __device__ __forceinline__ uint64_t* bar(int q) { return &full[(q0 + q) % kNBuf]; }
+  __device__ __forceinline__ uint8_t* buf(int q) {
+    return hb_smem + base + ((q0 + q) % kNBuf) * kChunkBytes;
+  }
+  __device__ __forceinline__ uint64_t* bar(int q) {
+    return (uint64_t*)(hb_smem + full) + (q0 + q) % kNBuf;
+  }
   __device__ __forceinline__ uint32_t slot(int pos, int v) const {
     return AXIS == 0 ? (uint32_t)(v * kVarBytes + pos * (32 * 8) + lane * 8)
                      : (uint32_t)(v * kVarBytes + lane * (kChunk * 8) + pos * 8);
@@ -512,19 +521,19 @@ struct Tiles {
 // Shared-memory carve-up of the staged sweeps: 4 warps x kNBuf chunk
 // buffers, then 4 x kNBuf mbarriers.
 template <int AXIS>
-__device__ __forceinline__ Tiles<AXIS> make_tiles(uint8_t* smem_raw, const CUtensorMap* load_map,
+__device__ __forceinline__ Tiles<AXIS> make_tiles(const CUtensorMap* load_map,
                                                   const CUtensorMap* store_map) {
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+  const uint32_t pad = (128u - (smem_u32(hb_smem) & 127u)) & 127u;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   Tiles<AXIS> t;
   t.load_map = load_map;
   t.store_map = store_map;
-  t.base = smem + warp * (kNBuf * kChunkBytes);
-  t.full = (uint64_t*)(smem + 4 * kNBuf * kChunkBytes) + warp * kNBuf;
+  t.base = pad + warp * (kNBuf * kChunkBytes);
+  t.full = pad + 4 * kNBuf * kChunkBytes + warp * kNBuf * 8;
   t.lane = lane;
   t.q0 = 0;
   if (lane == 0) {
-    for (int q = 0; q < kNBuf; ++q) mbar_init(&t.full[q], 1);
+    for (int q = 0; q < kNBuf; ++q) mbar_init((uint64_t*)(hb_smem + t.full) + q, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
@@ -536,7 +545,6 @@ template <int FLUX>
 __global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : 2)
     sweep_x_tma_kernel(SweepArgs a, const __grid_constant__ CUtensorMap load_map,
                        const __grid_constant__ CUtensorMap store_map) {
-  extern __shared__ uint8_t smem_raw[];
   if (latched(a)) return;
   if (*(volatile unsigned long long*)a.dt_err != kNoError) {
     // compute_dt of this step failed (detected by the previous row sweep).
@@ -547,7 +555,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : 2)
     if (a.limit_out) *a.limit_out = kEmptyLimit;
     *a.counter_next = 0u;
   }
-  Tiles<0> t = make_tiles<0>(smem_raw, &load_map, &store_map);
+  Tiles<0> t = make_tiles<0>(&load_map, &store_map);
   const int lane = t.lane;
   const Gas g = make_gas(a.gamma);
   const double dtdx = step_dt(a) / a.dx;
@@ -624,10 +632,9 @@ template <int FLUX>
 __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel(SweepArgs a,
                                                        const __grid_constant__ CUtensorMap load_map,
                                                        const __grid_constant__ CUtensorMap store_map) {
-  extern __shared__ uint8_t smem_raw[];
   if (latched(a)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.counter_next = 0u;
-  Tiles<1> t = make_tiles<1>(smem_raw, &load_map, &store_map);
+  Tiles<1> t = make_tiles<1>(&load_map, &store_map);
   const int lane = t.lane;
   const Gas g = make_gas(a.gamma);
   const double dtdx = step_dt(a) / a.dx;
