@@ -926,6 +926,9 @@ __global__ void math_selftest_kernel(int op, const double* a, const double* b, d
   } else if (op == 2) {
     fast[t] = fm.divz(a[t], b[t]);
     ref[t] = a[t] / b[t];
+  } else if (op == 3) {  // minmod of the differences (a, b)
+    fast[t] = minmod_d_fast(a[t], b[t]);
+    ref[t] = minmod_d(a[t], b[t]);
   } else {
     fast[t] = fm.sqrt(a[t]);
     ref[t] = sqrt(a[t]);

@@ -109,3 +109,20 @@ def test_signed_zero_division_any_denominator_sign():
     a = rng.uniform(-5, 5, b.size)
     fast, exact, ok = run(2, a, b)
     assert ok.all() and np.array_equal(bits(fast), bits(exact))
+
+
+def test_minmod_fast_equals_reference_comparisons():
+    """minmod_d_fast (integer sign/zero tests, one FP64 compare) == the
+    reference's slope_minmod (euler_kernel.cpp:41-47) for every non-NaN pair:
+    signed zeros, infinities, denormals, ties of equal magnitude."""
+    rng = np.random.default_rng(41)
+    x = operands(rng, 1 << 18)
+    x = x[~np.isnan(x)]
+    y = rng.permutation(x)
+    ties = rng.choice(x, 4096)
+    edge = np.array([0.0, -0.0, np.inf, -np.inf, 5e-324, -5e-324, 1.0, -1.0])
+    ea, eb = np.meshgrid(edge, edge)
+    a = np.concatenate([x, ties, -ties, ea.ravel()])
+    b = np.concatenate([y, ties, -ties, eb.ravel()])
+    fast, exact, ok = run(3, a, b)
+    assert np.array_equal(bits(fast), bits(exact))
