@@ -454,9 +454,9 @@ struct Tiles {
       mbar_wait(bar(q), ((q0 + q) / kNBuf) & 1);
       ready = q;
     }
-    Cons u = get(buf(q), pos);
-    if (!active) u = {1.0, 0.0, 0.0, 1.0};  // strips past the grid: inert
-    return u;
+    // strips past the grid compute on whatever the box holds (zero fill,
+    // ghost or padding cells); their results, flags and errors are masked
+    return get(buf(q), pos);
   }
 
   // Cell k again (already staged; its slot is overwritten only by put(k)).
