@@ -405,6 +405,10 @@ extern __shared__ __align__(128) uint8_t hb_smem[];
 
 template <int AXIS>
 struct Tiles {
+  // smem bytes between consecutive cells of a strip / adjacent strips
+  static constexpr uint32_t kPosBytes = AXIS == 0 ? 32 * 8 : 8;
+  static constexpr uint32_t kLaneBytes = AXIS == 0 ? 8 : kChunk * 8;
+
   const CUtensorMap* load_map;
   const CUtensorMap* store_map;
   uint32_t base;        // offset of this warp's kNBuf consecutive kChunkBytes buffers
@@ -414,18 +418,21 @@ struct Tiles {
   int ka, kb;           // output strip cells
   int nq;               // chunks of this item (cells ka-4 .. kb+2)
   unsigned q0;          // running chunk number of this item's chunk 0
-  int ready;            // highest local chunk this lane has waited for
+  int T;                // next chunk to complete (flush)
   bool active;
+  // Per-cell cursors (hb_smem offsets of this lane's variable-0 slot): the
+  // next cell to load, and the cell being updated (reload + put).  The
+  // walker visits cells in order, so they advance by one slot per cell
+  // instead of recomputing chunk/buffer indices.
+  uint32_t lo_addr, wr_addr;
+  int lo_pos, lo_buf, wr_pos, wr_buf;
+  unsigned lo_par;      // mbarrier phase parity of the load cursor's buffer
 
   __device__ __forceinline__ uint8_t* buf(int q) {
     return hb_smem + base + ((q0 + q) % kNBuf) * kChunkBytes;
   }
   __device__ __forceinline__ uint64_t* bar(int q) {
     return (uint64_t*)(hb_smem + full) + (q0 + q) % kNBuf;
-  }
-  __device__ __forceinline__ uint32_t slot(int pos, int v) const {
-    return AXIS == 0 ? (uint32_t)(v * kVarBytes + pos * (32 * 8) + lane * 8)
-                     : (uint32_t)(v * kVarBytes + lane * (kChunk * 8) + pos * 8);
   }
   // Tensor coordinates {column offset, variable, plane row} of the chunk
   // whose first strip cell is k (cell k is grid index k-1 along the strip).
@@ -441,78 +448,98 @@ struct Tiles {
   }
 
   // sweep orientation: mom_a is the momentum along the strip
-  __device__ __forceinline__ Cons get(const uint8_t* b, int pos) const {
+  __device__ __forceinline__ Cons get(uint32_t at) const {
     constexpr int va = AXIS == 0 ? 1 : 2, vb = AXIS == 0 ? 2 : 1;
-    return {*(const double*)(b + slot(pos, 0)), *(const double*)(b + slot(pos, va)),
-            *(const double*)(b + slot(pos, vb)), *(const double*)(b + slot(pos, 3))};
+    const uint8_t* b = hb_smem + at;
+    return {*(const double*)(b), *(const double*)(b + va * kVarBytes),
+            *(const double*)(b + vb * kVarBytes), *(const double*)(b + 3 * kVarBytes)};
   }
 
-  __device__ __forceinline__ Cons load(int k) {
-    const int rel = k - ka + 4;
-    const int q = rel / kChunk, pos = rel % kChunk;
-    if (q > ready) {
-      mbar_wait(bar(q), ((q0 + q) / kNBuf) & 1);
-      ready = q;
+  // Cell k (= the load cursor's cell: ka-2, ka-1, ... in order).  Strips
+  // past the grid compute on whatever the box holds (zero fill, ghost or
+  // padding cells); their results, flags and errors are masked.
+  __device__ __forceinline__ Cons load(int) {
+    if (lo_pos == 0) mbar_wait((uint64_t*)(hb_smem + full) + lo_buf, lo_par);
+    const Cons u = get(lo_addr);
+    lo_addr += kPosBytes;
+    if (++lo_pos == kChunk) {
+      lo_pos = 0;
+      lo_addr += kChunkBytes - kChunk * kPosBytes;
+      if (++lo_buf == kNBuf) {
+        lo_buf = 0;
+        lo_addr -= kNBuf * kChunkBytes;
+        lo_par ^= 1u;
+      }
     }
-    // strips past the grid compute on whatever the box holds (zero fill,
-    // ghost or padding cells); their results, flags and errors are masked
-    return get(buf(q), pos);
+    return u;
   }
 
-  // Cell k again (already staged; its slot is overwritten only by put(k)).
-  __device__ __forceinline__ Cons reload(int k) {
-    const int rel = k - ka + 4;
-    return get(buf(rel / kChunk), rel % kChunk);
-  }
+  // The cell being updated, again (staged; its slot is overwritten only by put).
+  __device__ __forceinline__ Cons reload(int) { return get(wr_addr); }
 
-  // Cell k of strip `ln` (default: this lane's) receives u.
-  __device__ __forceinline__ void put(int k, const Cons& u, int ln = -1) {
+  // The cell being updated, of strip `ln` (default: this lane's), receives u.
+  __device__ __forceinline__ void put(int, const Cons& u, int ln = -1) {
     constexpr int va = AXIS == 0 ? 1 : 2, vb = AXIS == 0 ? 2 : 1;
-    const int rel = k - ka + 4;
-    uint8_t* b = buf(rel / kChunk);
-    const int pos = rel % kChunk;
-    const int sh = ln < 0 ? 0 : (ln - lane) * (AXIS == 0 ? 8 : kChunk * 8);
-    b += sh;
-    *(double*)(b + slot(pos, 0)) = u.r;
-    *(double*)(b + slot(pos, va)) = u.ma;
-    *(double*)(b + slot(pos, vb)) = u.mb;
-    *(double*)(b + slot(pos, 3)) = u.e;
+    uint8_t* b = hb_smem + wr_addr + (ln < 0 ? 0 : (ln - lane) * (int)kLaneBytes);
+    *(double*)(b) = u.r;
+    *(double*)(b + va * kVarBytes) = u.ma;
+    *(double*)(b + vb * kVarBytes) = u.mb;
+    *(double*)(b + 3 * kVarBytes) = u.e;
   }
 
-  // After iteration c: chunk boundaries fall on c - ka = 4T.
+  // After iteration c (cell c-1 updated for c > ka): advance the update
+  // cursor; chunk boundaries fall on c - ka = 4T.
   __device__ __forceinline__ void boundary(int c) {
-    const int rel = c - ka;
-    if (rel < 0 || (rel % kChunk) != 0) return;
-    flush(rel / kChunk);
+    if (c > ka) {
+      wr_addr += kPosBytes;
+      if (++wr_pos == kChunk) {
+        wr_pos = 0;
+        wr_addr += kChunkBytes - kChunk * kPosBytes;
+        if (++wr_buf == kNBuf) {
+          wr_buf = 0;
+          wr_addr -= kNBuf * kChunkBytes;
+        }
+      }
+    }
+    if (c >= ka && wr_pos == 0) flush(T++);
   }
 
   // Chunk T's outputs are complete: store it, refill the buffer of chunk
   // T-1 (stored at the previous boundary) with chunk T+kNBuf-1.
-  __device__ __forceinline__ void flush(int T) {
-    if (lane == 0) bulk_wait_read0();  // chunk T-1's stores have left smem
+  __device__ __forceinline__ void flush(int t) {
+    if (lane == 0) bulk_wait_read0();  // chunk t-1's stores have left smem
     fence_async_smem();                // this lane's slot writes -> async proxy
     __syncwarp();
     if (lane == 0) {
-      if (T >= 1) {
-        const int k = ka - 4 + T * kChunk;
+      if (t >= 1) {
+        const int k = ka - 4 + t * kChunk;
 #pragma unroll
-        for (int v = 0; v < 4; ++v) tma_store(store_map, buf(T) + v * kVarBytes, c0(k), v, c2(k));
+        for (int v = 0; v < 4; ++v) tma_store(store_map, buf(t) + v * kVarBytes, c0(k), v, c2(k));
         bulk_commit();
       }
-      issue(T + kNBuf - 1);
+      issue(t + kNBuf - 1);
     }
   }
 
-  // Stage the first chunks of an item / drain it.
+  // Stage the first chunks of an item (the first load is cell ka-2, slot 2
+  // of chunk 0; the first update is cell ka, slot 0 of chunk 1) / drain it.
   __device__ __forceinline__ void begin() {
-    ready = -1;
+    T = 0;
+    const int b0 = (int)(q0 % kNBuf), b1 = (b0 + 1) % kNBuf;
+    lo_buf = b0;
+    lo_pos = 2;
+    lo_par = (q0 / kNBuf) & 1u;
+    lo_addr = base + b0 * kChunkBytes + 2 * kPosBytes + lane * kLaneBytes;
+    wr_buf = b1;
+    wr_pos = 0;
+    wr_addr = base + b1 * kChunkBytes + lane * kLaneBytes;
     if (lane == 0)
       for (int q = 0; q < kNBuf - 1; ++q) issue(q);
+    mbar_wait((uint64_t*)(hb_smem + full) + lo_buf, lo_par);
   }
   __device__ __forceinline__ void end() {
-    const int seg = kb + 1 - ka;
-    if (seg % kChunk != 0) flush(seg / kChunk + 1);  // a short final chunk
-    if (lane == 0) bulk_wait_read0();                // the ring is free again
+    if (wr_pos != 0) flush(T);          // a short final chunk
+    if (lane == 0) bulk_wait_read0();   // the ring is free again
     __syncwarp();
     q0 += nq;
   }
