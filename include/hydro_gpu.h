@@ -179,8 +179,9 @@ int hydro_gpu_reset_counters(hydro_gpu_ctx* ctx);
 /* Launch-geometry override (0 = default): strip segment length along the
  * column and row sweeps; block must be 0 or 128. */
 int hydro_gpu_tune(hydro_gpu_ctx* ctx, int seg_x, int seg_y, int block);
-/* Self-test of the device fp64 division (op 0), square root (op 1) and
- * signed-zero-safe division (op 2) fast paths against the compiler's IEEE
+/* Self-test of the device fp64 division (op 0), square root (op 1),
+ * signed-zero-safe division (op 2) and density division (op 4: zero
+ * numerators, positive denominators) fast paths against the compiler's IEEE
  * operations on n operand pairs (b ignored for sqrt), and of the fast-pass
  * minmod of two slopes (op 3) against the reference's comparisons.
  * in_range[k] = 1 where the fast path applied. */

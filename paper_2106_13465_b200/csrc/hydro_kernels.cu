@@ -947,7 +947,10 @@ __global__ void math_selftest_kernel(int op, const double* a, const double* b, d
   const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (t >= n) return;
   FastMath fm;
-  if (op == 0) {
+  if (op == 0) {  // general quotient (any signs)
+    fast[t] = fm.divnf(a[t], b[t]);
+    ref[t] = a[t] / b[t];
+  } else if (op == 4) {  // density quotient (zero numerators, positive denominators)
     fast[t] = fm.divf(a[t], b[t]);
     ref[t] = a[t] / b[t];
   } else if (op == 2) {

@@ -87,13 +87,25 @@ def test_division_zero_numerator_fast_and_signed():
     b = np.concatenate([rng.uniform(1e-300, 1e300, 4096), rng.uniform(1e-6, 1e6, 4096)])
     for zero in (0.0, -0.0):
         a = np.full(b.size, zero)
-        fast, exact, ok = run(0, a, b)
+        fast, exact, ok = run(4, a, b)
         assert ok.all()
         assert np.array_equal(bits(fast), bits(exact))
         assert np.array_equal(bits(fast), bits(a / b))
     # negative or non-normal denominators leave the fast path (exact recompute)
-    _, _, ok = run(0, np.array([-0.0, 0.0, 0.0, 0.0]), np.array([-2.0, 0.0, 5e-324, np.inf]))
+    _, _, ok = run(4, np.array([-0.0, 0.0, 0.0, 0.0, 1.0]),
+                   np.array([-2.0, 0.0, 5e-324, np.inf, -3.0]))
     assert not ok.any()
+
+
+def test_density_division_sign_or_is_ieee():
+    """op 4 (velocities, internal energy: x / rho): the quotient's sign bit is
+    OR-ed with the numerator's, exact for positive normal denominators."""
+    rng = np.random.default_rng(11)
+    a = operands(rng, 1 << 20)
+    b = np.abs(rng.permutation(operands(rng, 1 << 20))[: a.size])
+    fast, exact, ok = run(4, a, b)
+    assert ok.mean() > 0.8
+    assert np.array_equal(bits(fast[ok]), bits(exact[ok]))
 
 
 def test_signed_zero_division_any_denominator_sign():
