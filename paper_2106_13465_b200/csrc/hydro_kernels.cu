@@ -385,9 +385,11 @@ __device__ __forceinline__ void fence_async_smem() {
 
 // TMA staging (both sweeps): a warp (one strip per lane) walks a segment in
 // chunks of kChunk cells.  Chunk Q holds strip cells [ka-4+4Q, ka-1+4Q] of
-// all four variables, laid out [v][...] with one TMA box per variable:
-//   AXIS 1 (row sweep):    box {kChunk cols, 1 var, 32 rows}, slot [row][col]
-//   AXIS 0 (column sweep): box {32 cols, 1 var, kChunk rows}, slot [row][col]
+// all four variables:
+//   AXIS 1 (row sweep):    one box {kChunk cols, 1 var, 32 rows} per
+//                          variable, smem [var][row][col]
+//   AXIS 0 (column sweep): one box {32 cols, 4 vars, kChunk rows},
+//                          smem [row][var][col]
 // so a lane's cell is 8 bytes at stride 32 B (row sweep) or consecutive
 // lanes read consecutive 8-byte words (column sweep).  Box rows are 32 or
 // 256 bytes: whole DRAM sectors.  A ring of kNBuf buffers is used in place:
@@ -406,8 +408,12 @@ extern __shared__ __align__(128) uint8_t hb_smem[];
 template <int AXIS>
 struct Tiles {
   // smem bytes between consecutive cells of a strip / adjacent strips
-  static constexpr uint32_t kPosBytes = AXIS == 0 ? 32 * 8 : 8;
+  // AXIS 0: one box {32 cols, 4 vars, kChunk rows} per chunk, slot
+  //   [pos][var][lane]; AXIS 1: one box {kChunk cols, 1 var, 32 rows} per
+  //   variable, slot [var][lane][pos].
+  static constexpr uint32_t kPosBytes = AXIS == 0 ? 4 * 32 * 8 : 8;
   static constexpr uint32_t kLaneBytes = AXIS == 0 ? 8 : kChunk * 8;
+  static constexpr uint32_t kVarStride = AXIS == 0 ? 32 * 8 : kVarBytes;
 
   const CUtensorMap* load_map;
   const CUtensorMap* store_map;
@@ -443,16 +449,20 @@ struct Tiles {
     if (q >= nq) return;
     mbar_expect_tx(bar(q), kChunkBytes);
     const int k = ka - 4 + q * kChunk;
+    if constexpr (AXIS == 0) {
+      tma_load(buf(q), load_map, bar(q), c0(k), 0, c2(k));
+    } else {
 #pragma unroll
-    for (int v = 0; v < 4; ++v) tma_load(buf(q) + v * kVarBytes, load_map, bar(q), c0(k), v, c2(k));
+      for (int v = 0; v < 4; ++v) tma_load(buf(q) + v * kVarBytes, load_map, bar(q), c0(k), v, c2(k));
+    }
   }
 
   // sweep orientation: mom_a is the momentum along the strip
   __device__ __forceinline__ Cons get(uint32_t at) const {
     constexpr int va = AXIS == 0 ? 1 : 2, vb = AXIS == 0 ? 2 : 1;
     const uint8_t* b = hb_smem + at;
-    return {*(const double*)(b), *(const double*)(b + va * kVarBytes),
-            *(const double*)(b + vb * kVarBytes), *(const double*)(b + 3 * kVarBytes)};
+    return {*(const double*)(b), *(const double*)(b + va * kVarStride),
+            *(const double*)(b + vb * kVarStride), *(const double*)(b + 3 * kVarStride)};
   }
 
   // Cell k (= the load cursor's cell: ka-2, ka-1, ... in order).  Strips
@@ -482,9 +492,9 @@ struct Tiles {
     constexpr int va = AXIS == 0 ? 1 : 2, vb = AXIS == 0 ? 2 : 1;
     uint8_t* b = hb_smem + wr_addr + (ln < 0 ? 0 : (ln - lane) * (int)kLaneBytes);
     *(double*)(b) = u.r;
-    *(double*)(b + va * kVarBytes) = u.ma;
-    *(double*)(b + vb * kVarBytes) = u.mb;
-    *(double*)(b + 3 * kVarBytes) = u.e;
+    *(double*)(b + va * kVarStride) = u.ma;
+    *(double*)(b + vb * kVarStride) = u.mb;
+    *(double*)(b + 3 * kVarStride) = u.e;
   }
 
   // After iteration c (cell c-1 updated for c > ka): advance the update
@@ -513,8 +523,12 @@ struct Tiles {
     if (lane == 0) {
       if (t >= 1) {
         const int k = ka - 4 + t * kChunk;
+        if constexpr (AXIS == 0) {
+          tma_store(store_map, buf(t), c0(k), 0, c2(k));
+        } else {
 #pragma unroll
-        for (int v = 0; v < 4; ++v) tma_store(store_map, buf(t) + v * kVarBytes, c0(k), v, c2(k));
+          for (int v = 0; v < 4; ++v) tma_store(store_map, buf(t) + v * kVarBytes, c0(k), v, c2(k));
+        }
         bulk_commit();
       }
       issue(t + kNBuf - 1);
@@ -1038,7 +1052,7 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
            CUDA_SUCCESS;
   };
   const cuuint32_t box_y[3] = {(cuuint32_t)kChunk, 1, 32};  // row sweep: 4 cols x 32 rows
-  const cuuint32_t box_x[3] = {32, 1, (cuuint32_t)kChunk};  // column sweep: 32 cols x 4 rows
+  const cuuint32_t box_x[3] = {32, 4, (cuuint32_t)kChunk};  // column sweep: 32 cols x 4 vars x 4 rows
   return enc(&maps->y_load, B, dim_load, box_y) && enc(&maps->y_store, A, dim_store, box_y) &&
          enc(&maps->x_load, A, dim_load, box_x) && enc(&maps->x_store, B, dim_xstore, box_x);
 }
