@@ -431,6 +431,7 @@ struct Tiles {
   // walker visits cells in order, so they advance by one slot per cell
   // instead of recomputing chunk/buffer indices.
   uint32_t lo_addr, wr_addr;
+  uint32_t sw;          // this lane's TMA swizzle term (row sweep, SWIZZLE_32B)
   int lo_pos, lo_buf, wr_pos, wr_buf;
   unsigned lo_par;      // mbarrier phase parity of the load cursor's buffer
 
@@ -460,7 +461,7 @@ struct Tiles {
   // sweep orientation: mom_a is the momentum along the strip
   __device__ __forceinline__ Cons get(uint32_t at) const {
     constexpr int va = AXIS == 0 ? 1 : 2, vb = AXIS == 0 ? 2 : 1;
-    const uint8_t* b = hb_smem + at;
+    const uint8_t* b = hb_smem + (at ^ sw);
     return {*(const double*)(b), *(const double*)(b + va * kVarStride),
             *(const double*)(b + vb * kVarStride), *(const double*)(b + 3 * kVarStride)};
   }
@@ -490,7 +491,7 @@ struct Tiles {
   // The cell being updated, of strip `ln` (default: this lane's), receives u.
   __device__ __forceinline__ void put(int, const Cons& u, int ln = -1) {
     constexpr int va = AXIS == 0 ? 1 : 2, vb = AXIS == 0 ? 2 : 1;
-    uint8_t* b = hb_smem + wr_addr + (ln < 0 ? 0 : (ln - lane) * (int)kLaneBytes);
+    uint8_t* b = hb_smem + ((wr_addr + (ln < 0 ? 0 : (ln - lane) * (int)kLaneBytes)) ^ sw);
     *(double*)(b) = u.r;
     *(double*)(b + va * kVarStride) = u.ma;
     *(double*)(b + vb * kVarStride) = u.mb;
@@ -564,7 +565,7 @@ struct Tiles {
 template <int AXIS>
 __device__ __forceinline__ Tiles<AXIS> make_tiles(const CUtensorMap* load_map,
                                                   const CUtensorMap* store_map) {
-  const uint32_t pad = (128u - (smem_u32(hb_smem) & 127u)) & 127u;
+  const uint32_t pad = (256u - (smem_u32(hb_smem) & 255u)) & 255u;  // swizzle atoms
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   Tiles<AXIS> t;
   t.load_map = load_map;
@@ -573,6 +574,9 @@ __device__ __forceinline__ Tiles<AXIS> make_tiles(const CUtensorMap* load_map,
   t.full = pad + 4 * kNBuf * kChunkBytes + warp * kNBuf * 8;
   t.lane = lane;
   t.q0 = 0;
+  // SWIZZLE_32B (row sweep): within each 256-byte atom the 16-byte half of a
+  // 32-byte box row flips with address bit 7, i.e. with bit 2 of the row
+  t.sw = AXIS == 1 ? (uint32_t)((lane >> 2) & 1) << 4 : 0u;
   if (lane == 0) {
     for (int q = 0; q < kNBuf; ++q) mbar_init((uint64_t*)(hb_smem + t.full) + q, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1045,16 +1049,21 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
   // ghost value (sweep_x_tma_kernel)
   const cuuint64_t dim_xstore[3] = {((cuuint64_t)ny + 2 + kColOff) & ~(cuuint64_t)1, 4,
                                     (cuuint64_t)nx + 2};
-  auto enc = [&](CUtensorMap* m, double* base, const cuuint64_t* dim, const cuuint32_t* box) {
+  auto enc = [&](CUtensorMap* m, double* base, const cuuint64_t* dim, const cuuint32_t* box,
+                 CUtensorMapSwizzle swz) {
     return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dim, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
            CUDA_SUCCESS;
   };
   const cuuint32_t box_y[3] = {(cuuint32_t)kChunk, 1, 32};  // row sweep: 4 cols x 32 rows
   const cuuint32_t box_x[3] = {32, 4, (cuuint32_t)kChunk};  // column sweep: 32 cols x 4 vars x 4 rows
-  return enc(&maps->y_load, B, dim_load, box_y) && enc(&maps->y_store, A, dim_store, box_y) &&
-         enc(&maps->x_load, A, dim_load, box_x) && enc(&maps->x_store, B, dim_xstore, box_x);
+  // row sweep: 32-byte box rows swizzled (halves the smem bank conflicts of
+  // lane-per-row accesses); column sweep: 256-byte rows are conflict-free
+  const CUtensorMapSwizzle sy = CU_TENSOR_MAP_SWIZZLE_32B, sx = CU_TENSOR_MAP_SWIZZLE_NONE;
+  return enc(&maps->y_load, B, dim_load, box_y, sy) &&
+         enc(&maps->y_store, A, dim_store, box_y, sy) &&
+         enc(&maps->x_load, A, dim_load, box_x, sx) && enc(&maps->x_store, B, dim_xstore, box_x, sx);
 }
 
 void launch_sweep_x(const SweepArgs& a0, const TmaMaps& maps, const Geometry& geo,

@@ -23,7 +23,7 @@ constexpr int kColOff = 3;
 constexpr int kChunk = 4;
 constexpr int kNBuf = 3;
 constexpr int kChunkBytes = 32 * 4 * kChunk * 8;                         // 4 KB
-constexpr int kYSmemBytes = 4 * kNBuf * kChunkBytes + 128 + 4 * kNBuf * 8;  // + align, mbarriers
+constexpr int kYSmemBytes = 4 * kNBuf * kChunkBytes + 256 + 4 * kNBuf * 8;  // + align, mbarriers
 
 __host__ __device__ __forceinline__ size_t cell_index(size_t pitch, int v, int i, int j) {
   return ((size_t)(i + 1) * 4 + (size_t)v) * pitch + (size_t)(j + kColOff);
