@@ -154,12 +154,12 @@ def run_reference_arm(args, rank, world):
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": NX * NY * sample_steps / value * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (analytic Sod initial condition)",
-        "config": {"workload": f"BASELINE config 1 sample: {NX}x{NY} {CASE} {BC}, "
+        "data": "synthetic (analytic or seeded initial condition, no dataset)",
+        "config": {"workload": f"BASELINE {args.workload} sample: {NX}x{NY} {CASE} {BC}, "
                                f"{sample_steps} time steps per bench step",
                    "global_batch": NX * NY, "parallelism": f"cpu coarse_grain x{used}"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": kind,
-                         "sample": f"{sample_steps} time steps of the {NX}x{NY} config-1 grid, "
+                         "sample": f"{sample_steps} time steps of the {NX}x{NY} {args.workload} grid, "
                                    "reference coarse_grain (bench.cpp:53-90 dispatch)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -319,17 +319,21 @@ def main():
     avg_ms = kt[f"ms_{which}"] / n_launch
     alg_bytes = geo.nx * NY * ALG_BYTES_PER_CELL_SWEEP
     achieved = alg_bytes / (avg_ms / 1e3) / 1e9
+    # measured DRAM bytes per cell of that sweep (ncu --set full capture,
+    # profiles/traffic.json), scaled to this launch's cells
     traffic = None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
-        traffic = json.load(open(prof)).get(f"sweep_{which}_bytes_per_launch")
+        per_cell = json.load(open(prof)).get(f"sweep_{which}_dram_bytes_per_cell")
+        if per_cell:
+            traffic = per_cell * geo.nx * NY
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         v, kind, secs, used, nsteps = cpu_reference_sample(10, threads, min_seconds=10.0)
         cpu = {"value": v, "unit": UNIT, "cores": used, "kind": kind,
-               "sample": f"{nsteps} time steps of the {NX}x{NY} config-1 grid ({secs:.1f}s timed), "
+               "sample": f"{nsteps} time steps of the {NX}x{NY} {args.workload} grid ({secs:.1f}s timed), "
                          f"reference coarse_grain over {used} host threads"}
 
     if rank == 0:
