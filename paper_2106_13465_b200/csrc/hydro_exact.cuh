@@ -90,52 +90,86 @@ struct Side {
   double rho, u, p, c;
 };
 
+using K = ExactK;
+
 __device__ __forceinline__ Side make_side(const Prim& w, double gamma) {
   return {w.r, w.va, w.p, ::sqrt(gamma * w.p / w.r)};  // exact_riemann.cpp:17-22
 }
 
 // f_K(p) and f_K'(p) of one side at the same p (exact_riemann.cpp:26-45);
 // the rarefaction branch shares log(p/p_K) between the two powers.
-__device__ __forceinline__ void side_fn2(double p, const Side& s, double g, double& f,
+__device__ __forceinline__ void side_fn2(double p, const Side& s, const K& k, double& f,
                                          double& df) {
   if (p > s.p) {
-    const double a = 2.0 / ((g + 1.0) * s.rho);
-    const double b = (g - 1.0) / (g + 1.0) * s.p;
+    const double a = 2.0 / (k.gp1 * s.rho);
+    const double b = k.gm * s.p;
     const double root = ::sqrt(a / (p + b));
     f = (p - s.p) * root;
     df = root * (1.0 - 0.5 * (p - s.p) / (p + b));
   } else {
     const double l = log_(p / s.p);
-    f = 2.0 * s.c / (g - 1.0) * (exp_((g - 1.0) / (2.0 * g) * l) - 1.0);
-    df = 1.0 / (s.rho * s.c) * exp_(-(g + 1.0) / (2.0 * g) * l);
+    f = 2.0 * s.c / k.gm1 * (exp_(k.z * l) - 1.0);
+    df = 1.0 / (s.rho * s.c) * exp_(k.zn * l);
   }
 }
 
-__device__ __forceinline__ double side_fn(double p, const Side& s, double g) {
+// side_fn (exact_riemann.cpp:26-35) keeping, on the rarefaction branch,
+// L = log(p/p_K) and E = (p/p_K)^z = exp(z L) for the sampling below.
+struct SideEval {
+  double f, L, E;
+};
+__device__ __forceinline__ SideEval side_eval(double p, const Side& s, const K& k) {
+  SideEval e;
   if (p > s.p) {
-    const double a = 2.0 / ((g + 1.0) * s.rho);
-    const double b = (g - 1.0) / (g + 1.0) * s.p;
-    return (p - s.p) * ::sqrt(a / (p + b));
+    const double a = 2.0 / (k.gp1 * s.rho);
+    const double b = k.gm * s.p;
+    e.f = (p - s.p) * ::sqrt(a / (p + b));
+    e.L = e.E = 0.0;
+  } else {
+    e.L = log_(p / s.p);
+    e.E = exp_(k.z * e.L);
+    e.f = 2.0 * s.c / k.gm1 * (e.E - 1.0);
   }
-  return 2.0 * s.c / (g - 1.0) * (pow_(p / s.p, (g - 1.0) / (2.0 * g)) - 1.0);
+  return e;
+}
+
+__device__ __forceinline__ bool same_bits(double a, double b) {
+  return __double_as_longlong(a) == __double_as_longlong(b);
 }
 
 // Primitive state at xi = 0 of the Riemann problem (wl, wr); false if the
-// states generate vacuum (exact_riemann.cpp:52-59).
-__device__ __forceinline__ bool sample0(const Prim& wl, const Prim& wr, double g, Prim& out) {
+// states generate vacuum (exact_riemann.cpp:52-59).  Value-preserving
+// rearrangement of the oracle's sample_xi0 (oracle/hydro_oracle.c):
+//  * side_fn(p_min, K) is exactly +0 for the side whose pressure is p_min
+//    (pow(1, z) = exp(z log 1) = 1 bit for bit), so only the other side's
+//    term is evaluated;
+//  * the sampling reuses the rarefaction side's (p/p_K)^z from u_star and
+//    its log for (p/p_K)^(1/g); the fan's two powers share log(c/c_K);
+//  * for bitwise-identical side states (uniform flow), each side quantity
+//    is evaluated once.
+__device__ __forceinline__ bool sample0(const Prim& wl, const Prim& wr, const K& k, Prim& out) {
+  const double g = k.g;
+  const bool same = same_bits(wl.r, wr.r) & same_bits(wl.va, wr.va) & same_bits(wl.p, wr.p);
   const Side l = make_side(wl, g);
-  const Side r = make_side(wr, g);
+  Side r;
+  if (same) r = l;
+  else r = make_side(wr, g);
   const double du = wr.va - wl.va;
-  if (2.0 * (l.c + r.c) / (g - 1.0) <= du) return false;
+  if (2.0 * (l.c + r.c) / k.gm1 <= du) return false;
 
-  const double p_min = smin(l.p, r.p);
+  const bool rmin = r.p < l.p;
+  const double p_min = rmin ? r.p : l.p;  // smin(l.p, r.p)
+  double fo = 0.0;                        // + the min side's +0
+  if (!same) fo = side_eval(p_min, rmin ? l : r, k).f;
   double p;
-  if (side_fn(p_min, l, g) + side_fn(p_min, r, g) + du >= 0.0) {
+  if (fo + du >= 0.0) {
     // both rarefactions: closed-form root (:63-69)
-    const double z = (g - 1.0) / (2.0 * g);
-    const double numer = l.c + r.c - 0.5 * (g - 1.0) * du;
-    const double denom = l.c / pow_(l.p, z) + r.c / pow_(r.p, z);
-    p = pow_(numer / denom, 1.0 / z);
+    const double numer = l.c + r.c - k.hg * du;
+    const double ql = l.c / pow_(l.p, k.z);
+    double qr = ql;
+    if (!same) qr = r.c / pow_(r.p, k.z);
+    const double denom = ql + qr;
+    p = pow_(numer / denom, k.iz);
   } else {
     // Newton from the linearised guess with the p_min floor, 10 iterations
     const double guess =
@@ -147,8 +181,8 @@ __device__ __forceinline__ bool sample0(const Prim& wl, const Prim& wr, double g
 #pragma unroll 1
     for (int it = 0; it < 10; ++it) {
       double fl, dfl, fr, dfr;
-      side_fn2(p, l, g, fl, dfl);
-      side_fn2(p, r, g, fr, dfr);
+      side_fn2(p, l, k, fl, dfl);
+      side_fn2(p, r, k, fr, dfr);
       const double f = fl + fr + du;
       const double df = dfl + dfr;
       double next = p - f / df;
@@ -157,52 +191,52 @@ __device__ __forceinline__ bool sample0(const Prim& wl, const Prim& wr, double g
       p = next;
     }
   }
-  const double u_star = 0.5 * (wl.va + wr.va) + 0.5 * (side_fn(p, r, g) - side_fn(p, l, g));
-  const double gm = (g - 1.0) / (g + 1.0);
+  const SideEval el = side_eval(p, l, k);
+  SideEval er = el;
+  if (!same) er = side_eval(p, r, k);
+  const double u_star = 0.5 * (wl.va + wr.va) + 0.5 * (er.f - el.f);
   const double xi = 0.0;
   if (xi <= u_star) {  // left of the contact (:208-223)
     if (p > l.p) {     // left shock
       const double ratio = p / l.p;
-      const double head =
-          l.u - l.c * ::sqrt((g + 1.0) / (2.0 * g) * ratio + (g - 1.0) / (2.0 * g));
+      const double head = l.u - l.c * ::sqrt(k.zp * ratio + k.z);
       if (xi <= head) { out = wl; return true; }
-      out = {l.rho * (ratio + gm) / (gm * ratio + 1.0), u_star, wl.vb, p};
+      out = {l.rho * (ratio + k.gm) / (k.gm * ratio + 1.0), u_star, wl.vb, p};
       return true;
     }
     const double head = l.u - l.c;  // left rarefaction
     if (xi <= head) { out = wl; return true; }
-    const double c_star = l.c * pow_(p / l.p, (g - 1.0) / (2.0 * g));
+    const double c_star = l.c * el.E;
     const double tail = u_star - c_star;
     if (xi >= tail) {
-      out = {l.rho * pow_(p / l.p, 1.0 / g), u_star, wl.vb, p};
+      out = {l.rho * exp_(k.ig * el.L), u_star, wl.vb, p};
       return true;
     }
-    const double u = 2.0 / (g + 1.0) * (l.c + 0.5 * (g - 1.0) * l.u + xi);
-    const double c = 2.0 / (g + 1.0) * (l.c + 0.5 * (g - 1.0) * (l.u - xi));
-    out = {l.rho * pow_(c / l.c, 2.0 / (g - 1.0)), u, wl.vb,
-           l.p * pow_(c / l.c, 2.0 * g / (g - 1.0))};
+    const double u = k.a2 * (l.c + k.hg * l.u + xi);
+    const double c = k.a2 * (l.c + k.hg * (l.u - xi));
+    const double lc = log_(c / l.c);
+    out = {l.rho * exp_(k.er * lc), u, wl.vb, l.p * exp_(k.ep * lc)};
     return true;
   }
   if (p > r.p) {  // right shock (:225-240)
     const double ratio = p / r.p;
-    const double head =
-        r.u + r.c * ::sqrt((g + 1.0) / (2.0 * g) * ratio + (g - 1.0) / (2.0 * g));
+    const double head = r.u + r.c * ::sqrt(k.zp * ratio + k.z);
     if (xi >= head) { out = wr; return true; }
-    out = {r.rho * (ratio + gm) / (gm * ratio + 1.0), u_star, wr.vb, p};
+    out = {r.rho * (ratio + k.gm) / (k.gm * ratio + 1.0), u_star, wr.vb, p};
     return true;
   }
   const double head = r.u + r.c;  // right rarefaction
   if (xi >= head) { out = wr; return true; }
-  const double c_star = r.c * pow_(p / r.p, (g - 1.0) / (2.0 * g));
+  const double c_star = r.c * er.E;
   const double tail = u_star + c_star;
   if (xi <= tail) {
-    out = {r.rho * pow_(p / r.p, 1.0 / g), u_star, wr.vb, p};
+    out = {r.rho * exp_(k.ig * er.L), u_star, wr.vb, p};
     return true;
   }
-  const double u = 2.0 / (g + 1.0) * (-r.c + 0.5 * (g - 1.0) * r.u + xi);
-  const double c = 2.0 / (g + 1.0) * (r.c - 0.5 * (g - 1.0) * (r.u - xi));
-  out = {r.rho * pow_(c / r.c, 2.0 / (g - 1.0)), u, wr.vb,
-         r.p * pow_(c / r.c, 2.0 * g / (g - 1.0))};
+  const double u = k.a2 * (-r.c + k.hg * r.u + xi);
+  const double c = k.a2 * (r.c - k.hg * (r.u - xi));
+  const double lc = log_(c / r.c);
+  out = {r.rho * exp_(k.er * lc), u, wr.vb, r.p * exp_(k.ep * lc)};
   return true;
 }
 
@@ -210,9 +244,9 @@ __device__ __forceinline__ bool sample0(const Prim& wl, const Prim& wr, double g
 
 // Interface flux of the exact-10 mode; vacuum -> `vacuum` set, flux unused.
 __device__ __forceinline__ Flux exact10_flux(const Prim& wl, const Prim& wr, const Gas& g,
-                                             bool& vacuum) {
+                                             const exact::K& k, bool& vacuum) {
   Prim w;
-  vacuum = !exact::sample0(wl, wr, g.gamma, w);
+  vacuum = !exact::sample0(wl, wr, k, w);
   // physical_flux (euler_kernel.cpp:34-39), plain IEEE division
   const double ener = w.p / g.gm1 + (0.5 * w.r) * (w.va * w.va + w.vb * w.vb);
   const double rva = w.r * w.va;
