@@ -96,20 +96,30 @@ __device__ __forceinline__ Side make_side(const Prim& w, double gamma) {
   return {w.r, w.va, w.p, ::sqrt(gamma * w.p / w.r)};  // exact_riemann.cpp:17-22
 }
 
+// Per-side constants of f_K / f_K' (exact_riemann.cpp:26-45): the same
+// subexpressions the oracle evaluates on every Newton step, hoisted.
+struct SideK {
+  double a;   // 2 / ((g + 1) rho)
+  double b;   // (g - 1) / (g + 1) p
+  double cf;  // 2 c / (g - 1)
+  double dn;  // 1 / (rho c)
+};
+__device__ __forceinline__ SideK side_k(const Side& s, const K& k) {
+  return {2.0 / (k.gp1 * s.rho), k.gm * s.p, 2.0 * s.c / k.gm1, 1.0 / (s.rho * s.c)};
+}
+
 // f_K(p) and f_K'(p) of one side at the same p (exact_riemann.cpp:26-45);
 // the rarefaction branch shares log(p/p_K) between the two powers.
-__device__ __forceinline__ void side_fn2(double p, const Side& s, const K& k, double& f,
-                                         double& df) {
+__device__ __forceinline__ void side_fn2(double p, const Side& s, const SideK& sk, const K& k,
+                                         double& f, double& df) {
   if (p > s.p) {
-    const double a = 2.0 / (k.gp1 * s.rho);
-    const double b = k.gm * s.p;
-    const double root = ::sqrt(a / (p + b));
+    const double root = ::sqrt(sk.a / (p + sk.b));
     f = (p - s.p) * root;
-    df = root * (1.0 - 0.5 * (p - s.p) / (p + b));
+    df = root * (1.0 - 0.5 * (p - s.p) / (p + sk.b));
   } else {
     const double l = log_(p / s.p);
-    f = 2.0 * s.c / k.gm1 * (exp_(k.z * l) - 1.0);
-    df = 1.0 / (s.rho * s.c) * exp_(k.zn * l);
+    f = sk.cf * (exp_(k.z * l) - 1.0);
+    df = sk.dn * exp_(k.zn * l);
   }
 }
 
@@ -175,14 +185,15 @@ __device__ __forceinline__ bool sample0(const Prim& wl, const Prim& wr, const K&
     const double guess =
         0.5 * (l.p + r.p) - 0.125 * du * (l.rho + r.rho) * (l.c + r.c);  // :72-74
     p = smax(guess, p_min);
+    const SideK lk = side_k(l, k), rk = side_k(r, k);
     // Once a step reproduces p exactly, every remaining step does too (same
     // inputs, same arithmetic), so leaving the loop there is bitwise
     // identical to running all 10 iterations -- typically after 4-5.
 #pragma unroll 1
     for (int it = 0; it < 10; ++it) {
       double fl, dfl, fr, dfr;
-      side_fn2(p, l, k, fl, dfl);
-      side_fn2(p, r, k, fr, dfr);
+      side_fn2(p, l, lk, k, fl, dfl);
+      side_fn2(p, r, rk, k, fr, dfr);
       const double f = fl + fr + du;
       const double df = dfl + dfr;
       double next = p - f / df;
