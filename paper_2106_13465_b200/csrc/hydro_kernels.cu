@@ -65,7 +65,7 @@ struct StepOut {
   int fR;           // Riemann failure (exact-10: 3 = vacuum), -1 none
   Cons un;          // cell c-1 after the conservative update
   int fU;
-  double lim;       // cell_dt_limit of the updated cell (row sweep)
+  double spd;       // dt signal speed of the updated cell (row sweep)
   int fD;
 };
 
@@ -108,7 +108,7 @@ __device__ __forceinline__ void step_cell(M& m, const Window& w, const Cons& uC,
     o.un = old();
     Recip rn;
     o.fU = update_cell(m, o.un, w.fluxPrev, o.F, dtdx, rn);
-    if (WANT_DT) o.fD = dt_limit(m, o.un, rn, spacing, g, o.lim);
+    if (WANT_DT) o.fD = dt_speed(m, o.un, rn, g, o.spd);
   }
 }
 
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
   const int groups = (nx + 31) >> 5;
   const int items = groups * a.nseg;
   double* __restrict__ dst = a.dst;
-  double lim_min = __longlong_as_double(0x7ff0000000000000ll);
+  double spd_max = 0.0;  // speeds are >= +0
   unsigned long long dt_key = kNoError;
 
   for (int item = claim(a.counter); item < items; item = claim(a.counter)) {
@@ -716,12 +716,12 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
       q[pitch] = neg ? -u.mb : u.mb;
       q[3 * pitch] = u.e;
     };
-    double lim_item;
+    double spd_item;
     unsigned long long dt_item;
     // One pass over the item with math policy M (tiles restaged from U_b).
     auto pass = [&](auto math) {
       using M = decltype(math);
-      lim_item = __longlong_as_double(0x7ff0000000000000ll);
+      spd_item = 0.0;
       dt_item = kNoError;
       t.begin();
       auto sink = [&](int k, const StepOut& o) {
@@ -737,7 +737,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
         }
         if (a.want_limit) {
           if (o.fD >= 0) keep_min(dt_item, error_key(a.step + 1, 0, gi, 0, j, o.fD));
-          else lim_item = smin(lim_item, o.lim);
+          else spd_item = smax(spd_item, o.spd);
         }
       };
       unsigned long long ek = kNoError;
@@ -759,15 +759,18 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
     if (active) {
       if (r.key != kNoError) record(a.err, r.key);
       keep_min(dt_key, dt_item);
-      lim_min = smin(lim_min, lim_item);
+      spd_max = smax(spd_max, spd_item);
     }
   }
   if (lane == 0) bulk_wait0();
   if (a.want_limit) {
-    const unsigned long long m = warp_min_u64((unsigned long long)__double_as_longlong(lim_min));
+    // largest speed of the warp (non-negative doubles order like their bits)
+    // -> its cell_dt_limit, the warp's minimum limit
+    const double smx = __longlong_as_double(
+        (long long)~warp_min_u64(~(unsigned long long)__double_as_longlong(spd_max)));
     const unsigned long long e = warp_min_u64(dt_key);
     if (lane == 0) {
-      atomicMin(a.limit_out, m);
+      atomicMin(a.limit_out, (unsigned long long)__double_as_longlong(a.spacing / smx));
       if (e != kNoError) atomicMin(a.dt_err, e);
     }
   }
