@@ -13,7 +13,9 @@ Metric: cell-updates/s = interior cells x time steps / seconds (both sweeps +
 the dt reduction per time step).  ``value`` is device-resident (state in HBM
 before the timed region, CUDA events on the launch stream, max over ranks);
 ``e2e`` goes through the C-ABI with pinned host buffers: upload, run, download
-every bench step.  ``--impl reference`` times the reference's own CPU
+every bench step.  An hllc run also measures the exact-10 flux mode (BASELINE's
+stated solver) on the same workload under ``flux_variants``.
+``--impl reference`` times the reference's own CPU
 implementation (oracle/_ref, coarse_grain over all host threads) on a
 bounded sample of the same workload.
 """
@@ -177,6 +179,8 @@ def main():
                     help="BASELINE config (default cfg1, the metric's config)")
     ap.add_argument("--flux", default="hllc", choices=["hllc", "exact10"],
                     help="interface flux (hllc = the reference hot path)")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the exact-10 flux sub-measurement of an hllc run")
     args = ap.parse_args()
     global NX, NY, TSTEPS, CASE, BC, SEED, SCALING
     CASE, NX, NY, BC, TSTEPS, SEED, SCALING = WORKLOADS[args.workload]
@@ -336,6 +340,64 @@ def main():
                "sample": f"{nsteps} time steps of the {NX}x{NY} {args.workload} grid ({secs:.1f}s timed), "
                          f"reference coarse_grain over {used} host threads"}
 
+    # ---- the other flux of BASELINE's configs (exact Riemann, 10 Newton
+    # iterations) on the same workload, same protocol, reported beside the
+    # hot-path line ---------------------------------------------------------
+    variants = None
+    if args.flux == "hllc" and not args.no_variants:
+        vflux = "exact10"
+        if world == 1:
+            vgrid = P.GpuGrid(NX, NY, dx, dy, model, BC, device=local, flux=vflux)
+            vgrid.set_stream(stream.cuda_stream)
+            vslab = None
+        else:
+            vslab = S.GpuSlab(geo, dx, dy, model, BC, local, flux=vflux)
+            vslab.bind_stream(stream)
+            vgrid = vslab.grid
+
+        def vrun():
+            if world == 1:
+                vgrid.run_async(TSTEPS)
+            else:
+                S.run_slab(vslab, comm, TSTEPS)
+
+        vsteps = max(1, min(args.steps, 5))
+        for _ in range(args.warmup):
+            vgrid.init_case(CASE, SEED)
+            vrun()
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(vsteps):
+            vgrid.init_case(CASE, SEED)
+            vrun()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        vms = e0.elapsed_time(e1)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(vsteps):
+            vgrid.upload_ptr(ptrs0, NY + 4)
+            vrun()
+            vgrid.download_ptr(ptrs, NY + 4)
+        torch.cuda.synchronize()
+        ve2e = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([vms, ve2e], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            vms, ve2e = float(t[0].item()), float(t[1].item())
+        vdigest = (P.grid_digest(P.Grid2D(geo.nx, NY, dx, dy, host.numpy()))
+                   if world == 1 else None)
+        variants = {vflux: {
+            "value": cells * TSTEPS * vsteps / (vms / 1e3), "unit": UNIT,
+            "steps": vsteps, "warmup": args.warmup, "ms_per_step": vms / vsteps,
+            "e2e": {"value": cells * TSTEPS * vsteps / ve2e, "unit": UNIT,
+                    "h2d_bytes_per_step": plane_bytes, "d2h_bytes_per_step": plane_bytes},
+            "note": "BASELINE's stated solver: exact Riemann flux, 10 Newton iterations "
+                    "(DESIGN.md 3.5); bitwise equal to the oracle's restatement",
+            "result_digest": f"{vdigest:016x}" if vdigest is not None else None}}
+        vgrid.close()
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -361,6 +423,7 @@ def main():
             "clocks": clock_info,
             "cpu_baseline": cpu,
             "result_digest": f"{digest:016x}" if digest is not None else None,
+            "flux_variants": variants,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
