@@ -18,8 +18,10 @@
 // bit operations (no FMA: --fmad=false), so the C oracle's restatement
 // (oracle/hydro_oracle.c) produces identical bits.  Against the reference's
 // std::pow-based solver the mode agrees to a floored relative 1e-12
-// (tests/test_exact_flux.py).  Division and sqrt are the compiler's IEEE
-// operations.
+// (tests/test_exact_flux.py).  Divisions and square roots go through the
+// walker's math policy M: FastMath (bitwise the IEEE result in its proven
+// range, else the work item is redone) or ExactMath (the compiler's IEEE
+// operations).
 #pragma once
 
 #include <cstdint>
@@ -39,17 +41,18 @@ __device__ __forceinline__ unsigned long long to_bits(double x) {
 
 // log(x), x positive normal: x = 2^k (1+f), sqrt(2)/2 < 1+f < sqrt(2);
 // log(1+f) = f - (hfsq - s*(hfsq + R(s^2))), s = f/(2+f).
-__device__ __forceinline__ double log_(double x) {
+template <class M>
+__device__ __forceinline__ double log_(M& m, double x) {
   const unsigned long long bits = to_bits(x);
   unsigned hx = (unsigned)(bits >> 32);
   int k = (int)(hx >> 20) - 1023;
   hx &= 0x000fffffu;
   const unsigned i = (hx + 0x95f64u) & 0x100000u;  // mantissa above sqrt(2)?
-  const double m = from_bits(((unsigned long long)(hx | (i ^ 0x3ff00000u)) << 32) |
-                             (bits & 0xffffffffull));
+  const double mt = from_bits(((unsigned long long)(hx | (i ^ 0x3ff00000u)) << 32) |
+                              (bits & 0xffffffffull));
   k += (int)(i >> 20);
-  const double f = m - 1.0;
-  const double s = f / (2.0 + f);
+  const double f = mt - 1.0;
+  const double s = m.divf(f, 2.0 + f);
   const double z = s * s;
   const double w = z * z;
   const double t1 = w * (3.999999999940941908e-01 +
@@ -67,7 +70,8 @@ __device__ __forceinline__ double log_(double x) {
 // exp(x), |x| < 700: x = k ln2 + r, |r| <= ln2/2; exp(r) from the
 // rational form 1 - ((lo - r c/(2-c)) - hi), c = r - r^2 P(r^2); 2^k by
 // exponent arithmetic.
-__device__ __forceinline__ double exp_(double x) {
+template <class M>
+__device__ __forceinline__ double exp_(M& m, double x) {
   const double half = (x < 0.0) ? -0.5 : 0.5;
   const int k = (int)(1.44269504088896338700e+00 * x + half);  // truncation
   const double t = (double)k;
@@ -80,11 +84,14 @@ __device__ __forceinline__ double exp_(double x) {
                                    r2 * (6.61375632143793436117e-05 +
                                          r2 * (-1.65339022054652515390e-06 +
                                                r2 * 4.13813679705723846039e-08))));
-  const double y = 1.0 - ((lo - (r * c) / (2.0 - c)) - hi);
+  const double y = 1.0 - ((lo - m.divf(r * c, 2.0 - c)) - hi);
   return from_bits(to_bits(y) + ((unsigned long long)(long long)k << 52));
 }
 
-__device__ __forceinline__ double pow_(double x, double y) { return exp_(y * log_(x)); }
+template <class M>
+__device__ __forceinline__ double pow_(M& m, double x, double y) {
+  return exp_(m, y * log_(m, x));
+}
 
 struct Side {
   double rho, u, p, c;
@@ -92,8 +99,10 @@ struct Side {
 
 using K = ExactK;
 
-__device__ __forceinline__ Side make_side(const Prim& w, double gamma) {
-  return {w.r, w.va, w.p, ::sqrt(gamma * w.p / w.r)};  // exact_riemann.cpp:17-22
+// make_side (exact_riemann.cpp:17-22) of a face, whose 1/rho is at hand
+template <class M>
+__device__ __forceinline__ Side make_side(M& m, const Face& f, double gamma) {
+  return {f.w.r, f.w.va, f.w.p, m.sqrt(m.div(gamma * f.w.p, f.rr))};
 }
 
 // Per-side constants of f_K / f_K' (exact_riemann.cpp:26-45): the same
@@ -103,23 +112,28 @@ struct SideK {
   double b;   // (g - 1) / (g + 1) p
   double cf;  // 2 c / (g - 1)
   double dn;  // 1 / (rho c)
+  Recip rp;   // for p / p_K
 };
-__device__ __forceinline__ SideK side_k(const Side& s, const K& k) {
-  return {2.0 / (k.gp1 * s.rho), k.gm * s.p, 2.0 * s.c / k.gm1, 1.0 / (s.rho * s.c)};
+template <class M>
+__device__ __forceinline__ SideK side_k(M& m, const Side& s, const K& k) {
+  return {m.divf(2.0, k.gp1 * s.rho), k.gm * s.p, m.divf(2.0 * s.c, k.gm1),
+          m.divf(1.0, s.rho * s.c), m.recip(s.p)};
 }
 
 // f_K(p) and f_K'(p) of one side at the same p (exact_riemann.cpp:26-45);
 // the rarefaction branch shares log(p/p_K) between the two powers.
-__device__ __forceinline__ void side_fn2(double p, const Side& s, const SideK& sk, const K& k,
-                                         double& f, double& df) {
+template <class M>
+__device__ __forceinline__ void side_fn2(M& m, double p, const Side& s, const SideK& sk,
+                                         const K& k, double& f, double& df) {
   if (p > s.p) {
-    const double root = ::sqrt(sk.a / (p + sk.b));
+    const Recip d = m.recip(p + sk.b);
+    const double root = m.sqrt(m.div(sk.a, d));
     f = (p - s.p) * root;
-    df = root * (1.0 - 0.5 * (p - s.p) / (p + sk.b));
+    df = root * (1.0 - m.div(0.5 * (p - s.p), d));
   } else {
-    const double l = log_(p / s.p);
-    f = sk.cf * (exp_(k.z * l) - 1.0);
-    df = sk.dn * exp_(k.zn * l);
+    const double l = log_(m, m.div(p, sk.rp));
+    f = sk.cf * (exp_(m, k.z * l) - 1.0);
+    df = sk.dn * exp_(m, k.zn * l);
   }
 }
 
@@ -128,17 +142,18 @@ __device__ __forceinline__ void side_fn2(double p, const Side& s, const SideK& s
 struct SideEval {
   double f, L, E;
 };
-__device__ __forceinline__ SideEval side_eval(double p, const Side& s, const K& k) {
+template <class M>
+__device__ __forceinline__ SideEval side_eval(M& m, double p, const Side& s, const K& k) {
   SideEval e;
   if (p > s.p) {
-    const double a = 2.0 / (k.gp1 * s.rho);
+    const double a = m.divf(2.0, k.gp1 * s.rho);
     const double b = k.gm * s.p;
-    e.f = (p - s.p) * ::sqrt(a / (p + b));
+    e.f = (p - s.p) * m.sqrt(m.divf(a, p + b));
     e.L = e.E = 0.0;
   } else {
-    e.L = log_(p / s.p);
-    e.E = exp_(k.z * e.L);
-    e.f = 2.0 * s.c / k.gm1 * (e.E - 1.0);
+    e.L = log_(m, m.divf(p, s.p));
+    e.E = exp_(m, k.z * e.L);
+    e.f = m.divf(2.0 * s.c, k.gm1) * (e.E - 1.0);
   }
   return e;
 }
@@ -157,62 +172,66 @@ __device__ __forceinline__ bool same_bits(double a, double b) {
 //    its log for (p/p_K)^(1/g); the fan's two powers share log(c/c_K);
 //  * for bitwise-identical side states (uniform flow), each side quantity
 //    is evaluated once.
-__device__ __forceinline__ bool sample0(const Prim& wl, const Prim& wr, const K& k, Prim& out) {
+template <class M>
+__device__ __forceinline__ bool sample0(M& m, const Face& fl, const Face& fr, const K& k,
+                                        Prim& out) {
+  const Prim& wl = fl.w;
+  const Prim& wr = fr.w;
   const double g = k.g;
   const bool same = same_bits(wl.r, wr.r) & same_bits(wl.va, wr.va) & same_bits(wl.p, wr.p);
-  const Side l = make_side(wl, g);
+  const Side l = make_side(m, fl, g);
   Side r;
   if (same) r = l;
-  else r = make_side(wr, g);
+  else r = make_side(m, fr, g);
   const double du = wr.va - wl.va;
-  if (2.0 * (l.c + r.c) / k.gm1 <= du) return false;
+  if (m.divf(2.0 * (l.c + r.c), k.gm1) <= du) return false;
 
   const bool rmin = r.p < l.p;
   const double p_min = rmin ? r.p : l.p;  // smin(l.p, r.p)
   double fo = 0.0;                        // + the min side's +0
-  if (!same) fo = side_eval(p_min, rmin ? l : r, k).f;
+  if (!same) fo = side_eval(m, p_min, rmin ? l : r, k).f;
   double p;
   if (fo + du >= 0.0) {
     // both rarefactions: closed-form root (:63-69)
     const double numer = l.c + r.c - k.hg * du;
-    const double ql = l.c / pow_(l.p, k.z);
+    const double ql = m.divf(l.c, pow_(m, l.p, k.z));
     double qr = ql;
-    if (!same) qr = r.c / pow_(r.p, k.z);
+    if (!same) qr = m.divf(r.c, pow_(m, r.p, k.z));
     const double denom = ql + qr;
-    p = pow_(numer / denom, k.iz);
+    p = pow_(m, m.divf(numer, denom), k.iz);
   } else {
     // Newton from the linearised guess with the p_min floor, 10 iterations
     const double guess =
         0.5 * (l.p + r.p) - 0.125 * du * (l.rho + r.rho) * (l.c + r.c);  // :72-74
     p = smax(guess, p_min);
-    const SideK lk = side_k(l, k), rk = side_k(r, k);
+    const SideK lk = side_k(m, l, k), rk = side_k(m, r, k);
     // Once a step reproduces p exactly, every remaining step does too (same
     // inputs, same arithmetic), so leaving the loop there is bitwise
     // identical to running all 10 iterations -- typically after 4-5.
 #pragma unroll 1
     for (int it = 0; it < 10; ++it) {
-      double fl, dfl, fr, dfr;
-      side_fn2(p, l, lk, k, fl, dfl);
-      side_fn2(p, r, rk, k, fr, dfr);
-      const double f = fl + fr + du;
-      const double df = dfl + dfr;
-      double next = p - f / df;
+      double fL, dfL, fR, dfR;
+      side_fn2(m, p, l, lk, k, fL, dfL);
+      side_fn2(m, p, r, rk, k, fR, dfR);
+      const double f = fL + fR + du;
+      const double df = dfL + dfR;
+      double next = p - m.divf(f, df);
       if (next < p_min) next = p_min;
       if (next == p) break;
       p = next;
     }
   }
-  const SideEval el = side_eval(p, l, k);
+  const SideEval el = side_eval(m, p, l, k);
   SideEval er = el;
-  if (!same) er = side_eval(p, r, k);
+  if (!same) er = side_eval(m, p, r, k);
   const double u_star = 0.5 * (wl.va + wr.va) + 0.5 * (er.f - el.f);
   const double xi = 0.0;
   if (xi <= u_star) {  // left of the contact (:208-223)
     if (p > l.p) {     // left shock
-      const double ratio = p / l.p;
-      const double head = l.u - l.c * ::sqrt(k.zp * ratio + k.z);
+      const double ratio = m.divf(p, l.p);
+      const double head = l.u - l.c * m.sqrt(k.zp * ratio + k.z);
       if (xi <= head) { out = wl; return true; }
-      out = {l.rho * (ratio + k.gm) / (k.gm * ratio + 1.0), u_star, wl.vb, p};
+      out = {m.divf(l.rho * (ratio + k.gm), k.gm * ratio + 1.0), u_star, wl.vb, p};
       return true;
     }
     const double head = l.u - l.c;  // left rarefaction
@@ -220,20 +239,20 @@ __device__ __forceinline__ bool sample0(const Prim& wl, const Prim& wr, const K&
     const double c_star = l.c * el.E;
     const double tail = u_star - c_star;
     if (xi >= tail) {
-      out = {l.rho * exp_(k.ig * el.L), u_star, wl.vb, p};
+      out = {l.rho * exp_(m, k.ig * el.L), u_star, wl.vb, p};
       return true;
     }
     const double u = k.a2 * (l.c + k.hg * l.u + xi);
     const double c = k.a2 * (l.c + k.hg * (l.u - xi));
-    const double lc = log_(c / l.c);
-    out = {l.rho * exp_(k.er * lc), u, wl.vb, l.p * exp_(k.ep * lc)};
+    const double lc = log_(m, m.divf(c, l.c));
+    out = {l.rho * exp_(m, k.er * lc), u, wl.vb, l.p * exp_(m, k.ep * lc)};
     return true;
   }
   if (p > r.p) {  // right shock (:225-240)
-    const double ratio = p / r.p;
-    const double head = r.u + r.c * ::sqrt(k.zp * ratio + k.z);
+    const double ratio = m.divf(p, r.p);
+    const double head = r.u + r.c * m.sqrt(k.zp * ratio + k.z);
     if (xi >= head) { out = wr; return true; }
-    out = {r.rho * (ratio + k.gm) / (k.gm * ratio + 1.0), u_star, wr.vb, p};
+    out = {m.divf(r.rho * (ratio + k.gm), k.gm * ratio + 1.0), u_star, wr.vb, p};
     return true;
   }
   const double head = r.u + r.c;  // right rarefaction
@@ -241,25 +260,26 @@ __device__ __forceinline__ bool sample0(const Prim& wl, const Prim& wr, const K&
   const double c_star = r.c * er.E;
   const double tail = u_star + c_star;
   if (xi <= tail) {
-    out = {r.rho * exp_(k.ig * er.L), u_star, wr.vb, p};
+    out = {r.rho * exp_(m, k.ig * er.L), u_star, wr.vb, p};
     return true;
   }
   const double u = k.a2 * (-r.c + k.hg * r.u + xi);
   const double c = k.a2 * (r.c - k.hg * (r.u - xi));
-  const double lc = log_(c / r.c);
-  out = {r.rho * exp_(k.er * lc), u, wr.vb, r.p * exp_(k.ep * lc)};
+  const double lc = log_(m, m.divf(c, r.c));
+  out = {r.rho * exp_(m, k.er * lc), u, wr.vb, r.p * exp_(m, k.ep * lc)};
   return true;
 }
 
 }  // namespace exact
 
 // Interface flux of the exact-10 mode; vacuum -> `vacuum` set, flux unused.
-__device__ __forceinline__ Flux exact10_flux(const Prim& wl, const Prim& wr, const Gas& g,
-                                             const exact::K& k, bool& vacuum) {
+template <class M>
+__device__ __forceinline__ Flux exact10_flux(M& m, const Face& fl, const Face& fr, const Gas& g,
+                                             bool& vacuum) {
   Prim w;
-  vacuum = !exact::sample0(wl, wr, k, w);
-  // physical_flux (euler_kernel.cpp:34-39), plain IEEE division
-  const double ener = w.p / g.gm1 + (0.5 * w.r) * (w.va * w.va + w.vb * w.vb);
+  vacuum = !exact::sample0(m, fl, fr, g.ek, w);
+  // physical_flux (euler_kernel.cpp:34-39)
+  const double ener = m.divn(w.p, g.rgm1) + (0.5 * w.r) * (w.va * w.va + w.vb * w.vb);
   const double rva = w.r * w.va;
   return {rva, rva * w.va + w.p, rva * w.vb, (ener + w.p) * w.va};
 }

@@ -81,7 +81,7 @@ __device__ __forceinline__ Flux riemann(M& m, const Face& L, const Face& R, cons
     return hllc(m, L, R, g);
   } else {
     bool vacuum;
-    const Flux f = exact10_flux(L.w, R.w, g, g.ek, vacuum);
+    const Flux f = exact10_flux(m, L, R, g, vacuum);
     if (vacuum) {
       if constexpr (M::kFast) m.fallback();  // reported by the exact pass
       else fail = 3;
