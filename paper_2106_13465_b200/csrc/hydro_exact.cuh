@@ -39,8 +39,24 @@ __device__ __forceinline__ unsigned long long to_bits(double x) {
   return (unsigned long long)__double_as_longlong(x);
 }
 
+// Polynomial coefficients and ln2 split in constant memory: the FP64
+// instructions read them as constant-bank operands instead of
+// re-materialising 64-bit immediates in registers on every call.
+__constant__ double kLg[7] = {6.666666666666735130e-01, 3.999999999940941908e-01,
+                              2.857142874366239149e-01, 2.222219843214978396e-01,
+                              1.818357216161805012e-01, 1.531383769920937332e-01,
+                              1.479819860511658591e-01};
+__constant__ double kEp[5] = {1.66666666666666019037e-01, -2.77777777770155933842e-03,
+                              6.61375632143793436117e-05, -1.65339022054652515390e-06,
+                              4.13813679705723846039e-08};
+__constant__ double kLn2Hi = 6.93147180369123816490e-01;
+__constant__ double kLn2Lo = 1.90821492927058770002e-10;
+__constant__ double kInvLn2 = 1.44269504088896338700e+00;
+
 // log(x), x positive normal: x = 2^k (1+f), sqrt(2)/2 < 1+f < sqrt(2);
-// log(1+f) = f - (hfsq - s*(hfsq + R(s^2))), s = f/(2+f).
+// log(1+f) = f - (hfsq - s*(hfsq + R(s^2))), s = f/(2+f).  The division's
+// range is proven for every input: 2+f lies in [1.70, 2.42] and f = m - 1
+// is 0 or at least 2^-53 in magnitude.
 template <class M>
 __device__ __forceinline__ double log_(M& m, double x) {
   const unsigned long long bits = to_bits(x);
@@ -52,39 +68,34 @@ __device__ __forceinline__ double log_(M& m, double x) {
                               (bits & 0xffffffffull));
   k += (int)(i >> 20);
   const double f = mt - 1.0;
-  const double s = m.divf(f, 2.0 + f);
+  const double s = m.divr(f, 2.0 + f);
   const double z = s * s;
   const double w = z * z;
-  const double t1 = w * (3.999999999940941908e-01 +
-                         w * (2.222219843214978396e-01 + w * 1.531383769920937332e-01));
-  const double t2 = z * (6.666666666666735130e-01 +
-                         w * (2.857142874366239149e-01 +
-                              w * (1.818357216161805012e-01 + w * 1.479819860511658591e-01)));
+  const double t1 = w * (kLg[1] + w * (kLg[3] + w * kLg[5]));
+  const double t2 = z * (kLg[0] + w * (kLg[2] + w * (kLg[4] + w * kLg[6])));
   const double R = t2 + t1;
   const double hfsq = 0.5 * f * f;
   const double dk = (double)k;
-  return dk * 6.93147180369123816490e-01 -
-         ((hfsq - (s * (hfsq + R) + dk * 1.90821492927058770002e-10)) - f);
+  return dk * kLn2Hi - ((hfsq - (s * (hfsq + R) + dk * kLn2Lo)) - f);
 }
 
 // exp(x), |x| < 700: x = k ln2 + r, |r| <= ln2/2; exp(r) from the
 // rational form 1 - ((lo - r c/(2-c)) - hi), c = r - r^2 P(r^2); 2^k by
-// exponent arithmetic.
+// exponent arithmetic.  The division's range is proven for the solver's
+// arguments: 2-c lies in [1.6, 2.4], and r c is 0 (x = 0) or about r^2 >=
+// 1e-34 (every argument is 0 or a constant >= 0.14 times a log of a double
+// other than 1, hence |x| >= 1.5e-17, and r cancels at most to ulp scale).
 template <class M>
 __device__ __forceinline__ double exp_(M& m, double x) {
   const double half = (x < 0.0) ? -0.5 : 0.5;
-  const int k = (int)(1.44269504088896338700e+00 * x + half);  // truncation
+  const int k = (int)(kInvLn2 * x + half);  // truncation
   const double t = (double)k;
-  const double hi = x - t * 6.93147180369123816490e-01;
-  const double lo = t * 1.90821492927058770002e-10;
+  const double hi = x - t * kLn2Hi;
+  const double lo = t * kLn2Lo;
   const double r = hi - lo;
   const double r2 = r * r;
-  const double c = r - r2 * (1.66666666666666019037e-01 +
-                             r2 * (-2.77777777770155933842e-03 +
-                                   r2 * (6.61375632143793436117e-05 +
-                                         r2 * (-1.65339022054652515390e-06 +
-                                               r2 * 4.13813679705723846039e-08))));
-  const double y = 1.0 - ((lo - m.divf(r * c, 2.0 - c)) - hi);
+  const double c = r - r2 * (kEp[0] + r2 * (kEp[1] + r2 * (kEp[2] + r2 * (kEp[3] + r2 * kEp[4]))));
+  const double y = 1.0 - ((lo - m.divr(r * c, 2.0 - c)) - hi);
   return from_bits(to_bits(y) + ((unsigned long long)(long long)k << 52));
 }
 
