@@ -256,7 +256,10 @@ __device__ __forceinline__ bool sample0(M& m, const Face& fl, const Face& fr, co
     const double u = k.a2 * (l.c + k.hg * l.u + xi);
     const double c = k.a2 * (l.c + k.hg * (l.u - xi));
     const double lc = log_(m, m.divf(c, l.c));
-    out = {l.rho * exp_(m, k.er * lc), u, wl.vb, l.p * exp_(m, k.ep * lc)};
+    out.r = l.rho * exp_(m, k.er * lc);
+    out.va = u;
+    out.vb = wl.vb;
+    out.p = l.p * exp_(m, k.ep * lc);
     return true;
   }
   if (p > r.p) {  // right shock (:225-240)
@@ -277,7 +280,10 @@ __device__ __forceinline__ bool sample0(M& m, const Face& fl, const Face& fr, co
   const double u = k.a2 * (-r.c + k.hg * r.u + xi);
   const double c = k.a2 * (r.c - k.hg * (r.u - xi));
   const double lc = log_(m, m.divf(c, r.c));
-  out = {r.rho * exp_(m, k.er * lc), u, wr.vb, r.p * exp_(m, k.ep * lc)};
+  out.r = r.rho * exp_(m, k.er * lc);
+  out.va = u;
+  out.vb = wr.vb;
+  out.p = r.p * exp_(m, k.ep * lc);
   return true;
 }
 
