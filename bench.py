@@ -332,6 +332,21 @@ def main():
         if per_cell:
             traffic = per_cell * geo.nx * NY
 
+    # the bound that actually binds: FP64-pipe lane
+    # instructions of that kernel per cell (ncu, config 1 / hllc only) over
+    # 148 SMs x 64 FP64 lanes x the SM clock sampled during the timed region
+    fp64 = None
+    if os.path.exists(prof) and args.workload == "cfg1" and args.flux == "hllc":
+        per_cell = json.load(open(prof)).get(f"sweep_{which}_fp64_instr_per_cell")
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        mhz = (clock_info or {}).get("sm_mhz") or 1965.0
+        if per_cell:
+            ach = per_cell * geo.nx * NY / (avg_ms / 1e3)
+            pk = sms * 64 * mhz * 1e6
+            fp64 = {"bound": "fp64", "achieved": ach, "peak": pk, "unit": "FP64 lane-instr/s",
+                    "frac": ach / pk, "instr_per_cell": per_cell,
+                    "peak_source": f"{sms} SMs x 64 FP64 lanes x {mhz:.0f} MHz (sampled)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -414,7 +429,8 @@ def main():
             "roofline": {"bound": "hbm", "kernel": f"sweep_{which}", "achieved": achieved,
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms},
+                         "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms,
+                         "fp64_pipe": fp64},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": plane_bytes,
                     "d2h_bytes_per_step": plane_bytes},
             "gpu_launches": launches,
