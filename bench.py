@@ -220,6 +220,7 @@ def main():
         slab.bind_stream(stream)
         grid = slab.grid
         comm = S.TorchComm()
+        comm.setup_p2p(slab)  # peer-memory halo over NVLink if every rank can map its peers
 
     def one_step():
         grid.init_case(CASE, SEED)
@@ -369,6 +370,7 @@ def main():
             vslab = S.GpuSlab(geo, dx, dy, model, BC, local, flux=vflux)
             vslab.bind_stream(stream)
             vgrid = vslab.grid
+            comm.setup_p2p(vslab)
 
         def vrun():
             if world == 1:
@@ -423,6 +425,8 @@ def main():
                                    f"{args.flux}, {TSTEPS} time steps per bench step",
                        "global_batch": cells, "seq_len": TSTEPS,
                        "parallelism": f"row slabs x{world}" if world > 1 else "single GPU",
+                       "halo": (("peer-memory (row-sweep stores into neighbour inboxes)"
+                                 if comm.p2p else "nccl send/recv") if world > 1 else None),
                        "l2": "inputs larger than L2 (2 x %.0f MB state per GPU)"
                              % (4 * (geo.nx + 4) * (NY + 4) * 8 / 1e6),
                        "flux": args.flux, "seed": SEED},

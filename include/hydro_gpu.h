@@ -161,6 +161,31 @@ int hydro_gpu_halo(hydro_gpu_ctx* ctx, double** send_lo, double** send_hi,
                    double** recv_lo, double** recv_hi, size_t* count);
 int hydro_gpu_slab_sweep_x(hydro_gpu_ctx* ctx, int step);
 int hydro_gpu_slab_sweep_y(hydro_gpu_ctx* ctx, int step);
+/* Peer-memory halo (row slabs on NVLink-connected GPUs; replaces the per-step
+ * send/recv of hydro_gpu_halo's blocks).  Each slab owns an inbox of 2 step
+ * parities x 2 sides (side 0 = its ghost rows -1..0, side 1 = nx+1..nx+2),
+ * each one block of `count` doubles laid out like hydro_gpu_halo's.  With
+ * peers set, the row sweep of step s also stores the slab's updated rows 1..2
+ * into the upper neighbour's side-1 inbox of parity (s+1)&1 and rows
+ * nx-1..nx into the lower neighbour's side-0 inbox (the decomposition's
+ * InterfaceBuffer, proj/include/hydro/decomposition.hpp:58-79, written by
+ * the producing kernel); hydro_gpu_slab_inbox_in(step) copies the parity
+ * step&1 inbox into the ghost rows before the column sweep.  Writer and
+ * reader are ordered by the per-step dt min-allreduce between them, and the
+ * parity keeps a neighbour's next write off the block being read. */
+int hydro_gpu_inbox(hydro_gpu_ctx* ctx, double** inbox, size_t* count);
+/* cudaIpcMemHandle_t of the inbox allocation (64 bytes) for another process. */
+int hydro_gpu_inbox_ipc_handle(hydro_gpu_ctx* ctx, void* handle64);
+/* Maps a neighbour's inbox from its IPC handle (closed by hydro_gpu_destroy). */
+int hydro_gpu_ipc_open(hydro_gpu_ctx* ctx, const void* handle64, double** peer_inbox);
+/* Neighbour inboxes (NULL: physical wall / NCCL halo); upper = slab above
+ * (row0 smaller), lower = slab below. */
+int hydro_gpu_set_halo_peers(hydro_gpu_ctx* ctx, double* upper_inbox, double* lower_inbox);
+/* Copies the current rows 1..2 / nx-1..nx into the neighbours' inboxes of
+ * parity step&1 (the initial exchange, after hydro_gpu_slab_prologue). */
+int hydro_gpu_slab_halo_out(hydro_gpu_ctx* ctx, int step);
+/* Ghost rows of the non-wall sides from this slab's inbox of parity step&1. */
+int hydro_gpu_slab_inbox_in(hydro_gpu_ctx* ctx, int step);
 /* Writes the reference's end-of-run ghost state (mirrors of the last
  * column-sweep output, grid.cpp:23-60 as applied before the last row sweep). */
 int hydro_gpu_slab_finish(hydro_gpu_ctx* ctx);

@@ -76,6 +76,12 @@ def lib() -> C.CDLL:
         "hydro_gpu_halo": ([_ctx, P(_dp), P(_dp), P(_dp), P(_dp), P(sz)], i),
         "hydro_gpu_slab_sweep_x": ([_ctx, i], i),
         "hydro_gpu_slab_sweep_y": ([_ctx, i], i),
+        "hydro_gpu_inbox": ([_ctx, P(_dp), P(sz)], i),
+        "hydro_gpu_inbox_ipc_handle": ([_ctx, C.c_void_p], i),
+        "hydro_gpu_ipc_open": ([_ctx, C.c_void_p, P(_dp)], i),
+        "hydro_gpu_set_halo_peers": ([_ctx, C.c_void_p, C.c_void_p], i),
+        "hydro_gpu_slab_halo_out": ([_ctx, i], i),
+        "hydro_gpu_slab_inbox_in": ([_ctx, i], i),
         "hydro_gpu_slab_finish": ([_ctx], i),
         "hydro_gpu_decode_error": ([_ctx, u64, P(ErrorInfo)], i),
         "hydro_gpu_set_timing": ([_ctx, i], i),

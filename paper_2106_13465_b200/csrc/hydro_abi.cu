@@ -59,6 +59,12 @@ struct hydro_gpu_ctx {
   bool capturing = false;         // ev_begin/ev_end use dedicated graph events
   std::vector<cudaEvent_t> graph_events;
   size_t graph_next = 0;
+  // peer-memory halo (hydro_gpu_set_halo_peers): own inbox of 2 parities x 2
+  // sides, the neighbours' inboxes, IPC mappings to close
+  double* inbox = nullptr;
+  double* peer_up = nullptr;
+  double* peer_dn = nullptr;
+  std::vector<void*> ipc_opened;
 };
 
 namespace {
@@ -207,6 +213,11 @@ hb::SweepArgs sweep_args(hydro_gpu_ctx* c, int axis, int step) {
     a.src = c->B;
     a.dst = c->A;
     a.seg = c->seg_y;
+    // rows produced by this step's row sweep feed the neighbours' column
+    // sweep of step+1: inbox parity (step+1)&1
+    const size_t blk = 8 * c->pitch, par = (size_t)((step + 1) & 1);
+    if (c->peer_up) a.halo_up = c->peer_up + (par * 2 + 1) * blk;
+    if (c->peer_dn) a.halo_dn = c->peer_dn + (par * 2 + 0) * blk;
   }
   return a;
 }
@@ -465,7 +476,8 @@ int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out) {
   const size_t bytes = ctx->count * sizeof(double);
   if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&ctx->A, bytes) != cudaSuccess || cudaMalloc(&ctx->B, bytes) != cudaSuccess ||
-      cudaMalloc(&ctx->slots, kSlots * sizeof(unsigned long long)) != cudaSuccess) {
+      cudaMalloc(&ctx->slots, kSlots * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc(&ctx->inbox, 4 * 8 * ctx->pitch * sizeof(double)) != cudaSuccess) {
     hydro_gpu_destroy(ctx);
     cudaGetLastError();
     return HYDRO_GPU_ERR_CUDA;
@@ -479,6 +491,7 @@ int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out) {
   }
   cudaMemsetAsync(ctx->A, 0, bytes, ctx->stream);
   cudaMemsetAsync(ctx->B, 0, bytes, ctx->stream);
+  cudaMemsetAsync(ctx->inbox, 0, 4 * 8 * ctx->pitch * sizeof(double), ctx->stream);
   cudaMemsetAsync(ctx->slots, 0xff, 4 * sizeof(unsigned long long), ctx->stream);
   cudaMemsetAsync(ctx->slots + kSlotCounters, 0, sizeof(unsigned long long), ctx->stream);
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
@@ -499,6 +512,8 @@ int hydro_gpu_destroy(hydro_gpu_ctx* ctx) {
   if (ctx->A) cudaFree(ctx->A);
   if (ctx->B) cudaFree(ctx->B);
   if (ctx->slots) cudaFree(ctx->slots);
+  for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (ctx->inbox) cudaFree(ctx->inbox);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return HYDRO_GPU_OK;
@@ -718,6 +733,74 @@ int hydro_gpu_halo(hydro_gpu_ctx* c, double** send_lo, double** send_hi, double*
   if (recv_lo) *recv_lo = c->A + (size_t)(-1 + 1) * rowblk;      // rows -1..0
   if (recv_hi) *recv_hi = c->A + (size_t)(nx + 1 + 1) * rowblk;  // rows nx+1..nx+2
   if (count) *count = 2 * rowblk;
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_inbox(hydro_gpu_ctx* c, double** inbox, size_t* count) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  if (inbox) *inbox = c->inbox;
+  if (count) *count = 8 * c->pitch;
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_inbox_ipc_handle(hydro_gpu_ctx* c, void* handle64) {
+  if (!c || !handle64) return HYDRO_GPU_ERR_CONFIG;
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  DeviceGuard g(c->device);
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(c, cudaIpcGetMemHandle(&h, c->inbox));
+  std::memcpy(handle64, &h, sizeof h);
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_ipc_open(hydro_gpu_ctx* c, const void* handle64, double** peer_inbox) {
+  if (!c || !handle64 || !peer_inbox) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof h);
+  void* p = nullptr;
+  CUDA_TRY(c, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  c->ipc_opened.push_back(p);
+  *peer_inbox = static_cast<double*>(p);
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_set_halo_peers(hydro_gpu_ctx* c, double* upper_inbox, double* lower_inbox) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  if ((upper_inbox && c->cfg.wall_lo) || (lower_inbox && c->cfg.wall_hi))
+    return set_err(c, HYDRO_GPU_ERR_CONFIG, "a physical wall has no halo neighbour");
+  c->peer_up = upper_inbox;
+  c->peer_dn = lower_inbox;
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_slab_halo_out(hydro_gpu_ctx* c, int step) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  const size_t blk = 8 * c->pitch, rowblk = 4 * c->pitch, par = (size_t)(step & 1);
+  const size_t bytes = blk * sizeof(double);
+  if (c->peer_up)
+    CUDA_TRY(c, cudaMemcpyAsync(c->peer_up + (par * 2 + 1) * blk, c->A + 2 * rowblk, bytes,
+                                cudaMemcpyDeviceToDevice, c->stream));
+  if (c->peer_dn)
+    CUDA_TRY(c, cudaMemcpyAsync(c->peer_dn + (par * 2 + 0) * blk,
+                                c->A + (size_t)c->cfg.nx * rowblk, bytes,
+                                cudaMemcpyDeviceToDevice, c->stream));
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_slab_inbox_in(hydro_gpu_ctx* c, int step) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  const size_t blk = 8 * c->pitch, rowblk = 4 * c->pitch, par = (size_t)(step & 1);
+  const size_t bytes = blk * sizeof(double);
+  if (!c->cfg.wall_lo)  // ghost rows -1..0
+    CUDA_TRY(c, cudaMemcpyAsync(c->A, c->inbox + (par * 2 + 0) * blk, bytes,
+                                cudaMemcpyDeviceToDevice, c->stream));
+  if (!c->cfg.wall_hi)  // ghost rows nx+1..nx+2
+    CUDA_TRY(c, cudaMemcpyAsync(c->A + (size_t)(c->cfg.nx + 2) * rowblk,
+                                c->inbox + (par * 2 + 1) * blk, bytes, cudaMemcpyDeviceToDevice,
+                                c->stream));
   return HYDRO_GPU_OK;
 }
 

@@ -691,6 +691,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
   double* __restrict__ dst = a.dst;
   double spd_max = 0.0;  // speeds are >= +0
   unsigned long long dt_key = kNoError;
+  bool wrote_peer = false;
 
   for (int item = claim(a.counter); item < items; item = claim(a.counter)) {
     const int grp = item % groups, sg = item / groups;
@@ -707,6 +708,10 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
     // warps holding x-wall rows write the ghost rows of the next step
     const bool mirror_lo = a.wall_lo && grp == 0;
     const bool mirror_hi = a.wall_hi && (grp << 5) + 32 >= nx - 1;  // rows nx-1, nx
+    // peer-memory halo: rows 1..2 / nx-1..nx also go to the neighbours' inboxes
+    const bool send_up = a.halo_up && grp == 0;
+    const bool send_dn = a.halo_dn && (grp << 5) + 32 >= nx - 1;
+    wrote_peer |= send_up | send_dn;
     const int gi = a.row0 + i;
     const unsigned long long base = error_key(a.step, 2, gi, 0, 0, 0);
     auto put_row = [&](int ii, int j, const Cons& u, bool neg) {
@@ -714,6 +719,12 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
       q[0] = u.r;
       q[2 * pitch] = u.ma;
       q[pitch] = neg ? -u.mb : u.mb;
+      q[3 * pitch] = u.e;
+    };
+    auto put_peer = [&](double* q, const Cons& u) {  // NVLink store into a peer's inbox
+      q[0] = u.r;
+      q[2 * pitch] = u.ma;
+      q[pitch] = u.mb;
       q[3 * pitch] = u.e;
     };
     double spd_item;
@@ -735,6 +746,10 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
           if (refl) put_row(2 * nx + 1 - i, j, o.un, true);
           else if (i == nx) { put_row(nx + 1, j, o.un, false); put_row(nx + 2, j, o.un, false); }
         }
+        if (send_up && active && i <= 2)  // -> upper neighbour's ghost rows nx'+1..nx'+2
+          put_peer(a.halo_up + (size_t)(i - 1) * 4 * pitch + (j + kColOff), o.un);
+        if (send_dn && active && i >= nx - 1)  // -> lower neighbour's ghost rows -1..0
+          put_peer(a.halo_dn + (size_t)(i - (nx - 1)) * 4 * pitch + (j + kColOff), o.un);
         if (a.want_limit) {
           if (o.fD >= 0) keep_min(dt_item, error_key(a.step + 1, 0, gi, 0, j, o.fD));
           else spd_item = smax(spd_item, o.spd);
@@ -763,6 +778,9 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
     }
   }
   if (lane == 0) bulk_wait0();
+  // peer stores performed system-wide before this kernel completes (the
+  // neighbour reads them after the dt allreduce that follows on the stream)
+  if (wrote_peer) __threadfence_system();
   if (a.want_limit) {
     // largest speed of the warp (non-negative doubles order like their bits)
     // -> its cell_dt_limit, the warp's minimum limit

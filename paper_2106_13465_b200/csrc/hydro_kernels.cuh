@@ -58,6 +58,8 @@ struct SweepArgs {
   int want_limit;             // row sweep: produce limit_out
   unsigned* counter;          // work-item counter of this sweep (starts at 0)
   unsigned* counter_next;     // the other sweep's counter, reset for its launch
+  double* halo_up;            // row sweep: upper neighbour's inbox block for rows 1..2
+  double* halo_dn;            // row sweep: lower neighbour's inbox block for rows nx-1..nx
 };
 
 struct TmaMaps {

@@ -299,6 +299,33 @@ class GpuGrid:
         self._check(self._lib.hydro_gpu_error_slot(self._ctx, C.byref(p)))
         return C.cast(p, C.c_void_p).value
 
+    # peer-memory halo (include/hydro_gpu.h: hydro_gpu_inbox ...) -------------
+    def inbox(self) -> tuple[int, int]:
+        p = L._dp()
+        count = C.c_size_t()
+        self._check(self._lib.hydro_gpu_inbox(self._ctx, C.byref(p), C.byref(count)))
+        return C.cast(p, C.c_void_p).value, count.value
+
+    def inbox_ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        self._check(self._lib.hydro_gpu_inbox_ipc_handle(self._ctx, buf))
+        return buf.raw
+
+    def ipc_open(self, handle: bytes) -> int:
+        buf = C.create_string_buffer(bytes(handle), 64)
+        p = L._dp()
+        self._check(self._lib.hydro_gpu_ipc_open(self._ctx, buf, C.byref(p)))
+        return C.cast(p, C.c_void_p).value
+
+    def set_halo_peers(self, upper: int | None, lower: int | None):
+        self._check(self._lib.hydro_gpu_set_halo_peers(self._ctx, upper or None, lower or None))
+
+    def slab_halo_out(self, step: int):
+        self._check(self._lib.hydro_gpu_slab_halo_out(self._ctx, step))
+
+    def slab_inbox_in(self, step: int):
+        self._check(self._lib.hydro_gpu_slab_inbox_in(self._ctx, step))
+
     def halo(self) -> dict:
         ptrs = [L._dp() for _ in range(4)]
         count = C.c_size_t()

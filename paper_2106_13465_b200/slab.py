@@ -15,10 +15,23 @@ near-equal slabs, one per rank, exactly like split_range
 The driver is written against two small protocols so the same code path runs
 over NCCL on B200s (GpuSlab + TorchComm(nccl)) and over gloo on CPU in the
 tests (an oracle-backed slab + TorchComm(gloo)).
+
+Halo transport.  With peer memory (NVLink; CUDA IPC between the rank
+processes) the halo needs no communication call at all: the row sweep of
+step s stores its rows 1..2 / n-1..n straight into the neighbours' inboxes
+(parity (s+1)&1) and each rank copies its own inbox into its ghost rows
+before the column sweep of step s+1 (include/hydro_gpu.h,
+hydro_gpu_set_halo_peers).  The dt min-allreduce that sits between the two on
+every rank's stream is the synchronisation: a neighbour's allreduce of step
+s+1 cannot complete before this rank's row sweep of step s has, and the
+inbox parity keeps the neighbour's next write off the block being read.  All
+ranks agree on the transport collectively (TorchComm.setup_p2p); otherwise
+(or with HYDRO_HALO=nccl) the halo is one batched send/recv per neighbour.
 """
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import torch
@@ -93,9 +106,30 @@ class GpuSlab:
         self._limits = [device_tensor(self.grid.limit_slot(s), 1, device=self.device)
                         for s in (0, 1)]
         self._err = device_tensor(self.grid.error_slot(), 1, torch.int64, device=self.device)
+        self.p2p = False
 
     def bind_stream(self, stream: torch.cuda.Stream):
         self.grid.set_stream(stream.cuda_stream)
+
+    # peer-memory halo --------------------------------------------------------
+    def inbox_ptr(self) -> int:
+        return self.grid.inbox()[0]
+
+    def ipc_handle(self) -> bytes:
+        return self.grid.inbox_ipc_handle()
+
+    def open_peer(self, handle: bytes) -> int:
+        return self.grid.ipc_open(handle)
+
+    def set_peers(self, upper: int | None, lower: int | None):
+        self.grid.set_halo_peers(upper, lower)
+        self.p2p = True
+
+    def halo_out(self, step: int):
+        self.grid.slab_halo_out(step)
+
+    def inbox_in(self, step: int):
+        self.grid.slab_inbox_in(step)
 
     # phases ------------------------------------------------------------------
     def prologue(self, step: int):
@@ -162,6 +196,42 @@ class TorchComm:
             req.wait()
         slab.halo_done()
 
+    def _all_true(self, ok: bool) -> bool:
+        dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return bool(t.item())
+
+    def setup_p2p(self, slab) -> bool:
+        """Collective: maps the neighbours' inboxes into this rank (CUDA IPC)
+        and switches every rank to the peer-memory halo -- only if all ranks
+        succeeded, so the ranks never disagree on the transport."""
+        self.p2p = False
+        if self.world == 1:
+            return False
+        want = os.environ.get("HYDRO_HALO", "p2p") == "p2p"
+        ok, handle = want, None
+        if ok:
+            try:
+                handle = slab.ipc_handle()
+            except Exception:  # noqa: BLE001 -- any failure means: use NCCL
+                ok = False
+        handles = [None] * self.world
+        self.dist.all_gather_object(handles, handle, group=self.group)
+        up = dn = None
+        if ok:
+            try:
+                if self.rank > 0:
+                    up = slab.open_peer(handles[self.rank - 1])
+                if self.rank < self.world - 1:
+                    dn = slab.open_peer(handles[self.rank + 1])
+            except Exception:  # noqa: BLE001
+                ok = False
+        if self._all_true(ok):
+            slab.set_peers(up, dn)
+            self.p2p = True
+        return self.p2p
+
     def first_error(self, key: torch.Tensor) -> int:
         if self.world == 1:
             keys = [key.clone()]
@@ -178,6 +248,17 @@ class LoopbackComm:
 
     def __init__(self, slabs):
         self.slabs = slabs
+        self.p2p = False
+
+    def setup_p2p(self) -> bool:
+        """Peer-memory halo between slabs of one process: the neighbours'
+        inboxes are plain device pointers (no IPC needed)."""
+        ptrs = [s.inbox_ptr() for s in self.slabs]
+        n = len(self.slabs)
+        for k, s in enumerate(self.slabs):
+            s.set_peers(ptrs[k - 1] if k > 0 else None, ptrs[k + 1] if k < n - 1 else None)
+        self.p2p = n > 1
+        return self.p2p
 
     def min_limit_all(self, step: int):
         lims = torch.stack([s.limit(step) for s in self.slabs])
@@ -204,10 +285,16 @@ def run_slab(slab, comm: TorchComm, steps: int) -> None:
     final error gather."""
     if steps <= 0:
         return
+    p2p = getattr(comm, "p2p", False)
     slab.prologue(0)
+    if p2p:
+        slab.halo_out(0)
     for s in range(steps):
-        comm.min_limit(slab.limit(s))
-        comm.swap_halos(slab)
+        comm.min_limit(slab.limit(s))  # also orders the peer-memory halo
+        if p2p:
+            slab.inbox_in(s)
+        else:
+            comm.swap_halos(slab)
         slab.sweep_x(s)
         slab.sweep_y(s)
     slab.finish()
@@ -216,16 +303,25 @@ def run_slab(slab, comm: TorchComm, steps: int) -> None:
         slab.raise_error(key)
 
 
-def run_loopback(slabs, steps: int) -> None:
+def run_loopback(slabs, steps: int, p2p: bool = False) -> None:
     """Same schedule as run_slab for several slabs held by one process."""
     if steps <= 0:
         return
     comm = LoopbackComm(slabs)
+    if p2p:
+        comm.setup_p2p()
     for sl in slabs:
         sl.prologue(0)
+    if comm.p2p:
+        for sl in slabs:
+            sl.halo_out(0)
     for s in range(steps):
         comm.min_limit_all(s)
-        comm.swap_halos_all()
+        if comm.p2p:
+            for sl in slabs:
+                sl.inbox_in(s)
+        else:
+            comm.swap_halos_all()
         for sl in slabs:
             sl.sweep_x(s)
         for sl in slabs:

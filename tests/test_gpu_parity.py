@@ -207,11 +207,14 @@ def test_tolerance_metric_is_zero(gpu):
     assert max_rel <= 1e-12 and max_rel == 0.0 and l1 == 0.0
 
 
+@pytest.mark.parametrize("p2p", [False, True])
 @pytest.mark.parametrize("world,case,bc", [(2, "corner_blast", "reflect"), (3, "random", "transmit"),
-                                           (4, "sod_x", "transmit")])
-def test_slab_decomposition_loopback(gpu, world, case, bc):
+                                           (4, "sod_x", "transmit"), (5, "random", "reflect")])
+def test_slab_decomposition_loopback(gpu, world, case, bc, p2p):
     """Row slabs with halo swaps and the dt min-reduction, all slabs on one
-    device (the multi-GPU schedule without waiting kernels)."""
+    device (the multi-GPU schedule without waiting kernels).  p2p: the row
+    sweep stores the halo rows into the neighbours' inboxes itself
+    (hydro_gpu_set_halo_peers), as over NVLink."""
     import torch
 
     from paper_2106_13465_b200 import slab as S
@@ -225,7 +228,7 @@ def test_slab_decomposition_loopback(gpu, world, case, bc):
         sl.bind_stream(stream)
         sl.grid.upload(S.slab_planes(full.planes, nx, world, r))
         slabs.append(sl)
-    S.run_loopback(slabs, steps)
+    S.run_loopback(slabs, steps, p2p=p2p)
     torch.cuda.synchronize()
     parts = []
     for sl in slabs:

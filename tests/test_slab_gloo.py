@@ -79,15 +79,71 @@ class OracleSlab:
         raise RuntimeError(f"error key {key:x}")
 
 
-def _worker(rank, world, port, case, bc, outdir):
+class PeerOracleSlab(OracleSlab):
+    """OracleSlab with the peer-memory halo of GpuSlab: the inbox (2 parities
+    x 2 sides x one 2-row block) is a shared file mapping, its "IPC handle"
+    the file name, and the row sweep writes its rows 1..2 / n-1..n into the
+    neighbours' inboxes of parity (s+1)&1 -- the same protocol as the row
+    sweep kernel over NVLink, exercised by real concurrent processes."""
+
+    def __init__(self, geo, planes, dx, dy, bc, outdir, fail_handle=False):
+        super().__init__(geo, planes, dx, dy, bc)
+        self.path = os.path.join(outdir, f"inbox{geo.rank}.bin")
+        self.inbox = np.memmap(self.path, dtype=np.float64, mode="w+", shape=(2, 2, 4, 2, NY + 4))
+        self.fail_handle = fail_handle
+        self.up = self.dn = None
+        self.p2p = False
+
+    def ipc_handle(self):
+        if self.fail_handle:
+            raise RuntimeError("no peer access")
+        return self.path.encode()
+
+    def open_peer(self, handle):
+        return np.memmap(handle.decode(), dtype=np.float64, mode="r+", shape=(2, 2, 4, 2, NY + 4))
+
+    def set_peers(self, upper, lower):
+        self.up, self.dn = upper, lower
+        self.p2p = True
+
+    def halo_out(self, step):
+        par, n, u = step & 1, self.geo.nx, self.g.u
+        if self.up is not None:
+            self.up[par, 1] = u[:, 2:4, :]      # rows 1..2 -> its ghost rows n'+1..n'+2
+            self.up.flush()
+        if self.dn is not None:
+            self.dn[par, 0] = u[:, n:n + 2, :]  # rows n-1..n -> its ghost rows -1..0
+            self.dn.flush()
+
+    def inbox_in(self, step):
+        par, n = step & 1, self.geo.nx
+        if not self.geo.wall_lo:
+            self.g.u[:, 0:2, :] = self.inbox[par, 0]
+        if not self.geo.wall_hi:
+            self.g.u[:, n + 2:n + 4, :] = self.inbox[par, 1]
+
+    def sweep_y(self, step):
+        super().sweep_y(step)
+        if self.p2p:
+            self.halo_out(step + 1)
+
+
+def _worker(rank, world, port, case, bc, outdir, mode="nccl"):
     import torch.distributed as dist
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                            world_size=world)
     full = O.make_case(case, NX, NY, seed=6)
     geo = S.SlabGeometry(NX, NY, rank, world)
     planes = S.slab_planes(full.u, NX, world, rank)
-    sl = OracleSlab(geo, planes, full.dx, full.dy, bc)
-    S.run_slab(sl, S.TorchComm(), STEPS)
+    comm = S.TorchComm()
+    if mode == "nccl":
+        sl = OracleSlab(geo, planes, full.dx, full.dy, bc)
+    else:
+        sl = PeerOracleSlab(geo, planes, full.dx, full.dy, bc, outdir,
+                            fail_handle=(mode == "p2p_fail" and rank == 1))
+        used = comm.setup_p2p(sl)
+        assert used == (mode == "p2p")  # every rank agrees on the transport
+    S.run_slab(sl, comm, STEPS)
     np.save(os.path.join(outdir, f"slab{rank}.npy"), sl.g.u)
     dist.destroy_process_group()
 
@@ -103,6 +159,22 @@ def _free_port():
 def test_slab_driver_over_gloo_matches_single_domain(world, case, bc):
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_worker, args=(world, _free_port(), case, bc, d), nprocs=world, join=True)
+        parts = [np.load(os.path.join(d, f"slab{r}.npy")) for r in range(world)]
+    got = S.gather_planes(parts, NX, NY)
+    ref = O.make_case(case, NX, NY, seed=6)
+    O.run_sequential(ref, STEPS, bc)
+    assert np.array_equal(got[:, 2:NX + 2, 2:NY + 2], ref.u[:, 2:NX + 2, 2:NY + 2])
+
+
+@pytest.mark.parametrize("mode", ["p2p", "p2p_fail"])
+@pytest.mark.parametrize("world,case,bc", [(2, "random", "transmit"), (3, "corner_blast", "reflect")])
+def test_peer_memory_halo_schedule_over_gloo(world, case, bc, mode):
+    """The peer-memory halo protocol (row sweep writes the neighbours' inbox
+    of parity (s+1)&1, the reader copies parity s&1 after the dt allreduce)
+    with truly concurrent ranks; p2p_fail: one rank cannot export its inbox,
+    so all ranks fall back to send/recv together."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(world, _free_port(), case, bc, d, mode), nprocs=world, join=True)
         parts = [np.load(os.path.join(d, f"slab{r}.npy")) for r in range(world)]
     got = S.gather_planes(parts, NX, NY)
     ref = O.make_case(case, NX, NY, seed=6)
