@@ -673,7 +673,9 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : 2)
   if (lane == 0) bulk_wait0();
 }
 
-template <int FLUX>
+// PEER: also store the halo rows into the neighbours' inboxes (peer-memory
+// halo; a separate instantiation keeps the single-GPU path unchanged).
+template <int FLUX, bool PEER>
 __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel(SweepArgs a,
                                                        const __grid_constant__ CUtensorMap load_map,
                                                        const __grid_constant__ CUtensorMap store_map) {
@@ -709,8 +711,8 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
     const bool mirror_lo = a.wall_lo && grp == 0;
     const bool mirror_hi = a.wall_hi && (grp << 5) + 32 >= nx - 1;  // rows nx-1, nx
     // peer-memory halo: rows 1..2 / nx-1..nx also go to the neighbours' inboxes
-    const bool send_up = a.halo_up && grp == 0;
-    const bool send_dn = a.halo_dn && (grp << 5) + 32 >= nx - 1;
+    const bool send_up = PEER && a.halo_up && grp == 0;
+    const bool send_dn = PEER && a.halo_dn && (grp << 5) + 32 >= nx - 1;
     wrote_peer |= send_up | send_dn;
     const int gi = a.row0 + i;
     const unsigned long long base = error_key(a.step, 2, gi, 0, 0, 0);
@@ -746,10 +748,12 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
           if (refl) put_row(2 * nx + 1 - i, j, o.un, true);
           else if (i == nx) { put_row(nx + 1, j, o.un, false); put_row(nx + 2, j, o.un, false); }
         }
-        if (send_up && active && i <= 2)  // -> upper neighbour's ghost rows nx'+1..nx'+2
-          put_peer(a.halo_up + (size_t)(i - 1) * 4 * pitch + (j + kColOff), o.un);
-        if (send_dn && active && i >= nx - 1)  // -> lower neighbour's ghost rows -1..0
-          put_peer(a.halo_dn + (size_t)(i - (nx - 1)) * 4 * pitch + (j + kColOff), o.un);
+        if constexpr (PEER) {
+          if (send_up && active && i <= 2)  // -> upper neighbour's ghost rows nx'+1..nx'+2
+            put_peer(a.halo_up + (size_t)(i - 1) * 4 * pitch + (j + kColOff), o.un);
+          if (send_dn && active && i >= nx - 1)  // -> lower neighbour's ghost rows -1..0
+            put_peer(a.halo_dn + (size_t)(i - (nx - 1)) * 4 * pitch + (j + kColOff), o.un);
+        }
         if (a.want_limit) {
           if (o.fD >= 0) keep_min(dt_item, error_key(a.step + 1, 0, gi, 0, j, o.fD));
           else spd_item = smax(spd_item, o.spd);
@@ -780,7 +784,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
   if (lane == 0) bulk_wait0();
   // peer stores performed system-wide before this kernel completes (the
   // neighbour reads them after the dt allreduce that follows on the stream)
-  if (wrote_peer) __threadfence_system();
+  if (PEER && wrote_peer) __threadfence_system();
   if (a.want_limit) {
     // largest speed of the warp (non-negative doubles order like their bits)
     // -> its cell_dt_limit, the warp's minimum limit
@@ -1025,8 +1029,10 @@ int query_geometry(Geometry* g) {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(sweep_y_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
-  cudaFuncSetAttribute(sweep_y_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
+  cudaFuncSetAttribute(sweep_y_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
+  cudaFuncSetAttribute(sweep_y_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
+  cudaFuncSetAttribute(sweep_y_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
+  cudaFuncSetAttribute(sweep_y_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
   int ox = 0, oy = 0, ox1 = 0, oy1 = 0;
 #if HB_X_TMA
   cudaFuncSetAttribute(sweep_x_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
@@ -1037,8 +1043,8 @@ int query_geometry(Geometry* g) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, sweep_x_kernel<0>, 128, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox1, sweep_x_kernel<1>, 128, 0);
 #endif
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy, sweep_y_kernel<0>, 128, kYSmemBytes);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy1, sweep_y_kernel<1>, 128, kYSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy, sweep_y_kernel<0, false>, 128, kYSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy1, sweep_y_kernel<1, false>, 128, kYSmemBytes);
   g->ctas_x_per_sm = ox > 0 ? ox : 1;
   g->ctas_y_per_sm = oy > 0 ? oy : 1;
   g->ctas_x_exact = ox1 > 0 ? ox1 : 1;
@@ -1116,10 +1122,13 @@ void launch_sweep_y(const SweepArgs& a0, const TmaMaps& maps, const Geometry& ge
   if (a.seg <= 0) a.seg = pick_seg(a.ny, a.nx, ctas * 4);
   a.seg = (a.seg + kChunk - 1) / kChunk * kChunk;  // chunks never straddle segments
   a.nseg = (a.ny + a.seg - 1) / a.seg;
+  const bool peer = a.halo_up || a.halo_dn;
   if (a.flux == 1)
-    sweep_y_kernel<1><<<ctas, 128, kYSmemBytes, s>>>(a, maps.y_load, maps.y_store);
+    peer ? sweep_y_kernel<1, true><<<ctas, 128, kYSmemBytes, s>>>(a, maps.y_load, maps.y_store)
+         : sweep_y_kernel<1, false><<<ctas, 128, kYSmemBytes, s>>>(a, maps.y_load, maps.y_store);
   else
-    sweep_y_kernel<0><<<ctas, 128, kYSmemBytes, s>>>(a, maps.y_load, maps.y_store);
+    peer ? sweep_y_kernel<0, true><<<ctas, 128, kYSmemBytes, s>>>(a, maps.y_load, maps.y_store)
+         : sweep_y_kernel<0, false><<<ctas, 128, kYSmemBytes, s>>>(a, maps.y_load, maps.y_store);
 }
 
 void launch_prologue(const PrologueArgs& a, cudaStream_t s) {
