@@ -110,10 +110,16 @@ struct Side {
 
 using K = ExactK;
 
+// Divisions: every numerator below is nonzero in a valid state (pressures,
+// densities, sound speeds, constants), so they take FastMath's plain range
+// test (divn/divnf; a zero or tiny numerator just redoes the item); only the
+// Newton step f/df, whose f vanishes at convergence, keeps the signed-zero
+// form (divf, over df > 0).
+
 // make_side (exact_riemann.cpp:17-22) of a face, whose 1/rho is at hand
 template <class M>
 __device__ __forceinline__ Side make_side(M& m, const Face& f, double gamma) {
-  return {f.w.r, f.w.va, f.w.p, m.sqrt(m.div(gamma * f.w.p, f.rr))};
+  return {f.w.r, f.w.va, f.w.p, m.sqrt(m.divn(gamma * f.w.p, f.rr))};
 }
 
 // Per-side constants of f_K / f_K' (exact_riemann.cpp:26-45): the same
@@ -127,8 +133,8 @@ struct SideK {
 };
 template <class M>
 __device__ __forceinline__ SideK side_k(M& m, const Side& s, const K& k) {
-  return {m.divf(2.0, k.gp1 * s.rho), k.gm * s.p, m.divf(2.0 * s.c, k.gm1),
-          m.divf(1.0, s.rho * s.c), m.recip(s.p)};
+  return {m.divnf(2.0, k.gp1 * s.rho), k.gm * s.p, m.divnf(2.0 * s.c, k.gm1),
+          m.divnf(1.0, s.rho * s.c), m.recip(s.p)};
 }
 
 // f_K(p) and f_K'(p) of one side at the same p (exact_riemann.cpp:26-45);
@@ -138,11 +144,11 @@ __device__ __forceinline__ void side_fn2(M& m, double p, const Side& s, const Si
                                          const K& k, double& f, double& df) {
   if (p > s.p) {
     const Recip d = m.recip(p + sk.b);
-    const double root = m.sqrt(m.div(sk.a, d));
+    const double root = m.sqrt(m.divn(sk.a, d));
     f = (p - s.p) * root;
-    df = root * (1.0 - m.div(0.5 * (p - s.p), d));
+    df = root * (1.0 - m.divn(0.5 * (p - s.p), d));
   } else {
-    const double l = log_(m, m.div(p, sk.rp));
+    const double l = log_(m, m.divn(p, sk.rp));
     f = sk.cf * (exp_(m, k.z * l) - 1.0);
     df = sk.dn * exp_(m, k.zn * l);
   }
@@ -157,14 +163,14 @@ template <class M>
 __device__ __forceinline__ SideEval side_eval(M& m, double p, const Side& s, const K& k) {
   SideEval e;
   if (p > s.p) {
-    const double a = m.divf(2.0, k.gp1 * s.rho);
+    const double a = m.divnf(2.0, k.gp1 * s.rho);
     const double b = k.gm * s.p;
-    e.f = (p - s.p) * m.sqrt(m.divf(a, p + b));
+    e.f = (p - s.p) * m.sqrt(m.divnf(a, p + b));
     e.L = e.E = 0.0;
   } else {
-    e.L = log_(m, m.divf(p, s.p));
+    e.L = log_(m, m.divnf(p, s.p));
     e.E = exp_(m, k.z * e.L);
-    e.f = m.divf(2.0 * s.c, k.gm1) * (e.E - 1.0);
+    e.f = m.divnf(2.0 * s.c, k.gm1) * (e.E - 1.0);
   }
   return e;
 }
@@ -195,7 +201,7 @@ __device__ __forceinline__ bool sample0(M& m, const Face& fl, const Face& fr, co
   if (same) r = l;
   else r = make_side(m, fr, g);
   const double du = wr.va - wl.va;
-  if (m.divf(2.0 * (l.c + r.c), k.gm1) <= du) return false;
+  if (m.divnf(2.0 * (l.c + r.c), k.gm1) <= du) return false;
 
   const bool rmin = r.p < l.p;
   const double p_min = rmin ? r.p : l.p;  // smin(l.p, r.p)
@@ -205,11 +211,11 @@ __device__ __forceinline__ bool sample0(M& m, const Face& fl, const Face& fr, co
   if (fo + du >= 0.0) {
     // both rarefactions: closed-form root (:63-69)
     const double numer = l.c + r.c - k.hg * du;
-    const double ql = m.divf(l.c, pow_(m, l.p, k.z));
+    const double ql = m.divnf(l.c, pow_(m, l.p, k.z));
     double qr = ql;
-    if (!same) qr = m.divf(r.c, pow_(m, r.p, k.z));
+    if (!same) qr = m.divnf(r.c, pow_(m, r.p, k.z));
     const double denom = ql + qr;
-    p = pow_(m, m.divf(numer, denom), k.iz);
+    p = pow_(m, m.divnf(numer, denom), k.iz);
   } else {
     // Newton from the linearised guess with the p_min floor, 10 iterations
     const double guess =
@@ -239,10 +245,10 @@ __device__ __forceinline__ bool sample0(M& m, const Face& fl, const Face& fr, co
   const double xi = 0.0;
   if (xi <= u_star) {  // left of the contact (:208-223)
     if (p > l.p) {     // left shock
-      const double ratio = m.divf(p, l.p);
+      const double ratio = m.divnf(p, l.p);
       const double head = l.u - l.c * m.sqrt(k.zp * ratio + k.z);
       if (xi <= head) { out = wl; return true; }
-      out = {m.divf(l.rho * (ratio + k.gm), k.gm * ratio + 1.0), u_star, wl.vb, p};
+      out = {m.divnf(l.rho * (ratio + k.gm), k.gm * ratio + 1.0), u_star, wl.vb, p};
       return true;
     }
     const double head = l.u - l.c;  // left rarefaction
@@ -255,7 +261,7 @@ __device__ __forceinline__ bool sample0(M& m, const Face& fl, const Face& fr, co
     }
     const double u = k.a2 * (l.c + k.hg * l.u + xi);
     const double c = k.a2 * (l.c + k.hg * (l.u - xi));
-    const double lc = log_(m, m.divf(c, l.c));
+    const double lc = log_(m, m.divnf(c, l.c));
     out.r = l.rho * exp_(m, k.er * lc);
     out.va = u;
     out.vb = wl.vb;
@@ -263,10 +269,10 @@ __device__ __forceinline__ bool sample0(M& m, const Face& fl, const Face& fr, co
     return true;
   }
   if (p > r.p) {  // right shock (:225-240)
-    const double ratio = m.divf(p, r.p);
+    const double ratio = m.divnf(p, r.p);
     const double head = r.u + r.c * m.sqrt(k.zp * ratio + k.z);
     if (xi >= head) { out = wr; return true; }
-    out = {m.divf(r.rho * (ratio + k.gm), k.gm * ratio + 1.0), u_star, wr.vb, p};
+    out = {m.divnf(r.rho * (ratio + k.gm), k.gm * ratio + 1.0), u_star, wr.vb, p};
     return true;
   }
   const double head = r.u + r.c;  // right rarefaction
@@ -279,7 +285,7 @@ __device__ __forceinline__ bool sample0(M& m, const Face& fl, const Face& fr, co
   }
   const double u = k.a2 * (-r.c + k.hg * r.u + xi);
   const double c = k.a2 * (r.c - k.hg * (r.u - xi));
-  const double lc = log_(m, m.divf(c, r.c));
+  const double lc = log_(m, m.divnf(c, r.c));
   out.r = r.rho * exp_(m, k.er * lc);
   out.va = u;
   out.vb = wr.vb;
