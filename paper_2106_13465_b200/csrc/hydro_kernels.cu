@@ -760,10 +760,10 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel
         }
       };
       unsigned long long ek = kNoError;
-      const bool ok =
-          a.want_limit
-              ? walk_strip<M, true, FLUX>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, base, 0, ek)
-              : walk_strip<M, false, FLUX>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, base, 0, ek);
+      // the signal speeds are evaluated even when no limit is wanted (the last
+      // step of a run, advance): one walker instantiation per math policy
+      // keeps the kernel's code within the instruction cache
+      const bool ok = walk_strip<M, true, FLUX>(t.ka, t.kb, t, sink, g, dtdx, a.spacing, base, 0, ek);
       t.end();
       return make_pair_ok(ok, ek);
     };
