@@ -223,6 +223,9 @@ __device__ __forceinline__ int claim(unsigned* counter) {
 #ifndef HB_Y_MINB
 #define HB_Y_MINB 4
 #endif
+#ifndef HB_EX_MINB  // exact-10 sweeps (long log/exp chains, ~200 registers)
+#define HB_EX_MINB 3
+#endif
 
 #if !HB_X_TMA  // the register-prefetch column sweep (A/B reference)
 // ---------------------------------------------------------------------------
@@ -255,7 +258,7 @@ struct ColumnSource {
 // The exact-10 flux needs far more live state than HLLC: it gets the
 // register file of 2 CTAs/SM instead of a spilling 128-register cap.
 template <int FLUX>
-__global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : 2) sweep_x_kernel(SweepArgs a) {
+__global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : HB_EX_MINB) sweep_x_kernel(SweepArgs a) {
   if (latched(a)) return;
   const int lane = threadIdx.x & 31;
   if (*(volatile unsigned long long*)a.dt_err != kNoError) {
@@ -587,7 +590,7 @@ __device__ __forceinline__ Tiles<AXIS> make_tiles(const CUtensorMap* load_map,
 
 // Column sweep with TMA-staged tiles (same pipeline as the row sweep).
 template <int FLUX>
-__global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : 2)
+__global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : HB_EX_MINB)
     sweep_x_tma_kernel(SweepArgs a, const __grid_constant__ CUtensorMap load_map,
                        const __grid_constant__ CUtensorMap store_map) {
   if (latched(a)) return;
@@ -676,7 +679,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : 2)
 // PEER: also store the halo rows into the neighbours' inboxes (peer-memory
 // halo; a separate instantiation keeps the single-GPU path unchanged).
 template <int FLUX, bool PEER>
-__global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : 2) sweep_y_kernel(SweepArgs a,
+__global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : HB_EX_MINB) sweep_y_kernel(SweepArgs a,
                                                        const __grid_constant__ CUtensorMap load_map,
                                                        const __grid_constant__ CUtensorMap store_map) {
   if (latched(a)) return;
