@@ -10,6 +10,7 @@ reference run.
 import os
 import socket
 import tempfile
+import time
 
 import numpy as np
 import pytest
@@ -86,8 +87,10 @@ class PeerOracleSlab(OracleSlab):
     neighbours' inboxes of parity (s+1)&1 -- the same protocol as the row
     sweep kernel over NVLink, exercised by real concurrent processes."""
 
-    def __init__(self, geo, planes, dx, dy, bc, outdir, fail_handle=False):
+    def __init__(self, geo, planes, dx, dy, bc, outdir, fail_handle=False, jitter=0.0):
         super().__init__(geo, planes, dx, dy, bc)
+        self.rng = np.random.default_rng(geo.rank)
+        self.jitter = jitter
         self.path = os.path.join(outdir, f"inbox{geo.rank}.bin")
         self.inbox = np.memmap(self.path, dtype=np.float64, mode="w+", shape=(2, 2, 4, 2, NY + 4))
         self.fail_handle = fail_handle
@@ -115,7 +118,16 @@ class PeerOracleSlab(OracleSlab):
             self.dn[par, 0] = u[:, n:n + 2, :]  # rows n-1..n -> its ghost rows -1..0
             self.dn.flush()
 
+    def _wait(self):
+        if self.jitter:  # random per-rank delays: perturb the interleaving of ranks
+            time.sleep(self.rng.uniform(0, self.jitter))
+
+    def sweep_x(self, step):
+        self._wait()
+        super().sweep_x(step)
+
     def inbox_in(self, step):
+        self._wait()
         par, n = step & 1, self.geo.nx
         if not self.geo.wall_lo:
             self.g.u[:, 0:2, :] = self.inbox[par, 0]
@@ -124,6 +136,7 @@ class PeerOracleSlab(OracleSlab):
 
     def sweep_y(self, step):
         super().sweep_y(step)
+        self._wait()
         if self.p2p:
             self.halo_out(step + 1)
 
@@ -140,9 +153,10 @@ def _worker(rank, world, port, case, bc, outdir, mode="nccl"):
         sl = OracleSlab(geo, planes, full.dx, full.dy, bc)
     else:
         sl = PeerOracleSlab(geo, planes, full.dx, full.dy, bc, outdir,
-                            fail_handle=(mode == "p2p_fail" and rank == 1))
+                            fail_handle=(mode == "p2p_fail" and rank == 1),
+                            jitter=0.01 if mode == "p2p_jitter" else 0.0)
         used = comm.setup_p2p(sl)
-        assert used == (mode == "p2p")  # every rank agrees on the transport
+        assert used == (mode != "p2p_fail")  # every rank agrees on the transport
     S.run_slab(sl, comm, STEPS)
     np.save(os.path.join(outdir, f"slab{rank}.npy"), sl.g.u)
     dist.destroy_process_group()
@@ -166,7 +180,7 @@ def test_slab_driver_over_gloo_matches_single_domain(world, case, bc):
     assert np.array_equal(got[:, 2:NX + 2, 2:NY + 2], ref.u[:, 2:NX + 2, 2:NY + 2])
 
 
-@pytest.mark.parametrize("mode", ["p2p", "p2p_fail"])
+@pytest.mark.parametrize("mode", ["p2p", "p2p_fail", "p2p_jitter"])
 @pytest.mark.parametrize("world,case,bc", [(2, "random", "transmit"), (3, "corner_blast", "reflect")])
 def test_peer_memory_halo_schedule_over_gloo(world, case, bc, mode):
     """The peer-memory halo protocol (row sweep writes the neighbours' inbox
