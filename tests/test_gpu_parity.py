@@ -275,3 +275,22 @@ def test_exact_redo_path_is_bitwise(gpu, scale, bc):
     assert msg_gpu == msg_ref
     if msg_ref is None:
         assert np.array_equal(grid.planes, ref.u)
+
+
+@pytest.mark.parametrize("case,seed", [("random", 13465), ("sod_x", 0), ("corner_blast", 0), ("blast", 0)])
+def test_slab_device_initialiser_matches_full_grid(gpu, case, seed):
+    """hydro_gpu_init_case on a row slab (bench.py --gpus N) builds the slab's
+    rows of the global case: global row indices, global Sod position, global
+    random-field cell numbering."""
+    from paper_2106_13465_b200 import slab as S
+    nx, ny, world = 61, 37, 3
+    full = P.make_case(case, nx, ny, MODEL, seed=seed)
+    for r in range(world):
+        geo = S.SlabGeometry(nx, ny, r, world)
+        sl = S.GpuSlab(geo, full.dx, full.dy, MODEL, "reflect", 0)
+        sl.grid.init_case(case, seed)
+        got = np.zeros((4, geo.nx + 4, ny + 4))
+        sl.grid.download(got)
+        want = S.slab_planes(full.planes, nx, world, r)
+        assert np.array_equal(got[:, 2:geo.nx + 2, 2:ny + 2], want[:, 2:geo.nx + 2, 2:ny + 2]), r
+        sl.grid.close()
