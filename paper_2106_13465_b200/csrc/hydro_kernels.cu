@@ -1135,7 +1135,9 @@ void launch_sweep_y(const SweepArgs& a0, const TmaMaps& maps, const Geometry& ge
 }
 
 void launch_prologue(const PrologueArgs& a, cudaStream_t s) {
-  dim3 grid((a.ny + 255) / 256, a.nx < 4096 ? a.nx : 4096);
+  // each thread walks ~nx/128 rows of its column: few enough warps that the
+  // per-warp atomicMin of the dt limit does not serialise on one address
+  dim3 grid((a.ny + 255) / 256, a.nx < 128 ? a.nx : 128);
   prologue_kernel<<<grid, 256, 0, s>>>(a);
 }
 
