@@ -217,9 +217,6 @@ __device__ __forceinline__ int claim(unsigned* counter) {
 #ifndef HB_X_MINB
 #define HB_X_MINB 4
 #endif
-#ifndef HB_X_TMA
-#define HB_X_TMA 1
-#endif
 #ifndef HB_Y_MINB
 #define HB_Y_MINB 4
 #endif
@@ -227,109 +224,7 @@ __device__ __forceinline__ int claim(unsigned* counter) {
 #define HB_EX_MINB 3
 #endif
 
-#if !HB_X_TMA  // the register-prefetch column sweep (A/B reference)
-// ---------------------------------------------------------------------------
-// Column sweep: lane = column j, item = 32 columns x a segment of rows.
 
-struct ColumnSource {
-  const double* __restrict__ p;  // next row to fetch (cell k = row k-1)
-  size_t pitch;
-  Cons next;
-  __device__ __forceinline__ Cons fetch() {
-    const Cons u = {__ldg(p), __ldg(p + pitch), __ldg(p + 2 * pitch), __ldg(p + 3 * pitch)};
-    p += 4 * pitch;
-    return u;
-  }
-  __device__ __forceinline__ void start() { next = fetch(); }
-  // Cells arrive strictly in order; the following cell is already in flight.
-  __device__ __forceinline__ Cons load(int) {
-    const Cons u = next;
-    next = fetch();
-    return u;
-  }
-  // Cell c-1 during iteration c (after load(c+1) the cursor is at c+3).
-  __device__ __forceinline__ Cons reload(int) const {
-    const double* q = p - 16 * pitch;
-    return {__ldg(q), __ldg(q + pitch), __ldg(q + 2 * pitch), __ldg(q + 3 * pitch)};
-  }
-  __device__ __forceinline__ void boundary(int) {}
-};
-
-// The exact-10 flux needs far more live state than HLLC: it gets the
-// register file of 2 CTAs/SM instead of a spilling 128-register cap.
-template <int FLUX>
-__global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : HB_EX_MINB) sweep_x_kernel(SweepArgs a) {
-  if (latched(a)) return;
-  const int lane = threadIdx.x & 31;
-  if (*(volatile unsigned long long*)a.dt_err != kNoError) {
-    // compute_dt of this step failed (detected by the previous row sweep).
-    if (blockIdx.x == 0 && threadIdx.x == 0) record(a.err, *(volatile unsigned long long*)a.dt_err);
-    return;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (a.limit_out) *a.limit_out = kEmptyLimit;
-    *a.counter_next = 0u;
-  }
-  const Gas g = make_gas(a.gamma);
-  const double dtdx = step_dt(a) / a.dx;
-  const size_t pitch = a.pitch;
-  const int ny = a.ny;
-  const bool refl = a.bc == 0;
-  const int groups = (ny + 31) >> 5;
-  const int items = groups * a.nseg;
-  double* __restrict__ dst = a.dst;
-  for (int item = claim(a.counter); item < items; item = claim(a.counter)) {
-    const int grp = item % groups, sg = item / groups;
-    const int jt = (grp << 5) + lane + 1;
-    const bool active = jt <= ny;
-    const int j = active ? jt : ny;  // idle lanes shadow the last column, writes masked
-    const int i_lo = 1 + sg * a.seg;
-    const int i_hi = min(a.nx, i_lo + a.seg - 1);
-    // warps holding a y-wall column (1, 2, ny-1 or ny; the last two may sit in
-    // different groups)
-    const bool edge = grp == 0 || (grp << 5) + 32 >= ny - 1;
-    const unsigned long long base = error_key(a.step, 1, j, 0, 0, 0);
-    // One pass over the item with math policy M; returns (in range, error key).
-    auto pass = [&](auto math) {
-      using M = decltype(math);
-      // the prefetch reads one row past the stencil (row nx+3 at most: a
-      // padding row of the allocation)
-      ColumnSource src{a.src + cell_index(pitch, 0, i_lo - 2, j), pitch, {}};
-      src.start();
-      double* out = dst + cell_index(pitch, 0, i_lo, j);
-      auto put = [&](double* q, const Cons& u, bool neg) {
-        q[0] = u.r;
-        q[pitch] = u.ma;
-        q[2 * pitch] = neg ? -u.mb : u.mb;
-        q[3 * pitch] = u.e;
-      };
-      auto sink = [&](int, const StepOut& o) {
-        if (active) put(out, o.un, false);
-        if (edge && active) {  // y-wall ghosts of the column-sweep output (grid.cpp:44-59)
-          if (refl) {
-            if (j <= 2) put(out + (1 - 2 * j), o.un, true);
-            if (j >= ny - 1) put(out + (2 * ny + 1 - 2 * j), o.un, true);
-          } else {
-            if (j == 1) { put(out - 1, o.un, false); put(out - 2, o.un, false); }
-            if (j == ny) { put(out + 1, o.un, false); put(out + 2, o.un, false); }
-          }
-        }
-        out += 4 * pitch;
-      };
-      unsigned long long ek = kNoError;
-      const bool ok = walk_strip<M, false, FLUX>(i_lo + 1, i_hi + 1, src, sink, g, dtdx, 0.0,
-                                                 base, a.row0, ek);
-      return make_pair_ok(ok, ek);
-    };
-    OkKey r = pass(FastMath{});
-    // a fast path left its proven range somewhere: the warp redoes the item
-    // with the compiler's IEEE division/sqrt (overwriting every output)
-    if (!__all_sync(0xffffffffu, r.ok || !active)) r = pass(ExactMath{});
-    if (active && r.key != kNoError) record(a.err, r.key);
-  }
-}
-
-#endif  // !HB_X_TMA
 
 // ---------------------------------------------------------------------------
 // Row sweep with TMA-staged tiles, one independent pipeline per warp.
@@ -1037,15 +932,10 @@ int query_geometry(Geometry* g) {
   cudaFuncSetAttribute(sweep_y_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
   cudaFuncSetAttribute(sweep_y_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
   int ox = 0, oy = 0, ox1 = 0, oy1 = 0;
-#if HB_X_TMA
   cudaFuncSetAttribute(sweep_x_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
   cudaFuncSetAttribute(sweep_x_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, sweep_x_tma_kernel<0>, 128, kYSmemBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox1, sweep_x_tma_kernel<1>, 128, kYSmemBytes);
-#else
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, sweep_x_kernel<0>, 128, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox1, sweep_x_kernel<1>, 128, 0);
-#endif
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy, sweep_y_kernel<0, false>, 128, kYSmemBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy1, sweep_y_kernel<1, false>, 128, kYSmemBytes);
   g->ctas_x_per_sm = ox > 0 ? ox : 1;
@@ -1101,21 +991,12 @@ void launch_sweep_x(const SweepArgs& a0, const TmaMaps& maps, const Geometry& ge
   SweepArgs a = a0;
   const int ctas = geo.sms * (a.flux == 1 ? geo.ctas_x_exact : geo.ctas_x_per_sm);
   if (a.seg <= 0) a.seg = pick_seg(a.nx, a.ny, ctas * 4);
-#if HB_X_TMA
   a.seg = (a.seg + kChunk - 1) / kChunk * kChunk;  // chunks never straddle segments
-#endif
   a.nseg = (a.nx + a.seg - 1) / a.seg;
-#if HB_X_TMA
   if (a.flux == 1)
     sweep_x_tma_kernel<1><<<ctas, 128, kYSmemBytes, s>>>(a, maps.x_load, maps.x_store);
   else
     sweep_x_tma_kernel<0><<<ctas, 128, kYSmemBytes, s>>>(a, maps.x_load, maps.x_store);
-#else
-  if (a.flux == 1)
-    sweep_x_kernel<1><<<ctas, 128, 0, s>>>(a);
-  else
-    sweep_x_kernel<0><<<ctas, 128, 0, s>>>(a);
-#endif
 }
 
 void launch_sweep_y(const SweepArgs& a0, const TmaMaps& maps, const Geometry& geo,
