@@ -311,14 +311,14 @@ def check_execution_equivalence() -> list[CheckResult]:
     out.append(CheckResult("equivalence-stepwise", np.array_equal(grid.interior(), ref.interior()),
                            _first_diff(grid.interior(), ref.interior())))
     import torch
-    for world in (2, 4):
+    for world, p2p in ((2, False), (4, False), (4, True)):
         slabs = []
         for r in range(world):
             sl = S.GpuSlab(S.SlabGeometry(64, 64, r, world), base.dx, base.dy, model, "reflect", 0)
             sl.bind_stream(torch.cuda.current_stream())
             sl.grid.upload(S.slab_planes(base.planes, 64, world, r))
             slabs.append(sl)
-        S.run_loopback(slabs, steps)
+        S.run_loopback(slabs, steps, p2p=p2p)
         torch.cuda.synchronize()
         parts = []
         for sl in slabs:
@@ -326,8 +326,8 @@ def check_execution_equivalence() -> list[CheckResult]:
             sl.grid.download(p)
             parts.append(p)
         got = S.gather_planes(parts, 64, 64)
-        out.append(CheckResult(f"equivalence-slabs-{world}", np.array_equal(got, ref.planes),
-                               _first_diff(got, ref.planes)))
+        name = f"equivalence-slabs-{world}" + ("-peer-halo" if p2p else "")
+        out.append(CheckResult(name, np.array_equal(got, ref.planes), _first_diff(got, ref.planes)))
     return out
 
 
