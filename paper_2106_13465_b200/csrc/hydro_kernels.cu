@@ -100,7 +100,9 @@ __device__ __forceinline__ void step_cell(M& m, const Window& w, const Cons& uC,
   // left face first: it meets the previous right face in this iteration's
   // Riemann problem, after which that face is dead and the new right face
   // can take its registers
-  o.fl = face_prim(m, el, w.wB, g);
+  // (the first halo iteration's left face would only meet the interface
+  // before the segment's halo: it is not evaluated)
+  if (STAGE >= 1) o.fl = face_prim(m, el, w.wB, g);
   o.fR = -1;
   if (STAGE >= 1) o.F = riemann<FLUX>(m, w.frPrev, o.fl, g, o.fR);
   o.fr = face_prim(m, er, w.wB, g);
