@@ -920,6 +920,13 @@ int pick_seg(int n, int strips, int warps) {
   if (seg < 16) seg = 16;
   if (seg > 128) seg = 128;
   seg = (seg + kChunk - 1) / kChunk * kChunk;
+  // small grids: 16-cell segments leave warps without work, and a segment
+  // is a sequential walk, so trade halo recomputation for parallelism --
+  // segments down to one chunk, about one item per resident warp
+  if (groups * ((n + seg - 1) / seg) < warps) {
+    long long s2 = (long long)n * groups / (warps > 0 ? warps : 1) / kChunk * kChunk;
+    seg = s2 < kChunk ? kChunk : s2;
+  }
   return (int)seg;
 }
 
