@@ -358,7 +358,7 @@ def main():
         if per_cell:
             traffic = per_cell * geo.nx * NY
 
-    # the bound that actually binds (DESIGN.md 3.6): FP64-pipe lane
+    # the bound that actually binds (DESIGN.md 3.5): FP64-pipe lane
     # instructions of that kernel per cell (ncu, config 1 / hllc only) over
     # 148 SMs x 64 FP64 lanes x the SM clock sampled during the timed region
     fp64 = None
@@ -436,7 +436,7 @@ def main():
             "e2e": {"value": cells * TSTEPS * vsteps / ve2e, "unit": UNIT,
                     "h2d_bytes_per_step": plane_bytes, "d2h_bytes_per_step": plane_bytes},
             "note": "BASELINE's stated solver: exact Riemann flux, 10 Newton iterations "
-                    "(DESIGN.md 3.5); bitwise equal to the oracle's restatement",
+                    "(DESIGN.md 3.4); bitwise equal to the oracle's restatement",
             "result_digest": f"{vdigest:016x}" if vdigest is not None else None}}
         vgrid.close()
 
