@@ -183,7 +183,8 @@ def run_reference_arm(args, rank, world):
         "data": "synthetic (analytic or seeded initial condition, no dataset)",
         "config": {"workload": f"BASELINE {args.workload} sample: {NX}x{NY} {CASE} {BC}, "
                                f"{sample_steps} time steps per bench step",
-                   "global_batch": NX * NY, "parallelism": f"cpu {strat} x{used}"},
+                   "cells": NX * NY, "time_steps_per_bench_step": sample_steps,
+                   "parallelism": f"cpu {strat} x{used}"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": kind,
                          "sample": f"{sample_steps} time steps of the {NX}x{NY} {args.workload} grid, "
                                    f"reference {strat} (its fastest strategy here, "
@@ -448,7 +449,7 @@ def main():
             "data": "synthetic (analytic or seeded initial condition, no dataset)",
             "config": {"workload": f"BASELINE {args.workload}: {global_nx}x{NY} {CASE} {BC}, "
                                    f"{args.flux}, {TSTEPS} time steps per bench step",
-                       "global_batch": cells, "seq_len": TSTEPS,
+                       "cells": cells, "time_steps_per_bench_step": TSTEPS,
                        "parallelism": f"row slabs x{world}" if world > 1 else "single GPU",
                        "halo": (("peer-memory (row-sweep stores into neighbour inboxes)"
                                  if comm.p2p else "nccl send/recv") if world > 1 else None),
