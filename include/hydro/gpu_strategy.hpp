@@ -38,6 +38,7 @@ namespace hydro {
 struct GpuOptions {
   int device = -1;                    // CUDA device; -1 = current
   int bc = HYDRO_GPU_BC_REFLECT;      // the reference's walls; TRANSMIT for BASELINE configs
+  int flux = HYDRO_GPU_FLUX_HLLC;     // the reference hot path; EXACT10 = BASELINE's solver
 };
 
 namespace gpu_detail {
@@ -63,7 +64,7 @@ class Context {
     cfg.gamma = m.gamma;
     cfg.cfl = m.cfl;
     cfg.bc = o.bc;
-    cfg.flux = HYDRO_GPU_FLUX_HLLC;
+    cfg.flux = o.flux;
     cfg.device = o.device;
     cfg.row0 = 0;
     cfg.global_nx = g.nx();

@@ -10,6 +10,7 @@
 //   hydrobench_gpu run --case blast --nx 48 --ny 48 --steps 5 --strategy gpu
 //   hydrobench_gpu bench --case blast --nx 2048 --ny 2048 --steps 10 --strategy gpu
 //   extra: --case corner_blast|sod_x|random (BASELINE configs), --bc reflect|transmit,
+//          --flux hllc|exact10 (gpu strategy),
 //          --seed N (random field), --device N
 #include <chrono>
 #include <cstdio>
@@ -30,6 +31,7 @@ struct Args {
   hydro::RunConfig config;
   std::string command;
   std::string bc = "reflect";
+  std::string flux = "hllc";
   int device = -1;
 };
 
@@ -53,6 +55,7 @@ Args parse(int argc, char** argv) {
     else if (key == "--seed") c.seed = std::stoull(val);
     else if (key == "--output") c.output = val;
     else if (key == "--bc") a.bc = val;
+    else if (key == "--flux") a.flux = val;
     else if (key == "--device") a.device = std::stoi(val);
     else throw hydro::ConfigError("unknown option " + key);
   }
@@ -86,10 +89,15 @@ void step(hydro::Grid2D& grid, const Args& a, int steps) {
     hydro::GpuOptions opt;
     opt.device = a.device;
     opt.bc = a.bc == "transmit" ? HYDRO_GPU_BC_TRANSMIT : HYDRO_GPU_BC_REFLECT;
+    if (a.flux != "hllc" && a.flux != "exact10")
+      throw hydro::ConfigError("unknown flux '" + a.flux + "'");
+    opt.flux = a.flux == "exact10" ? HYDRO_GPU_FLUX_EXACT10 : HYDRO_GPU_FLUX_HLLC;
     hydro::run_gpu(grid, hydro::GasModel{c.gamma, c.cfl}, steps, opt);
   } else {
     if (a.bc != "reflect")
       throw hydro::ConfigError("the CPU strategies only have reflective walls");
+    if (a.flux != "hllc")
+      throw hydro::ConfigError("the CPU strategies only have the HLLC flux");
     hydro::run_strategy(grid, c, c.workers[0]);
   }
 }

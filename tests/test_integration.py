@@ -65,3 +65,30 @@ def test_gpu_positivity_error_line_matches_reference():
     assert cpu.returncode == gpu.returncode == 1
     assert cpu.stderr == gpu.stderr
     assert cpu.stderr.startswith("error: positivity: step ")
+
+
+@needs_bin
+def test_cpu_strategies_reject_the_gpu_only_flux():
+    out = run("run", "--case", "blast", "--nx", "32", "--ny", "32", "--steps", "1",
+              "--strategy", "sequential", "--flux", "exact10")
+    assert out.returncode == 1
+    assert out.stderr.startswith("error: config: the CPU strategies only have the HLLC flux")
+
+
+@needs_bin
+@pytest.mark.gpu
+def test_gpu_strategy_exact10_flux_equals_oracle():
+    """--flux exact10 through the C++ adaptor (GpuOptions::flux): the checksum
+    digest equals the oracle's exact-10 run of the same case."""
+    import numpy as np
+
+    from oracle import oracle as O
+    out = run("run", "--case", "sod_x", "--nx", "64", "--ny", "40", "--steps", "12",
+              "--bc", "transmit", "--strategy", "gpu", "--flux", "exact10")
+    assert out.returncode == 0, out.stderr
+    digest = out.stdout.splitlines()[1].split()[1]
+    ref = O.make_case("sod_x", 64, 40)
+    with O.flux_mode("exact10"):
+        O.run_sequential(ref, 12, "transmit")
+    assert digest == f"{O.digest(ref):016x}"
+    assert np.isfinite(ref.u).all()
