@@ -5,6 +5,7 @@ oracle/_ref/libhydro_ref.so by ``make -C oracle``):
 
     python tests/golden/make_golden.py            # golden.json (seconds)
     python tests/golden/make_golden.py --full     # golden_full.json (minutes)
+    python tests/golden/make_golden.py --full --only cfg1_sod_x_2048_200_exact10  # ~15 min
 
 Every digest here is produced by the reference's own run_sequential /
 run_coarse_grain (bitwise equal to each other, acceptance_tests.cpp:48-113)
@@ -70,6 +71,31 @@ FULL = [
 ]
 
 
+# The exact-10 flux is not on the reference's hot path: its full-size digest
+# comes from the oracle's C restatement (oracle/hydro_oracle.c, exact10),
+# which tests/test_exact_flux.py pins within 1e-12 of the reference's own
+# exact solver (proj/src/exact_riemann.cpp).
+FULL_EXACT10 = [
+    ("cfg1_sod_x_2048_200_exact10", "sod_x", 2048, 2048, "transmit", 200, 0,
+     "BASELINE config 1 with its stated exact Riemann solver (10 Newton iterations), full"),
+]
+
+
+def run_oracle_exact10(entry):
+    name, case, nx, ny, bc, steps, seed, prov = entry
+    g = O.make_case(case, nx, ny, seed=seed)
+    t0 = time.time()
+    with O.flux_mode("exact10"):
+        O.run_sequential(g, steps, bc)
+    secs = time.time() - t0
+    rec = {"case": case, "nx": g.nx, "ny": g.ny, "bc": bc, "steps": steps, "seed": seed,
+           "flux": "exact10", "digest": f"{O.digest(g):016x}", "provenance": prov,
+           "generator": "oracle (C restatement, oracle_set_flux exact10), single thread",
+           "ref_seconds": round(secs, 1)}
+    print(f"{name}: {rec['digest']} ({secs:.1f}s)", flush=True)
+    return name, rec
+
+
 def run_case(entry, strategy, workers):
     name, case, nx, ny, bc, steps, seed, prov = entry
     g = O.make_case(case, nx, ny, seed=seed)
@@ -105,6 +131,13 @@ def main():
             name, rec = run_case(entry, "sequential", 1)
         result[name] = rec
         json.dump(result, open(out_path, "w"), indent=1, sort_keys=True)
+    if args.full:
+        for entry in FULL_EXACT10:
+            if args.only and entry[0] != args.only:
+                continue
+            name, rec = run_oracle_exact10(entry)
+            result[name] = rec
+            json.dump(result, open(out_path, "w"), indent=1, sort_keys=True)
 
 
 if __name__ == "__main__":
