@@ -340,6 +340,46 @@ def main():
     e2e_value = cells * TSTEPS * args.steps / e2e_s
     plane_bytes = 4 * (geo.nx + 4) * (NY + 4) * 8
 
+    # ---- the same end-to-end work pipelined over two contexts -------------
+    # Independent problems through the asynchronous C-ABI
+    # (hydro_gpu_upload_async / run_async / download_async): each bench step
+    # still uploads its inputs from pinned memory, runs and downloads its
+    # result, but on alternating contexts and streams, so the copies of one
+    # overlap the other's kernels.
+    e2e_pipe = None
+    if world == 1:
+        streams = [stream, torch.cuda.Stream()]
+        grids = [grid, P.GpuGrid(NX, NY, dx, dy, model, BC, device=local, flux=args.flux)]
+        grids[1].set_stream(streams[1].cuda_stream)
+        outs = [host, torch.zeros_like(host0).pin_memory()]
+        optrs = [[o[v].data_ptr() for v in range(4)] for o in outs]
+
+        def pipe_step(k):
+            g2, st = grids[k & 1], streams[k & 1]
+            g2.upload_ptr_async(ptrs0, NY + 4)
+            g2.run_async(TSTEPS)
+            g2.download_ptr_async(optrs[k & 1], NY + 4)
+
+        for k in range(2):
+            pipe_step(k)
+        for g2 in grids:
+            g2.sync()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            pipe_step(k)
+        for g2 in grids:
+            g2.sync()
+        torch.cuda.synchronize()
+        pipe_s = time.perf_counter() - t0
+        last = outs[(args.steps - 1) & 1].numpy()
+        e2e_pipe = {"value": cells * TSTEPS * args.steps / pipe_s, "unit": UNIT,
+                    "h2d_bytes_per_step": plane_bytes, "d2h_bytes_per_step": plane_bytes,
+                    "result_digest": f"{P.grid_digest(P.Grid2D(NX, NY, dx, dy, last)):016x}",
+                    "note": "two contexts, alternating streams: hydro_gpu_upload_async / "
+                            "run_async / download_async per step"}
+        grids[1].close()
+
     # result check of the e2e leg against the digest of the first run
     digest = P.grid_digest(P.Grid2D(geo.nx, NY, dx, dy, host.numpy())) if world == 1 else None
 
@@ -463,6 +503,7 @@ def main():
                          "fp64_pipe": fp64},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": plane_bytes,
                     "d2h_bytes_per_step": plane_bytes},
+            "e2e_pipelined": e2e_pipe,
             "gpu_launches": launches,
             "kernel_ms": {"sweep_x": kt["ms_x"], "sweep_y": kt["ms_y"], "other": kt["ms_other"],
                           "note": "event-instrumented pass of the same K bench steps"},

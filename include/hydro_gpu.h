@@ -118,6 +118,14 @@ int hydro_gpu_upload(hydro_gpu_ctx* ctx, const double* const planes[4],
                      size_t row_stride);
 int hydro_gpu_download(hydro_gpu_ctx* ctx, double* const planes[4],
                        size_t row_stride);
+/* The same transfers enqueued on the context's stream without waiting (see
+ * hydro_gpu_set_stream): with pinned host planes they overlap kernels of
+ * other streams, so independent problems on two contexts pipeline copies
+ * with compute.  The host planes must stay valid until hydro_gpu_sync. */
+int hydro_gpu_upload_async(hydro_gpu_ctx* ctx, const double* const planes[4],
+                           size_t row_stride);
+int hydro_gpu_download_async(hydro_gpu_ctx* ctx, double* const planes[4],
+                             size_t row_stride);
 /* Device-side initialiser, bitwise equal to hydro_init_case_host. */
 int hydro_gpu_init_case(hydro_gpu_ctx* ctx, int case_id, uint64_t seed);
 

@@ -61,6 +61,8 @@ def lib() -> C.CDLL:
         "hydro_gpu_last_error": ([_ctx, P(ErrorInfo)], i),
         "hydro_gpu_upload": ([_ctx, _planes, sz], i),
         "hydro_gpu_download": ([_ctx, _planes, sz], i),
+        "hydro_gpu_upload_async": ([_ctx, _planes, sz], i),
+        "hydro_gpu_download_async": ([_ctx, _planes, sz], i),
         "hydro_gpu_init_case": ([_ctx, i, u64], i),
         "hydro_gpu_run": ([_ctx, i, _dp], i),
         "hydro_gpu_advance": ([_ctx, d], i),

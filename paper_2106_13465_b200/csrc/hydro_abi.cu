@@ -538,7 +538,7 @@ int hydro_gpu_set_stream(hydro_gpu_ctx* ctx, void* s) {
   return HYDRO_GPU_OK;
 }
 
-int hydro_gpu_upload(hydro_gpu_ctx* c, const double* const planes[4], size_t row_stride) {
+int hydro_gpu_upload_async(hydro_gpu_ctx* c, const double* const planes[4], size_t row_stride) {
   if (!c || !planes) return HYDRO_GPU_ERR_CONFIG;
   if (row_stride < (size_t)c->cfg.ny + 4)
     return set_err(c, HYDRO_GPU_ERR_CONFIG, "row stride %zu below ny+4", row_stride);
@@ -549,11 +549,18 @@ int hydro_gpu_upload(hydro_gpu_ctx* c, const double* const planes[4], size_t row
                                   planes[v], row_stride * 8, (size_t)(c->cfg.ny + 4) * 8,
                                   (size_t)(c->cfg.nx + 4), cudaMemcpyHostToDevice, c->stream));
   }
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_upload(hydro_gpu_ctx* c, const double* const planes[4], size_t row_stride) {
+  const int rc = hydro_gpu_upload_async(c, planes, row_stride);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return HYDRO_GPU_OK;
 }
 
-int hydro_gpu_download(hydro_gpu_ctx* c, double* const planes[4], size_t row_stride) {
+int hydro_gpu_download_async(hydro_gpu_ctx* c, double* const planes[4], size_t row_stride) {
   if (!c || !planes) return HYDRO_GPU_ERR_CONFIG;
   if (row_stride < (size_t)c->cfg.ny + 4)
     return set_err(c, HYDRO_GPU_ERR_CONFIG, "row stride %zu below ny+4", row_stride);
@@ -565,6 +572,13 @@ int hydro_gpu_download(hydro_gpu_ctx* c, double* const planes[4], size_t row_str
                                   (size_t)(c->cfg.ny + 4) * 8, (size_t)(c->cfg.nx + 4),
                                   cudaMemcpyDeviceToHost, c->stream));
   }
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_download(hydro_gpu_ctx* c, double* const planes[4], size_t row_stride) {
+  const int rc = hydro_gpu_download_async(c, planes, row_stride);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return HYDRO_GPU_OK;
 }

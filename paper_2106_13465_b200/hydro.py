@@ -240,6 +240,16 @@ class GpuGrid:
         arr = L._planes(*[C.cast(C.c_void_p(p), L._dp) for p in plane_ptrs])
         self._check(self._lib.hydro_gpu_download(self._ctx, arr, row_stride))
 
+    def upload_ptr_async(self, plane_ptrs, row_stride: int):
+        """hydro_gpu_upload_async: enqueued on the context's stream (pinned
+        host planes that stay alive until sync)."""
+        arr = L._planes(*[C.cast(C.c_void_p(p), L._dp) for p in plane_ptrs])
+        self._check(self._lib.hydro_gpu_upload_async(self._ctx, arr, row_stride))
+
+    def download_ptr_async(self, plane_ptrs, row_stride: int):
+        arr = L._planes(*[C.cast(C.c_void_p(p), L._dp) for p in plane_ptrs])
+        self._check(self._lib.hydro_gpu_download_async(self._ctx, arr, row_stride))
+
     def init_case(self, case: str, seed: int = 0):
         self._check(self._lib.hydro_gpu_init_case(self._ctx, CASES[case], seed))
 
