@@ -194,6 +194,22 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
   return m.ok;
 }
 
+// Programmatic dependent launch (the sweeps are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a sweep lets the next
+// one be scheduled at once -- its CTAs occupy SM slots as this grid's retire
+// and do their local setup -- and each sweep waits for its predecessor's
+// completion before touching any global state.
+__device__ __forceinline__ void pdl_wait() {
+#if HB_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_launch_dependents() {
+#if HB_PDL
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+#endif
+}
+
 __device__ __forceinline__ bool latched(const SweepArgs& a) {
   return *(volatile unsigned long long*)a.err != kNoError;
 }
@@ -216,6 +232,9 @@ __device__ __forceinline__ int claim(unsigned* counter) {
   return __shfl_sync(0xffffffffu, item, 0);
 }
 
+#ifndef HB_PDL
+#define HB_PDL 1
+#endif
 #ifndef HB_X_MINB
 #define HB_X_MINB 4
 #endif
@@ -490,6 +509,11 @@ template <int FLUX>
 __global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : HB_EX_MINB)
     sweep_x_tma_kernel(SweepArgs a, const __grid_constant__ CUtensorMap load_map,
                        const __grid_constant__ CUtensorMap store_map) {
+  pdl_launch_dependents();
+  Tiles<0> t = make_tiles<0>(&load_map, &store_map);
+  const int lane = t.lane;
+  const Gas g = make_gas(a.gamma);
+  pdl_wait();
   if (latched(a)) return;
   if (*(volatile unsigned long long*)a.dt_err != kNoError) {
     // compute_dt of this step failed (detected by the previous row sweep).
@@ -500,9 +524,6 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : HB_EX_MINB)
     if (a.limit_out) *a.limit_out = kEmptyLimit;
     *a.counter_next = 0u;
   }
-  Tiles<0> t = make_tiles<0>(&load_map, &store_map);
-  const int lane = t.lane;
-  const Gas g = make_gas(a.gamma);
   const double dtdx = step_dt(a) / a.dx;
   const size_t pitch = a.pitch;
   const int ny = a.ny;
@@ -579,11 +600,13 @@ template <int FLUX, bool PEER>
 __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : HB_EX_MINB) sweep_y_kernel(SweepArgs a,
                                                        const __grid_constant__ CUtensorMap load_map,
                                                        const __grid_constant__ CUtensorMap store_map) {
-  if (latched(a)) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *a.counter_next = 0u;
+  pdl_launch_dependents();
   Tiles<1> t = make_tiles<1>(&load_map, &store_map);
   const int lane = t.lane;
   const Gas g = make_gas(a.gamma);
+  pdl_wait();
+  if (latched(a)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.counter_next = 0u;
   const double dtdx = step_dt(a) / a.dx;
   const size_t pitch = a.pitch;
   const int nx = a.nx;
@@ -995,6 +1018,21 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
          enc(&maps->x_load, A, dim_load, box_x, sx) && enc(&maps->x_store, B, dim_xstore, box_x, sx);
 }
 
+template <class... KArgs, class... Args>
+void launch_sweep(void (*kernel)(KArgs...), int ctas, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = kYSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = HB_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 void launch_sweep_x(const SweepArgs& a0, const TmaMaps& maps, const Geometry& geo,
                     cudaStream_t s) {
   SweepArgs a = a0;
@@ -1003,9 +1041,9 @@ void launch_sweep_x(const SweepArgs& a0, const TmaMaps& maps, const Geometry& ge
   a.seg = (a.seg + kChunk - 1) / kChunk * kChunk;  // chunks never straddle segments
   a.nseg = (a.nx + a.seg - 1) / a.seg;
   if (a.flux == 1)
-    sweep_x_tma_kernel<1><<<ctas, 128, kYSmemBytes, s>>>(a, maps.x_load, maps.x_store);
+    launch_sweep(sweep_x_tma_kernel<1>, ctas, s, a, maps.x_load, maps.x_store);
   else
-    sweep_x_tma_kernel<0><<<ctas, 128, kYSmemBytes, s>>>(a, maps.x_load, maps.x_store);
+    launch_sweep(sweep_x_tma_kernel<0>, ctas, s, a, maps.x_load, maps.x_store);
 }
 
 void launch_sweep_y(const SweepArgs& a0, const TmaMaps& maps, const Geometry& geo,
@@ -1016,12 +1054,13 @@ void launch_sweep_y(const SweepArgs& a0, const TmaMaps& maps, const Geometry& ge
   a.seg = (a.seg + kChunk - 1) / kChunk * kChunk;  // chunks never straddle segments
   a.nseg = (a.ny + a.seg - 1) / a.seg;
   const bool peer = a.halo_up || a.halo_dn;
-  if (a.flux == 1)
-    peer ? sweep_y_kernel<1, true><<<ctas, 128, kYSmemBytes, s>>>(a, maps.y_load, maps.y_store)
-         : sweep_y_kernel<1, false><<<ctas, 128, kYSmemBytes, s>>>(a, maps.y_load, maps.y_store);
-  else
-    peer ? sweep_y_kernel<0, true><<<ctas, 128, kYSmemBytes, s>>>(a, maps.y_load, maps.y_store)
-         : sweep_y_kernel<0, false><<<ctas, 128, kYSmemBytes, s>>>(a, maps.y_load, maps.y_store);
+  if (a.flux == 1) {
+    if (peer) launch_sweep(sweep_y_kernel<1, true>, ctas, s, a, maps.y_load, maps.y_store);
+    else launch_sweep(sweep_y_kernel<1, false>, ctas, s, a, maps.y_load, maps.y_store);
+  } else {
+    if (peer) launch_sweep(sweep_y_kernel<0, true>, ctas, s, a, maps.y_load, maps.y_store);
+    else launch_sweep(sweep_y_kernel<0, false>, ctas, s, a, maps.y_load, maps.y_store);
+  }
 }
 
 void launch_prologue(const PrologueArgs& a, cudaStream_t s) {
