@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <type_traits>
+
 #include "hydro_exact.cuh"
 #include "hydro_kernels.cuh"
 
@@ -74,14 +76,56 @@ struct StepOut {
 // STAGE 2: + conservative update (+ dt limit).
 // FLUX 0: HLLC (euler_kernel.cpp:59-109); FLUX 1: exact Riemann, 10 Newton
 // iterations (hydro_exact.cuh).
-template <int FLUX, class M>
-__device__ __forceinline__ Flux riemann(M& m, const Face& L, const Face& R, const Gas& g, int& fail) {
+extern __shared__ __align__(128) uint8_t hb_smem[];
+
+// Exact-10 interface memo (per thread, in shared memory after the tiles):
+// the last Riemann problem this walk solved -- both face states bit for bit
+// -- and its flux.  The solver is a pure function of the two states, so an
+// interface whose states repeat the previous one's (uniform flow, where the
+// exact solver is as expensive as anywhere) takes the stored flux: the same
+// bits without the Newton/log/exp work.  Reset at every walk (pass), so a
+// hit never skips a range test the pass has not already folded in.
+struct Memo {
+  uint32_t at;  // hb_smem offset of this thread's field 0 (fields 1 KB apart)
+  bool valid;
+  __device__ __forceinline__ double& f(int k) const {
+    return *(double*)(hb_smem + at + k * 1024);
+  }
+  __device__ __forceinline__ static bool same(double a, double b) {
+    return __double_as_longlong(a) == __double_as_longlong(b);
+  }
+  __device__ __forceinline__ bool match(const Prim& a, const Prim& b) const {
+    return valid & same(f(0), a.r) & same(f(1), a.va) & same(f(2), a.vb) & same(f(3), a.p) &
+           same(f(4), b.r) & same(f(5), b.va) & same(f(6), b.vb) & same(f(7), b.p);
+  }
+  __device__ __forceinline__ void put(const Prim& a, const Prim& b, const Flux& F, bool vac) {
+    f(0) = a.r; f(1) = a.va; f(2) = a.vb; f(3) = a.p;
+    f(4) = b.r; f(5) = b.va; f(6) = b.vb; f(7) = b.p;
+    f(8) = F.m; f(9) = F.ma; f(10) = F.mb; f(11) = F.e;
+    f(12) = vac ? 1.0 : 0.0;
+    valid = true;
+  }
+};
+struct NoMemo {
+  bool valid;
+};
+
+template <int FLUX, class M, class Mem>
+__device__ __forceinline__ Flux riemann(M& m, const Face& L, const Face& R, const Gas& g, int& fail,
+                                        Mem& memo) {
   fail = -1;
   if constexpr (FLUX == 0) {
     return hllc(m, L, R, g);
   } else {
     bool vacuum;
-    const Flux f = exact10_flux(m, L, R, g, vacuum);
+    Flux f;
+    if (memo.match(L.w, R.w)) {
+      f = {memo.f(8), memo.f(9), memo.f(10), memo.f(11)};
+      vacuum = memo.f(12) != 0.0;
+    } else {
+      f = exact10_flux(m, L, R, g, vacuum);
+      memo.put(L.w, R.w, f, vacuum);
+    }
     if (vacuum) {
       if constexpr (M::kFast) m.fallback();  // reported by the exact pass
       else fail = 3;
@@ -90,10 +134,10 @@ __device__ __forceinline__ Flux riemann(M& m, const Face& L, const Face& R, cons
   }
 }
 
-template <int STAGE, bool WANT_DT, int FLUX, class M, class Old>
+template <int STAGE, bool WANT_DT, int FLUX, class M, class Old, class Mem>
 __device__ __forceinline__ void step_cell(M& m, const Window& w, const Cons& uC, double half,
                                           double dtdx, double spacing, const Gas& g,
-                                          const Old& old, StepOut& o) {
+                                          const Old& old, StepOut& o, Mem& memo) {
   o.fC = to_prim(m, uC, g, o.wC);
   Cons el, er;
   predict_evolved(m, w.wA, w.wB, o.wC, half, g, el, er);
@@ -104,7 +148,7 @@ __device__ __forceinline__ void step_cell(M& m, const Window& w, const Cons& uC,
   // before the segment's halo: it is not evaluated)
   if (STAGE >= 1) o.fl = face_prim(m, el, w.wB, g);
   o.fR = -1;
-  if (STAGE >= 1) o.F = riemann<FLUX>(m, w.frPrev, o.fl, g, o.fR);
+  if (STAGE >= 1) o.F = riemann<FLUX>(m, w.frPrev, o.fl, g, o.fR, memo);
   o.fr = face_prim(m, er, w.wB, g);
   if (STAGE >= 2) {
     o.un = old();
@@ -144,6 +188,10 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
                                            unsigned long long& ekey) {
   M m;
   const double half = 0.5 * dtdx;
+  using Mem = std::conditional_t<FLUX == 1, Memo, NoMemo>;
+  Mem memo{};
+  if constexpr (FLUX == 1) memo.at = src.memo_at;
+  memo.valid = false;
   Window w;
   auto none = [] { return Cons{}; };
   int f = to_prim(m, src.load(ka - 2), g, w.wA);
@@ -153,7 +201,7 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
   {  // c = ka-1: faces of the first halo cell
     const Cons uC = src.load(ka);
     StepOut o;
-    step_cell<0, false, FLUX>(m, w, uC, half, dtdx, spacing, g, none, o);
+    step_cell<0, false, FLUX>(m, w, uC, half, dtdx, spacing, g, none, o, memo);
     if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka + kg) << 2) | o.fC);
     src.boundary(ka - 1);
     w.wA = w.wB;
@@ -163,7 +211,7 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
   {  // c = ka: faces of cell ka and the flux through its left interface
     const Cons uC = src.load(ka + 1);
     StepOut o;
-    step_cell<1, false, FLUX>(m, w, uC, half, dtdx, spacing, g, none, o);
+    step_cell<1, false, FLUX>(m, w, uC, half, dtdx, spacing, g, none, o, memo);
     if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka + 1 + kg) << 2) | o.fC);
     if (o.fR >= 0)
       keep_min(ekey, key_base | (1ull << 20) | ((unsigned long long)(ka - 1 + kg) << 2) | o.fR);
@@ -178,7 +226,7 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
     const Cons uC = src.load(c + 1);
     StepOut o;
     step_cell<2, WANT_DT, FLUX>(m, w, uC, half, dtdx, spacing, g,
-                                [&] { return src.reload(c - 1); }, o);
+                                [&] { return src.reload(c - 1); }, o, memo);
     if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(c + 1 + kg) << 2) | o.fC);
     if (o.fR >= 0)
       keep_min(ekey, key_base | (1ull << 20) | ((unsigned long long)(c - 1 + kg) << 2) | o.fR);
@@ -319,10 +367,9 @@ __device__ __forceinline__ void fence_async_smem() {
 // bookkeeping never resets.
 constexpr int kVarBytes = 32 * kChunk * 8;
 
-// The staged sweeps' dynamic shared memory.  Addressing it as hb_smem +
-// offset (rather than through generic pointers) lets the compiler emit
-// LDS/STS with 32-bit addresses.
-extern __shared__ __align__(128) uint8_t hb_smem[];
+// The staged sweeps' dynamic shared memory (hb_smem, declared above):
+// addressing it as hb_smem + offset (rather than through generic pointers)
+// lets the compiler emit LDS/STS with 32-bit addresses.
 
 template <int AXIS>
 struct Tiles {
@@ -338,6 +385,7 @@ struct Tiles {
   const CUtensorMap* store_map;
   uint32_t base;        // offset of this warp's kNBuf consecutive kChunkBytes buffers
   uint32_t full;        // offset of this warp's kNBuf mbarriers
+  uint32_t memo_at;     // this thread's exact-10 interface memo (Memo)
   int lane;
   int s0;               // first strip of the item: column j0 (AXIS 0) or row i0 (AXIS 1)
   int ka, kb;           // output strip cells
@@ -491,6 +539,7 @@ __device__ __forceinline__ Tiles<AXIS> make_tiles(const CUtensorMap* load_map,
   t.store_map = store_map;
   t.base = pad + warp * (kNBuf * kChunkBytes);
   t.full = pad + 4 * kNBuf * kChunkBytes + warp * kNBuf * 8;
+  t.memo_at = pad + 4 * kNBuf * kChunkBytes + 4 * kNBuf * 8 + threadIdx.x * 8;
   t.lane = lane;
   t.q0 = 0;
   // SWIZZLE_32B (row sweep): within each 256-byte atom the 16-byte half of a
@@ -960,16 +1009,16 @@ int query_geometry(Geometry* g) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncSetAttribute(sweep_y_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
-  cudaFuncSetAttribute(sweep_y_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
+  cudaFuncSetAttribute(sweep_y_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExSmemBytes);
   cudaFuncSetAttribute(sweep_y_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
-  cudaFuncSetAttribute(sweep_y_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
+  cudaFuncSetAttribute(sweep_y_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExSmemBytes);
   int ox = 0, oy = 0, ox1 = 0, oy1 = 0;
   cudaFuncSetAttribute(sweep_x_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
-  cudaFuncSetAttribute(sweep_x_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
+  cudaFuncSetAttribute(sweep_x_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExSmemBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, sweep_x_tma_kernel<0>, 128, kYSmemBytes);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox1, sweep_x_tma_kernel<1>, 128, kYSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox1, sweep_x_tma_kernel<1>, 128, kExSmemBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy, sweep_y_kernel<0, false>, 128, kYSmemBytes);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy1, sweep_y_kernel<1, false>, 128, kYSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy1, sweep_y_kernel<1, false>, 128, kExSmemBytes);
   g->ctas_x_per_sm = ox > 0 ? ox : 1;
   g->ctas_y_per_sm = oy > 0 ? oy : 1;
   g->ctas_x_exact = ox1 > 0 ? ox1 : 1;
@@ -1019,11 +1068,11 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
 }
 
 template <class... KArgs, class... Args>
-void launch_sweep(void (*kernel)(KArgs...), int ctas, cudaStream_t s, Args... args) {
+void launch_sweep(void (*kernel)(KArgs...), int ctas, int smem, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ctas);
   cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = kYSmemBytes;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1041,9 +1090,9 @@ void launch_sweep_x(const SweepArgs& a0, const TmaMaps& maps, const Geometry& ge
   a.seg = (a.seg + kChunk - 1) / kChunk * kChunk;  // chunks never straddle segments
   a.nseg = (a.nx + a.seg - 1) / a.seg;
   if (a.flux == 1)
-    launch_sweep(sweep_x_tma_kernel<1>, ctas, s, a, maps.x_load, maps.x_store);
+    launch_sweep(sweep_x_tma_kernel<1>, ctas, kExSmemBytes, s, a, maps.x_load, maps.x_store);
   else
-    launch_sweep(sweep_x_tma_kernel<0>, ctas, s, a, maps.x_load, maps.x_store);
+    launch_sweep(sweep_x_tma_kernel<0>, ctas, kYSmemBytes, s, a, maps.x_load, maps.x_store);
 }
 
 void launch_sweep_y(const SweepArgs& a0, const TmaMaps& maps, const Geometry& geo,
@@ -1055,11 +1104,11 @@ void launch_sweep_y(const SweepArgs& a0, const TmaMaps& maps, const Geometry& ge
   a.nseg = (a.ny + a.seg - 1) / a.seg;
   const bool peer = a.halo_up || a.halo_dn;
   if (a.flux == 1) {
-    if (peer) launch_sweep(sweep_y_kernel<1, true>, ctas, s, a, maps.y_load, maps.y_store);
-    else launch_sweep(sweep_y_kernel<1, false>, ctas, s, a, maps.y_load, maps.y_store);
+    if (peer) launch_sweep(sweep_y_kernel<1, true>, ctas, kExSmemBytes, s, a, maps.y_load, maps.y_store);
+    else launch_sweep(sweep_y_kernel<1, false>, ctas, kExSmemBytes, s, a, maps.y_load, maps.y_store);
   } else {
-    if (peer) launch_sweep(sweep_y_kernel<0, true>, ctas, s, a, maps.y_load, maps.y_store);
-    else launch_sweep(sweep_y_kernel<0, false>, ctas, s, a, maps.y_load, maps.y_store);
+    if (peer) launch_sweep(sweep_y_kernel<0, true>, ctas, kYSmemBytes, s, a, maps.y_load, maps.y_store);
+    else launch_sweep(sweep_y_kernel<0, false>, ctas, kYSmemBytes, s, a, maps.y_load, maps.y_store);
   }
 }
 

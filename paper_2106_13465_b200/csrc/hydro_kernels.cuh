@@ -24,6 +24,9 @@ constexpr int kChunk = 4;
 constexpr int kNBuf = 3;
 constexpr int kChunkBytes = 32 * 4 * kChunk * 8;                         // 4 KB
 constexpr int kYSmemBytes = 4 * kNBuf * kChunkBytes + 256 + 4 * kNBuf * 8;  // + align, mbarriers
+// exact-10 sweeps: + one 13-double interface memo per thread
+constexpr int kMemoBytes = 13 * 128 * 8;
+constexpr int kExSmemBytes = kYSmemBytes + kMemoBytes;
 
 __host__ __device__ __forceinline__ size_t cell_index(size_t pitch, int v, int i, int j) {
   return ((size_t)(i + 1) * 4 + (size_t)v) * pitch + (size_t)(j + kColOff);
