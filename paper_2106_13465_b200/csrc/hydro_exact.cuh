@@ -196,51 +196,88 @@ __device__ __forceinline__ bool sample0(M& m, const Face& fl, const Face& fr, co
   const Prim& wr = fr.w;
   const double g = k.g;
   const bool same = same_bits(wl.r, wr.r) & same_bits(wl.va, wr.va) & same_bits(wl.p, wr.p);
-  const Side l = make_side(m, fl, g);
-  Side r;
-  if (same) r = l;
-  else r = make_side(m, fr, g);
+  // The two sides ordered by pressure: at p > p_min the low side is on the
+  // shock branch of f_K in every lane and only the high side's branch varies
+  // across the warp, so a warp evaluates three side branches per pressure
+  // instead of four.  Every use of the pair below is a sum (f_L + f_R, the
+  // derivatives, l.c + r.c, ...), and IEEE addition commutes bit for bit.
+  bool rmin;
+  Side lo, hi;
+  {
+    const Side l = make_side(m, fl, g);
+    Side r;
+    if (same) r = l;
+    else r = make_side(m, fr, g);
+    rmin = r.p < l.p;
+    lo = rmin ? r : l;
+    hi = rmin ? l : r;
+  }
   const double du = wr.va - wl.va;
-  if (m.divnf(2.0 * (l.c + r.c), k.gm1) <= du) return false;
+  if (m.divnf(2.0 * (lo.c + hi.c), k.gm1) <= du) return false;  // l.c + r.c
 
-  const bool rmin = r.p < l.p;
-  const double p_min = rmin ? r.p : l.p;  // smin(l.p, r.p)
+  const double p_min = lo.p;  // smin(l.p, r.p)
   double fo = 0.0;                        // + the min side's +0
-  if (!same) fo = side_eval(m, p_min, rmin ? l : r, k).f;
+  if (!same) fo = side_eval(m, p_min, hi, k).f;
   double p;
   if (fo + du >= 0.0) {
     // both rarefactions: closed-form root (:63-69)
-    const double numer = l.c + r.c - k.hg * du;
-    const double ql = m.divnf(l.c, pow_(m, l.p, k.z));
-    double qr = ql;
-    if (!same) qr = m.divnf(r.c, pow_(m, r.p, k.z));
-    const double denom = ql + qr;
+    const double numer = lo.c + hi.c - k.hg * du;
+    const double qlo = m.divnf(lo.c, pow_(m, lo.p, k.z));
+    double qhi = qlo;
+    if (!same) qhi = m.divnf(hi.c, pow_(m, hi.p, k.z));
+    const double denom = qlo + qhi;
     p = pow_(m, m.divnf(numer, denom), k.iz);
   } else {
     // Newton from the linearised guess with the p_min floor, 10 iterations
     const double guess =
-        0.5 * (l.p + r.p) - 0.125 * du * (l.rho + r.rho) * (l.c + r.c);  // :72-74
+        0.5 * (lo.p + hi.p) - 0.125 * du * (lo.rho + hi.rho) * (lo.c + hi.c);  // :72-74
     p = smax(guess, p_min);
-    const SideK lk = side_k(m, l, k), rk = side_k(m, r, k);
-    // Once a step reproduces p exactly, every remaining step does too (same
-    // inputs, same arithmetic), so leaving the loop there is bitwise
-    // identical to running all 10 iterations -- typically after 4-5.
+    const SideK klo = side_k(m, lo, k), khi = side_k(m, hi, k);
+    // The step is a fixed map p -> N(p) (same inputs, same arithmetic), so
+    // once an iterate repeats one of the last T the sequence is periodic
+    // with period T from there and the 10th iterate is known: leaving the
+    // loop then is bitwise identical to running all 10 iterations.  In
+    // rounding, Newton ends on a fixed point (T = 1) or on a 2-, 3- or
+    // 4-cycle of neighbouring doubles about equally often; catching the
+    // cycles too matters because a warp runs until its last lane leaves
+    // (random states: every warp ran all 10 iterations with T = 1 only,
+    // ~6.7 with T <= 4).  pK = p_{j-1-K} for the new iterate p_j.
+    double p1 = -1.0, p2 = -1.0, p3 = -1.0;  // never an iterate (p >= p_min > 0)
 #pragma unroll 1
-    for (int it = 0; it < 10; ++it) {
-      double fL, dfL, fR, dfR;
-      side_fn2(m, p, l, lk, k, fL, dfL);
-      side_fn2(m, p, r, rk, k, fR, dfR);
-      const double f = fL + fR + du;
-      const double df = dfL + dfR;
+    for (int j = 1; j <= 10; ++j) {
+      double fA, dfA, fB, dfB;
+      side_fn2(m, p, lo, klo, k, fA, dfA);
+      side_fn2(m, p, hi, khi, k, fB, dfB);
+      const double f = fA + fB + du;  // = f_L + f_R + du
+      const double df = dfA + dfB;
       double next = p - m.divf(f, df);
       if (next < p_min) next = p_min;
+      // p_10 = p_{j-T+((10-j) mod T)}; p_j itself equals p_{j-T}
       if (next == p) break;
+      if (next == p1) { p = ((10 - j) & 1) ? p : next; break; }
+      if (next == p2) {
+        const int q = (10 - j) % 3;
+        p = q == 0 ? next : (q == 1 ? p1 : p);
+        break;
+      }
+      if (next == p3) {
+        const int q = (10 - j) & 3;
+        p = q == 0 ? next : (q == 1 ? p2 : (q == 2 ? p1 : p));
+        break;
+      }
+      p3 = p2;
+      p2 = p1;
+      p1 = p;
       p = next;
     }
   }
-  const SideEval el = side_eval(m, p, l, k);
-  SideEval er = el;
-  if (!same) er = side_eval(m, p, r, k);
+  const SideEval elo = side_eval(m, p, lo, k);
+  SideEval ehi = elo;
+  if (!same) ehi = side_eval(m, p, hi, k);
+  const SideEval el = rmin ? ehi : elo;
+  const SideEval er = rmin ? elo : ehi;
+  const Side l = rmin ? hi : lo;
+  const Side r = rmin ? lo : hi;
   const double u_star = 0.5 * (wl.va + wr.va) + 0.5 * (er.f - el.f);
   const double xi = 0.0;
   if (xi <= u_star) {  // left of the contact (:208-223)

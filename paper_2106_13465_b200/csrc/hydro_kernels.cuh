@@ -20,8 +20,11 @@ constexpr int kColOff = 3;
 
 // Row-sweep tiling: every warp stages kChunk columns x 32 rows x 4 variables
 // per chunk into its own ring of kNBuf buffers (4 warps per CTA).
+#ifndef HB_NBUF
+#define HB_NBUF 3
+#endif
 constexpr int kChunk = 4;
-constexpr int kNBuf = 3;
+constexpr int kNBuf = HB_NBUF;
 constexpr int kChunkBytes = 32 * 4 * kChunk * 8;                         // 4 KB
 constexpr int kYSmemBytes = 4 * kNBuf * kChunkBytes + 256 + 4 * kNBuf * 8;  // + align, mbarriers
 // exact-10 sweeps: + one 13-double interface memo per thread

@@ -104,7 +104,8 @@ def test_oracle_reports_vacuum_as_validation_error():
 @pytest.mark.parametrize("case,nx,ny,steps,bc,seed", [
     ("blast", 48, 48, 6, "reflect", 0), ("corner_blast", 64, 40, 10, "reflect", 0),
     ("sod_x", 64, 24, 20, "transmit", 0), ("random", 40, 33, 8, "transmit", 5),
-    ("random", 33, 40, 8, "reflect", 6),
+    ("random", 33, 40, 8, "reflect", 6), ("random", 256, 192, 20, "transmit", 11),
+    ("corner_blast", 160, 128, 40, "reflect", 0),
 ])
 def test_gpu_exact10_bitwise_equals_oracle(gpu, case, nx, ny, steps, bc, seed):
     grid = P.make_case(case, nx, ny, MODEL, seed=seed)
