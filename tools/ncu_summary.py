@@ -30,7 +30,8 @@ KEYS = {
     "l2_hit_pct": "lts__t_sector_hit_rate.pct",
 }
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1,
-         "msecond": 1e3}
+         "msecond": 1e3, "ns": 1e-3, "us": 1, "ms": 1e3, "s": 1e6,
+         "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
 
 def raw_rows(rep):
