@@ -28,6 +28,7 @@
 
 #include "hydro_physics.cuh"
 
+
 namespace hb {
 
 namespace exact {
@@ -280,53 +281,42 @@ __device__ __forceinline__ bool sample0(M& m, const Face& fl, const Face& fr, co
   const Side r = rmin ? lo : hi;
   const double u_star = 0.5 * (wl.va + wr.va) + 0.5 * (er.f - el.f);
   const double xi = 0.0;
-  if (xi <= u_star) {  // left of the contact (:208-223)
-    if (p > l.p) {     // left shock
-      const double ratio = m.divnf(p, l.p);
-      const double head = l.u - l.c * m.sqrt(k.zp * ratio + k.z);
-      if (xi <= head) { out = wl; return true; }
-      out = {m.divnf(l.rho * (ratio + k.gm), k.gm * ratio + 1.0), u_star, wl.vb, p};
-      return true;
-    }
-    const double head = l.u - l.c;  // left rarefaction
-    if (xi <= head) { out = wl; return true; }
-    const double c_star = l.c * el.E;
-    const double tail = u_star - c_star;
-    if (xi >= tail) {
-      out = {l.rho * exp_(m, k.ig * el.L), u_star, wl.vb, p};
-      return true;
-    }
-    const double u = k.a2 * (l.c + k.hg * l.u + xi);
-    const double c = k.a2 * (l.c + k.hg * (l.u - xi));
-    const double lc = log_(m, m.divnf(c, l.c));
-    out.r = l.rho * exp_(m, k.er * lc);
-    out.va = u;
-    out.vb = wl.vb;
-    out.p = l.p * exp_(m, k.ep * lc);
+  // sample_riemann's right half (:225-240) is the left half (:208-223)
+  // mirrored, u -> -u, xi -> -xi: every right-side expression is the exact
+  // negation of the left-side one on negated operands (IEEE negation and
+  // round-to-nearest are sign-symmetric), and each comparison flips with it.
+  // One mirrored evaluation keeps a warp whose lanes sample both sides of
+  // the contact in one branch family; va is negated back at the end.
+  const bool lft = xi <= u_star;
+  const Side& S = lft ? l : r;
+  const SideEval& E = lft ? el : er;
+  const Prim& wS = lft ? wl : wr;
+  const double su = lft ? S.u : -S.u;
+  const double sus = lft ? u_star : -u_star;
+  const double sx = lft ? xi : -xi;
+  double va;
+  if (p > S.p) {  // shock
+    const double ratio = m.divnf(p, S.p);
+    const double head = su - S.c * m.sqrt(k.zp * ratio + k.z);
+    if (sx <= head) { out = wS; return true; }
+    out = {m.divnf(S.rho * (ratio + k.gm), k.gm * ratio + 1.0), u_star, wS.vb, p};
     return true;
   }
-  if (p > r.p) {  // right shock (:225-240)
-    const double ratio = m.divnf(p, r.p);
-    const double head = r.u + r.c * m.sqrt(k.zp * ratio + k.z);
-    if (xi >= head) { out = wr; return true; }
-    out = {m.divnf(r.rho * (ratio + k.gm), k.gm * ratio + 1.0), u_star, wr.vb, p};
+  const double head = su - S.c;  // rarefaction
+  if (sx <= head) { out = wS; return true; }
+  const double c_star = S.c * E.E;
+  const double tail = sus - c_star;
+  if (sx >= tail) {
+    out = {S.rho * exp_(m, k.ig * E.L), u_star, wS.vb, p};
     return true;
   }
-  const double head = r.u + r.c;  // right rarefaction
-  if (xi >= head) { out = wr; return true; }
-  const double c_star = r.c * er.E;
-  const double tail = u_star + c_star;
-  if (xi <= tail) {
-    out = {r.rho * exp_(m, k.ig * er.L), u_star, wr.vb, p};
-    return true;
-  }
-  const double u = k.a2 * (-r.c + k.hg * r.u + xi);
-  const double c = k.a2 * (r.c - k.hg * (r.u - xi));
-  const double lc = log_(m, m.divnf(c, r.c));
-  out.r = r.rho * exp_(m, k.er * lc);
-  out.va = u;
-  out.vb = wr.vb;
-  out.p = r.p * exp_(m, k.ep * lc);
+  va = k.a2 * (S.c + k.hg * su + sx);
+  const double c = k.a2 * (S.c + k.hg * (su - sx));
+  const double lc = log_(m, m.divnf(c, S.c));
+  out.r = S.rho * exp_(m, k.er * lc);
+  out.va = lft ? va : -va;
+  out.vb = wS.vb;
+  out.p = S.p * exp_(m, k.ep * lc);
   return true;
 }
 

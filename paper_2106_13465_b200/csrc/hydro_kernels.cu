@@ -134,10 +134,18 @@ __device__ __forceinline__ Flux riemann(M& m, const Face& L, const Face& R, cons
   }
 }
 
+#ifndef HB_FOLD_EXACT
+#define HB_FOLD_EXACT 1
+#endif
+#ifndef HB_FOLD_HLLC
+#define HB_FOLD_HLLC 0
+#endif
+
 template <int STAGE, bool WANT_DT, int FLUX, class M, class Old, class Mem>
 __device__ __forceinline__ void step_cell(M& m, const Window& w, const Cons& uC, double half,
                                           double dtdx, double spacing, const Gas& g,
-                                          const Old& old, StepOut& o, Mem& memo) {
+                                          const Old& old, StepOut& o, Mem& memo,
+                                          bool upd = true) {
   o.fC = to_prim(m, uC, g, o.wC);
   Cons el, er;
   predict_evolved(m, w.wA, w.wB, o.wC, half, g, el, er);
@@ -150,7 +158,7 @@ __device__ __forceinline__ void step_cell(M& m, const Window& w, const Cons& uC,
   o.fR = -1;
   if (STAGE >= 1) o.F = riemann<FLUX>(m, w.frPrev, o.fl, g, o.fR, memo);
   o.fr = face_prim(m, er, w.wB, g);
-  if (STAGE >= 2) {
+  if (STAGE >= 2 && upd) {
     o.un = old();
     Recip rn;
     o.fU = update_cell(m, o.un, w.fluxPrev, o.F, dtdx, rn);
@@ -187,6 +195,7 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
                                            unsigned long long key_base, int kg,
                                            unsigned long long& ekey) {
   M m;
+  if constexpr (M::kFast) m.ok = g.rgm1.pos;  // total_energy's divnp by gamma - 1
   const double half = 0.5 * dtdx;
   using Mem = std::conditional_t<FLUX == 1, Memo, NoMemo>;
   Mem memo{};
@@ -208,7 +217,11 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
     w.wB = o.wC;
     w.frPrev = o.fr;
   }
-  {  // c = ka: faces of cell ka and the flux through its left interface
+  // FOLD: the c = ka iteration runs in the main loop with its update
+  // skipped, so the walker holds one copy of the Riemann solve (the exact-10
+  // solver is ~5k instructions per copy: instruction-cache pressure)
+  constexpr bool kFold = FLUX == 1 ? HB_FOLD_EXACT : HB_FOLD_HLLC;
+  if constexpr (!kFold) {  // c = ka: faces of cell ka and the flux through its left interface
     const Cons uC = src.load(ka + 1);
     StepOut o;
     step_cell<1, false, FLUX>(m, w, uC, half, dtdx, spacing, g, none, o, memo);
@@ -222,17 +235,20 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
     w.fluxPrev = o.F;
   }
 #pragma unroll 1
-  for (int c = ka + 1; c <= kb + 1; ++c) {
+  for (int c = kFold ? ka : ka + 1; c <= kb + 1; ++c) {
     const Cons uC = src.load(c + 1);
     StepOut o;
+    const bool upd = !kFold || c > ka;
     step_cell<2, WANT_DT, FLUX>(m, w, uC, half, dtdx, spacing, g,
-                                [&] { return src.reload(c - 1); }, o, memo);
+                                [&] { return src.reload(c - 1); }, o, memo, upd);
     if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(c + 1 + kg) << 2) | o.fC);
     if (o.fR >= 0)
       keep_min(ekey, key_base | (1ull << 20) | ((unsigned long long)(c - 1 + kg) << 2) | o.fR);
-    if (o.fU >= 0)
-      keep_min(ekey, key_base | (2ull << 20) | ((unsigned long long)(c - 1 + kg) << 2) | o.fU);
-    sink(c - 1, o);
+    if (upd) {
+      if (o.fU >= 0)
+        keep_min(ekey, key_base | (2ull << 20) | ((unsigned long long)(c - 1 + kg) << 2) | o.fU);
+      sink(c - 1, o);
+    }
     src.boundary(c);
     w.wA = w.wB;
     w.wB = o.wC;
