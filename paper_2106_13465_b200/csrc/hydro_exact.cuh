@@ -29,6 +29,7 @@
 #include "hydro_physics.cuh"
 
 
+
 namespace hb {
 
 namespace exact {
@@ -138,23 +139,6 @@ __device__ __forceinline__ SideK side_k(M& m, const Side& s, const K& k) {
           m.divnf(1.0, s.rho * s.c), m.recip(s.p)};
 }
 
-// f_K(p) and f_K'(p) of one side at the same p (exact_riemann.cpp:26-45);
-// the rarefaction branch shares log(p/p_K) between the two powers.
-template <class M>
-__device__ __forceinline__ void side_fn2(M& m, double p, const Side& s, const SideK& sk,
-                                         const K& k, double& f, double& df) {
-  if (p > s.p) {
-    const Recip d = m.recip(p + sk.b);
-    const double root = m.sqrt(m.divn(sk.a, d));
-    f = (p - s.p) * root;
-    df = root * (1.0 - m.divn(0.5 * (p - s.p), d));
-  } else {
-    const double l = log_(m, m.divn(p, sk.rp));
-    f = sk.cf * (exp_(m, k.z * l) - 1.0);
-    df = sk.dn * exp_(m, k.zn * l);
-  }
-}
-
 // side_fn (exact_riemann.cpp:26-35) keeping, on the rarefaction branch,
 // L = log(p/p_K) and E = (p/p_K)^z = exp(z L) for the sampling below.
 struct SideEval {
@@ -247,8 +231,32 @@ __device__ __forceinline__ bool sample0(M& m, const Face& fl, const Face& fr, co
 #pragma unroll 1
     for (int j = 1; j <= 10; ++j) {
       double fA, dfA, fB, dfB;
-      side_fn2(m, p, lo, klo, k, fA, dfA);
-      side_fn2(m, p, hi, khi, k, fB, dfB);
+      // f_K(p), f_K'(p) of both sides (exact_riemann.cpp:26-45); the
+      // rarefaction branch shares log(p/p_K) between its two powers.
+      // Low side without a branch: p >= p_min = lo.p, and at p == lo.p the
+      // shock form's f = (p - lo.p) * root = +0 is the rarefaction
+      // branch's cf * (exp(z log 1) - 1) = +0 bit for bit, while f' is the
+      // rarefaction's dn * exp(0) = dn.  It is evaluated inside both arms
+      // of the high side's branch, so each arm holds two independent chains.
+      auto low = [&] {
+        const Recip d = m.recip(p + klo.b);
+        const double root = m.sqrt(m.divn(klo.a, d));
+        fA = (p - lo.p) * root;
+        const double dq = root * (1.0 - m.div(0.5 * (p - lo.p), d));  // zero-safe at p == lo.p
+        dfA = (p > lo.p) ? dq : klo.dn;
+      };
+      if (p > hi.p) {
+        low();
+        const Recip d = m.recip(p + khi.b);
+        const double root = m.sqrt(m.divn(khi.a, d));
+        fB = (p - hi.p) * root;
+        dfB = root * (1.0 - m.divn(0.5 * (p - hi.p), d));
+      } else {
+        low();
+        const double l = log_(m, m.divn(p, khi.rp));
+        fB = khi.cf * (exp_(m, k.z * l) - 1.0);
+        dfB = khi.dn * exp_(m, k.zn * l);
+      }
       const double f = fA + fB + du;  // = f_L + f_R + du
       const double df = dfA + dfB;
       double next = p - m.divf(f, df);
