@@ -214,9 +214,11 @@ int hydro_gpu_reset_counters(hydro_gpu_ctx* ctx);
 int hydro_gpu_tune(hydro_gpu_ctx* ctx, int seg_x, int seg_y, int block);
 /* Self-test of the device fp64 division (op 0), square root (op 1),
  * signed-zero-safe division (op 2) and density division (op 4: zero
- * numerators, positive denominators) fast paths against the compiler's IEEE
- * operations on n operand pairs (b ignored for sqrt), and of the fast-pass
- * minmod of two slopes (op 3) against the reference's comparisons.
+ * numerators, denominators inside the fast-pass envelope [2^-256, 2^256))
+ * and envelope-bounded division (op 5: no range test) fast paths against the
+ * compiler's IEEE operations on n operand pairs (b ignored for sqrt), and of
+ * the fast-pass minmod of two slopes (op 3) against the reference's
+ * comparisons.
  * in_range[k] = 1 where the fast path applied. */
 int hydro_gpu_math_selftest(int op, const double* a, const double* b, double* fast,
                             double* exact, int* in_range, size_t n);

@@ -943,7 +943,7 @@ int hydro_gpu_totals(hydro_gpu_ctx* c, double out[4]) {
 
 int hydro_gpu_math_selftest(int op, const double* a, const double* b, double* fast,
                             double* exact, int* in_range, size_t n) {
-  if (op < 0 || op > 4 || !a || !fast || !exact || !in_range) return HYDRO_GPU_ERR_CONFIG;
+  if (op < 0 || op > 5 || !a || !fast || !exact || !in_range) return HYDRO_GPU_ERR_CONFIG;
   double *da = nullptr, *db = nullptr, *df = nullptr, *dr = nullptr;
   int* dk = nullptr;
   const size_t bytes = n * sizeof(double);

@@ -195,7 +195,7 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
                                            unsigned long long key_base, int kg,
                                            unsigned long long& ekey) {
   M m;
-  if constexpr (M::kFast) m.ok = g.rgm1.pos;  // total_energy's divnp by gamma - 1
+  if constexpr (M::kFast) m.ok = g.fast;  // divb's bounds need gamma - 1 in [2^-6, 2^6]
   const double half = 0.5 * dtdx;
   using Mem = std::conditional_t<FLUX == 1, Memo, NoMemo>;
   Mem memo{};
@@ -983,6 +983,9 @@ __global__ void math_selftest_kernel(int op, const double* a, const double* b, d
     ref[t] = a[t] / b[t];
   } else if (op == 4) {  // density quotient (zero numerators, positive denominators)
     fast[t] = fm.divf(a[t], b[t]);
+    ref[t] = a[t] / b[t];
+  } else if (op == 5) {  // envelope-bounded quotient (divb: no range test)
+    fast[t] = fm.divb(a[t], fm.recip(b[t]));
     ref[t] = a[t] / b[t];
   } else if (op == 2) {
     fast[t] = fm.divz(a[t], b[t]);

@@ -82,15 +82,20 @@ def test_sqrt_fast_path_is_ieee():
 
 def test_division_zero_numerator_fast_and_signed():
     """Zero momenta are everywhere in the benchmark cases (u = v = 0 at rest):
-    +-0 / positive-normal must stay on the fast path with the IEEE sign."""
+    +-0 / a density inside the fast-pass envelope [2^-256, 2^256) must stay on
+    the fast path with the IEEE sign; outside it the exact pass takes over."""
     rng = np.random.default_rng(7)
-    b = np.concatenate([rng.uniform(1e-300, 1e300, 4096), rng.uniform(1e-6, 1e6, 4096)])
+    b = np.concatenate([10.0 ** rng.uniform(-77, 77, 4096), rng.uniform(1e-6, 1e6, 4096)])
     for zero in (0.0, -0.0):
         a = np.full(b.size, zero)
         fast, exact, ok = run(4, a, b)
         assert ok.all()
         assert np.array_equal(bits(fast), bits(exact))
         assert np.array_equal(bits(fast), bits(a / b))
+    # densities outside the envelope leave the fast path (exact recompute)
+    for far in (1e-300, 1e-78, 1e78, 1e300):
+        _, _, ok = run(4, np.zeros(1), np.full(1, far))
+        assert not ok.any()
     # negative or non-normal denominators leave the fast path (exact recompute)
     _, _, ok = run(4, np.array([-0.0, 0.0, 0.0, 0.0, 1.0]),
                    np.array([-2.0, 0.0, 5e-324, np.inf, -3.0]))
@@ -104,7 +109,9 @@ def test_density_division_sign_or_is_ieee():
     a = operands(rng, 1 << 20)
     b = np.abs(rng.permutation(operands(rng, 1 << 20))[: a.size])
     fast, exact, ok = run(4, a, b)
-    assert ok.mean() > 0.8
+    env = (b >= np.ldexp(1.0, -256)) & (b < np.ldexp(1.0, 256))  # the fast-pass envelope
+    assert ok[env].mean() > 0.8
+    assert not ok[~env].any()
     assert np.array_equal(bits(fast[ok]), bits(exact[ok]))
 
 
@@ -138,3 +145,20 @@ def test_minmod_fast_equals_reference_comparisons():
     b = np.concatenate([y, ties, -ties, eb.ravel()])
     fast, exact, ok = run(3, a, b)
     assert np.array_equal(bits(fast), bits(exact))
+
+
+def test_bounded_division_is_ieee_inside_the_envelope():
+    """divb (p / (gamma - 1), gamma p / rho) skips the range test: for every
+    numerator in [2^-256, 65 * 2^256) and denominator in the envelope
+    [2^-256, 2^256) the fast path must give the IEEE quotient bit for bit."""
+    rng = np.random.default_rng(2106)
+    n = 1 << 20
+    a = np.ldexp(rng.uniform(1.0, 2.0, n), rng.integers(-256, 262, n))
+    b = np.ldexp(rng.uniform(1.0, 2.0, n), rng.integers(-256, 256, n))
+    lo, hi = np.ldexp(1.0, -256), np.nextafter(np.ldexp(1.0, 256), 0.0)
+    top = np.nextafter(65.0 * np.ldexp(1.0, 256), 0.0)
+    a = np.concatenate([a, [lo, lo, top, top, 0.4, 1.4]])
+    b = np.concatenate([b, [lo, hi, lo, hi, 0.3999999999999999, 0.4]])
+    fast, exact, _ = run(5, a, b)
+    assert np.array_equal(bits(fast), bits(exact))
+    assert np.array_equal(bits(fast), bits(a / b))
