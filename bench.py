@@ -223,11 +223,20 @@ def main():
     from paper_2106_13465_b200 import slab as S
 
     assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    # HYDRO_BENCH_SHARED_GPU=1: code-path check of the N>1 bench on a 1-GPU box
+    # (every rank on cuda:0, gloo for the host-side dt allreduce, so no kernel
+    # waits on another rank) -- its numbers are not measurements
+    shared = world > 1 and os.environ.get("HYDRO_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     model = P.GasModel()
     # weak scaling grows the slab axis i by the GPU count;
     # strong scaling splits one grid

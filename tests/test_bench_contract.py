@@ -34,3 +34,34 @@ def test_reference_arm_nonzero_ranks_exit_quietly():
                          capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-2000:]
     assert out.stdout.strip() == ""
+
+
+def _torchrun_bench(n, port, *extra):
+    env = dict(os.environ, HYDRO_BENCH_SHARED_GPU="1")
+    return subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+                           f"--master-port={port}", os.path.join(ROOT, "bench.py"), "--gpus", str(n),
+                           "--steps", "1", "--warmup", "1", "--no-variants", *extra],
+                          capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_multi_rank_bench_code_path(gpu):
+    """The driver's N>1 launch (torchrun, one process per GPU): every rank runs
+    the slab driver with the peer-memory halo and rank 0 alone prints one
+    contract line.  Run here with all ranks sharing cuda:0 and gloo for the
+    host-side dt allreduce (HYDRO_BENCH_SHARED_GPU), so it checks the code
+    path, not the speed; 3 ranks give the middle slab two neighbours."""
+    out = _torchrun_bench(3, 29641)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 3 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["config"]["cells"] == 3 * 2048 * 2048
+    assert "peer-memory" in d["config"]["halo"]
+    for key in ("roofline", "e2e", "gpu_launches", "clocks", "ms_per_step"):
+        assert key in d, key
