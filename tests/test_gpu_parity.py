@@ -295,3 +295,26 @@ def test_slab_device_initialiser_matches_full_grid(gpu, case, seed):
         want = S.slab_planes(full.planes, nx, world, r)
         assert np.array_equal(got[:, 2:geo.nx + 2, 2:ny + 2], want[:, 2:geo.nx + 2, 2:ny + 2]), r
         sl.grid.close()
+
+
+@pytest.mark.gpu
+def test_one_cell_perturbation_stays_inside_the_stencil(gpu):
+    """Stencil locality of the whole GPU step (the reference pins it per strip,
+    proj/tests/test_kernel.cpp:153-179): with a fixed dt (advance_sequential)
+    a one-ulp change of one interior cell can only reach cells within the
+    two-cell stencil of the column sweep and then of the row sweep -- a 5x5
+    box (plus the mirrored ghost copies) -- and leaves every other value bit
+    for bit unchanged."""
+    base = P.make_case("random", 48, 40, MODEL, seed=31)
+    pert = base.copy()
+    i0, j0 = 21, 17
+    for v in range(4):
+        k = (v, i0 + 1, j0 + 1)  # planes index = grid index + 1 (ghost offset -1 -> 0)
+        pert.planes[k] = np.nextafter(pert.planes[k], np.inf)
+    P.advance_gpu(base, MODEL, 2.5e-4, "transmit")
+    P.advance_gpu(pert, MODEL, 2.5e-4, "transmit")
+    diff = np.argwhere(base.planes != pert.planes)
+    assert len(diff) > 0
+    for v, ii, jj in diff:
+        i, j = ii - 1, jj - 1
+        assert abs(i - i0) <= 2 and abs(j - j0) <= 2, (v, i, j)
