@@ -702,6 +702,10 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : HB_EX_MINB) sweep
     const bool send_up = PEER && a.halo_up && grp == 0;
     const bool send_dn = PEER && a.halo_dn && (grp << 5) + 32 >= nx - 1;
     wrote_peer |= send_up | send_dn;
+    // this lane's row has ghost-row or halo copies to write (rare lanes only:
+    // the per-cell test is one predicate)
+    const bool extra = active && (((mirror_lo || send_up) && i <= 2) ||
+                                  ((mirror_hi || send_dn) && i >= nx - 1));
     const int gi = a.row0 + i;
     const unsigned long long base = error_key(a.step, 2, gi, 0, 0, 0);
     auto put_row = [&](int ii, int j, const Cons& u, bool neg) {
@@ -728,6 +732,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : HB_EX_MINB) sweep
       auto sink = [&](int k, const StepOut& o) {
         t.put(k, o.un);
         const int j = k - 1;
+        if (extra) {
         if (mirror_lo && active && i <= 2) {  // x-wall ghosts for the next column sweep (grid.cpp:26-42)
           if (refl) put_row(1 - i, j, o.un, true);
           else if (i == 1) { put_row(0, j, o.un, false); put_row(-1, j, o.un, false); }
@@ -741,6 +746,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : HB_EX_MINB) sweep
             put_peer(a.halo_up + (size_t)(i - 1) * 4 * pitch + (j + kColOff), o.un);
           if (send_dn && active && i >= nx - 1)  // -> lower neighbour's ghost rows -1..0
             put_peer(a.halo_dn + (size_t)(i - (nx - 1)) * 4 * pitch + (j + kColOff), o.un);
+        }
         }
         if (a.want_limit) {
           if (o.fD >= 0) keep_min(dt_item, error_key(a.step + 1, 0, gi, 0, j, o.fD));
