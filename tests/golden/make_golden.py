@@ -78,6 +78,12 @@ FULL = [
 FULL_EXACT10 = [
     ("cfg1_sod_x_2048_200_exact10", "sod_x", 2048, 2048, "transmit", 200, 0,
      "BASELINE config 1 with its stated exact Riemann solver (10 Newton iterations), full"),
+    ("cfg2_random_8192_50_exact10", "random", 8192, 8192, "transmit", 50, SEED_CFG2,
+     "BASELINE config 2 with its stated exact Riemann solver (10 Newton iterations), full"),
+    ("cfg4_random_16384_20_exact10", "random", 16384, 16384, "transmit", 20, SEED_CFG4,
+     "BASELINE config 4 at P=1 with its stated exact Riemann solver, full"),
+    ("random_1024_20_exact10", "random", 1024, 1024, "transmit", 20, 7,
+     "dense random states, exact-10: Newton cycle exits at scale"),
 ]
 
 
@@ -113,10 +119,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--only", default=None)
+    ap.add_argument("--out", default=None, help="write to this file instead (parallel runs)")
     args = ap.parse_args()
     if not O.ref_available():
         sys.exit("oracle/_ref/libhydro_ref.so missing: make -C oracle")
-    out_path = os.path.join(HERE, "golden_full.json" if args.full else "golden.json")
+    out_path = args.out or os.path.join(HERE, "golden_full.json" if args.full else "golden.json")
     table = FULL if args.full else SMALL
     result = {}
     if os.path.exists(out_path):
