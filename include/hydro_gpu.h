@@ -200,6 +200,37 @@ int hydro_gpu_slab_finish(hydro_gpu_ctx* ctx);
 /* Synchronises and decodes a (possibly all-reduced) error key. */
 int hydro_gpu_decode_error(hydro_gpu_ctx* ctx, uint64_t key, hydro_gpu_error* out);
 
+/* ---- one process, several GPUs (n_gpus > 1) -------------- */
+/* A row-slab decomposition of one grid driven by the calling host thread:
+ * slab k (rows split like split_range, proj/src/decomposition.cpp:9-16) is a
+ * hydro_gpu_ctx on devices[k] (NULL: device k mod the device count; repeated
+ * ordinals are allowed, e.g. all slabs on one GPU).  Peer access is enabled
+ * between all slab devices; the halo is the peer-memory inbox path above
+ * with plain device pointers, and the dt of every step is the minimum of the
+ * slabs' limits, read over NVLink by a one-warp kernel on each device after
+ * an event join (the single-process twin of the NCCL min-allreduce,
+ * compute_dt_parallel, proj/src/schedulers.cpp:47-65).  cfg describes the
+ * whole grid (row0 / global_nx / wall_* are ignored).  Results are bitwise
+ * those of one context on the whole grid.  Returns HYDRO_GPU_ERR_CUDA if two
+ * distinct devices cannot access each other's memory. */
+typedef struct hydro_gpu_group hydro_gpu_group;
+int hydro_gpu_group_create(const hydro_gpu_cfg* cfg, int n_gpus, const int* devices,
+                           hydro_gpu_group** out);
+int hydro_gpu_group_destroy(hydro_gpu_group* group);
+int hydro_gpu_group_last_error(const hydro_gpu_group* group, hydro_gpu_error* out);
+/* Slab count and, per slab (arrays of n entries, any may be NULL), its first
+ * global row minus 1, its rows and its device. */
+int hydro_gpu_group_slabs(const hydro_gpu_group* group, int* n, int* row0, int* rows,
+                          int* devices);
+/* Whole-grid planes in the reference layout (as hydro_gpu_upload/download). */
+int hydro_gpu_group_upload(hydro_gpu_group* group, const double* const planes[4],
+                           size_t row_stride);
+int hydro_gpu_group_download(hydro_gpu_group* group, double* const planes[4],
+                             size_t row_stride);
+int hydro_gpu_group_init_case(hydro_gpu_group* group, int case_id, uint64_t seed);
+/* run_sequential over all slabs; *last_dt as hydro_gpu_run. */
+int hydro_gpu_group_run(hydro_gpu_group* group, int steps, double* last_dt);
+
 /* ---- instrumentation ---------------------------------------------------- */
 /* When on, every sweep launch is bracketed by CUDA events on the launch
  * stream; hydro_gpu_kernel_times returns the summed device milliseconds and

@@ -101,6 +101,14 @@ def lib() -> C.CDLL:
         "hydro_gpu_state_hash": ([_ctx, P(u64)], i),
         "hydro_gpu_totals": ([_ctx, _dp], i),
         "hydro_init_case_host": ([i, i, i, d, u64, _planes, sz, _dp, _dp], i),
+        "hydro_gpu_group_create": ([P(Cfg), i, P(i), P(_ctx)], i),
+        "hydro_gpu_group_destroy": ([_ctx], i),
+        "hydro_gpu_group_last_error": ([_ctx, P(ErrorInfo)], i),
+        "hydro_gpu_group_slabs": ([_ctx, P(i), P(i), P(i), P(i)], i),
+        "hydro_gpu_group_upload": ([_ctx, _planes, sz], i),
+        "hydro_gpu_group_download": ([_ctx, _planes, sz], i),
+        "hydro_gpu_group_init_case": ([_ctx, i, u64], i),
+        "hydro_gpu_group_run": ([_ctx, i, _dp], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -394,6 +394,77 @@ class GpuGrid:
         return C.cast(p, C.c_void_p).value, pitch.value
 
 
+class GpuGroup:
+    """One grid as row slabs over several devices, driven by this thread
+    (hydro_gpu_group, include/hydro_gpu.h): peer-memory halo and an on-device
+    dt min across slabs; bitwise equal to one GpuGrid on the whole grid.
+    devices: one ordinal per slab (repeats allowed, e.g. [0, 0, 0])."""
+
+    def __init__(self, nx: int, ny: int, dx: float, dy: float, model: GasModel = GasModel(),
+                 bc: str = "reflect", devices=(0,), flux: str = "hllc"):
+        if bc not in BC:
+            raise ConfigError(f"unknown boundary '{bc}' (expected reflect or transmit)")
+        if flux not in FLUX:
+            raise ConfigError(f"unknown flux '{flux}' (expected hllc or exact10)")
+        self.nx, self.ny, self.dx, self.dy = nx, ny, dx, dy
+        cfg = L.Cfg(nx, ny, dx, dy, model.gamma, model.cfl, BC[bc], FLUX[flux], -1, 0, nx, 1, 1)
+        n = len(devices)
+        devs = (C.c_int * n)(*devices)
+        self._lib = L.lib()
+        self._g = C.c_void_p()
+        rc = self._lib.hydro_gpu_group_create(C.byref(cfg), n, devs, C.byref(self._g))
+        if rc:
+            _raise_for(rc, message=f"hydro_gpu_group_create failed "
+                                   f"({self._lib.hydro_gpu_status_string(rc).decode()}) "
+                                   f"for {n} slabs of a {nx}x{ny} grid")
+
+    def close(self):
+        if self._g:
+            self._lib.hydro_gpu_group_destroy(self._g)
+            self._g = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _check(self, rc: int):
+        if rc:
+            info = L.ErrorInfo()
+            self._lib.hydro_gpu_group_last_error(self._g, C.byref(info))
+            _raise_for(rc, info)
+
+    def slabs(self) -> list[tuple[int, int, int]]:
+        """(row0, rows, device) per slab."""
+        n = C.c_int(0)
+        self._check(self._lib.hydro_gpu_group_slabs(self._g, C.byref(n), None, None, None))
+        r0, rows, dev = (C.c_int * n.value)(), (C.c_int * n.value)(), (C.c_int * n.value)()
+        self._check(self._lib.hydro_gpu_group_slabs(self._g, C.byref(n), r0, rows, dev))
+        return list(zip(r0, rows, dev))
+
+    def upload(self, planes: np.ndarray):
+        self._check(self._lib.hydro_gpu_group_upload(self._g, L.planes_of(planes), planes.shape[2]))
+
+    def download(self, planes: np.ndarray):
+        self._check(self._lib.hydro_gpu_group_download(self._g, L.planes_of(planes),
+                                                       planes.shape[2]))
+
+    def init_case(self, case: str, seed: int = 0):
+        self._check(self._lib.hydro_gpu_group_init_case(self._g, CASES[case], seed))
+
+    def run(self, steps: int) -> float:
+        last = C.c_double(0.0)
+        self._check(self._lib.hydro_gpu_group_run(self._g, steps, C.byref(last)))
+        return last.value
+
+
 def _context_for(grid: Grid2D, model: GasModel, bc: str, flux: str = "hllc") -> GpuGrid:
     g = GpuGrid(grid.nx, grid.ny, grid.dx, grid.dy, model, bc, flux=flux)
     g.upload(grid.planes)

@@ -318,3 +318,53 @@ def test_one_cell_perturbation_stays_inside_the_stencil(gpu):
     for v, ii, jj in diff:
         i, j = ii - 1, jj - 1
         assert abs(i - i0) <= 2 and abs(j - j0) <= 2, (v, i, j)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,case,bc,flux", [
+    (2, "sod_x", "transmit", "hllc"), (3, "random", "transmit", "hllc"),
+    (5, "corner_blast", "reflect", "hllc"), (4, "blast", "reflect", "hllc"),
+    (3, "random", "reflect", "exact10"),
+])
+def test_single_process_group_equals_one_domain(gpu, n, case, bc, flux):
+    """hydro_gpu_group (one host thread, n row slabs, peer-memory halo,
+    on-device dt min): here all slabs share cuda:0, so the event joins and
+    inbox parities run for real; every plane and ghost, the last dt and the
+    digest equal a single context on the whole grid."""
+    nx, ny, steps = 77, 52, 30
+    one = P.make_case(case, nx, ny, MODEL, seed=9)
+    grp = one.copy()
+    dt_one = P.run_gpu(one, MODEL, steps, bc, flux=flux)
+    with P.GpuGroup(nx, ny, grp.dx, grp.dy, MODEL, bc, devices=[0] * n, flux=flux) as g:
+        assert [r for _, r, _ in g.slabs()] == [nx // n + (1 if k < nx % n else 0) for k in range(n)]
+        g.upload(grp.planes)
+        dt_grp = g.run(steps)
+        g.download(grp.planes)
+    assert dt_grp == dt_one
+    assert np.array_equal(grp.planes, one.planes)
+
+
+@pytest.mark.gpu
+def test_single_process_group_device_init_and_error(gpu):
+    """The group's device initialiser builds the global case slab by slab,
+    and a positivity failure is the one the single domain reports."""
+    nx, ny = 64, 40
+    ref = P.make_case("sod_x", nx, ny, MODEL)
+    P.run_gpu(ref, MODEL, 12, "transmit")
+    got = np.zeros_like(ref.planes)
+    with P.GpuGroup(nx, ny, 1.0 / nx, 1.0 / ny, MODEL, "transmit", devices=[0, 0, 0]) as g:
+        g.init_case("sod_x")
+        g.run(12)
+        g.download(got)
+    assert np.array_equal(got, ref.planes)
+    # CFL 25 drives the blast to a positivity failure (test_schedulers.cpp:115-128)
+    hot = P.GasModel(cfl=25.0)
+    one = P.make_case("blast", 64, 64, hot)
+    with pytest.raises(P.PositivityError) as e1:
+        P.run_gpu(one, hot, 5, "reflect")
+    two = P.make_case("blast", 64, 64, hot)
+    with P.GpuGroup(64, 64, two.dx, two.dy, hot, "reflect", devices=[0, 0, 0]) as g:
+        g.upload(two.planes)
+        with pytest.raises(P.PositivityError) as e2:
+            g.run(5)
+    assert str(e1.value) == str(e2.value)
