@@ -27,6 +27,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "hydro/errors.hpp"
 #include "hydro/grid.hpp"
@@ -36,7 +37,9 @@
 namespace hydro {
 
 struct GpuOptions {
-  int device = -1;                    // CUDA device; -1 = current
+  int device = -1;                    // CUDA device; -1 = current (gpus == 1)
+  int gpus = 1;                       // > 1: row slabs on devices 0..gpus-1 (hydro_gpu_group),
+                                      // all on `device` if it is >= 0
   int bc = HYDRO_GPU_BC_REFLECT;      // the reference's walls; TRANSMIT for BASELINE configs
   int flux = HYDRO_GPU_FLUX_HLLC;     // the reference hot path; EXACT10 = BASELINE's solver
 };
@@ -102,10 +105,53 @@ inline const double* plane(const Grid2D& g, int v) {
 
 }  // namespace gpu_detail
 
+// run_sequential over row slabs on several GPUs driven by this thread
+// (hydro_gpu_group: peer-memory halo, on-device dt min), bitwise equal to
+// the single-device run.
+inline double run_gpu_slabs(Grid2D& grid, const GasModel& model, int steps,
+                            const GpuOptions& opt) {
+  hydro_gpu_cfg cfg{};
+  cfg.nx = grid.nx();
+  cfg.ny = grid.ny();
+  cfg.dx = grid.dx();
+  cfg.dy = grid.dy();
+  cfg.gamma = model.gamma;
+  cfg.cfl = model.cfl;
+  cfg.bc = opt.bc;
+  cfg.flux = opt.flux;
+  cfg.device = -1;
+  // device >= 0: every slab on that device (a single-GPU check of the slab path)
+  std::vector<int> devices(opt.gpus > 0 ? opt.gpus : 1, opt.device);
+  hydro_gpu_group* g = nullptr;
+  int rc = hydro_gpu_group_create(&cfg, opt.gpus, opt.device >= 0 ? devices.data() : nullptr, &g);
+  if (rc != HYDRO_GPU_OK)
+    gpu_detail::raise(rc, std::string("hydro_gpu_group_create: ") + hydro_gpu_status_string(rc));
+  auto fail = [&](int status) {
+    hydro_gpu_error e{};
+    hydro_gpu_group_last_error(g, &e);
+    hydro_gpu_group_destroy(g);
+    gpu_detail::raise(status, e.message);
+  };
+  const double* in[4];
+  double* out[4];
+  for (int v = 0; v < kNumVars; ++v) {
+    in[v] = gpu_detail::plane(grid, v);
+    out[v] = &grid.at(Var(v), -1, -1);
+  }
+  if ((rc = hydro_gpu_group_upload(g, in, grid.ny() + 2 * kGhost)) != HYDRO_GPU_OK) fail(rc);
+  double last_dt = 0.0;
+  const int run_rc = hydro_gpu_group_run(g, steps, &last_dt);
+  if ((rc = hydro_gpu_group_download(g, out, grid.ny() + 2 * kGhost)) != HYDRO_GPU_OK) fail(rc);
+  if (run_rc != HYDRO_GPU_OK) fail(run_rc);
+  hydro_gpu_group_destroy(g);
+  return last_dt;
+}
+
 // run_sequential on the GPU: `steps` steps of BC -> dt -> column sweep ->
 // BC -> row sweep, bitwise equal to the reference; returns the last dt.
 inline double run_gpu(Grid2D& grid, const GasModel& model, int steps,
                       const GpuOptions& opt = {}) {
+  if (opt.gpus > 1) return run_gpu_slabs(grid, model, steps, opt);
   gpu_detail::Context ctx(grid, model, opt);
   const double* planes[4];
   for (int v = 0; v < kNumVars; ++v) planes[v] = gpu_detail::plane(grid, v);

@@ -58,6 +58,19 @@ def test_gpu_strategy_equals_cpu_strategy(case, n, steps, strategy):
 
 @needs_bin
 @pytest.mark.gpu
+@pytest.mark.parametrize("gpus", [2, 3])
+def test_gpu_strategy_row_slabs_equal_cpu_strategy(gpus):
+    """--gpus N: the C++ adaptor's hydro_gpu_group path (all slabs on GPU 0
+    here via --device 0) reproduces the reference's checksum line."""
+    args = ["--case", "blast", "--nx", "96", "--ny", "80", "--steps", "12"]
+    cpu = run("run", *args, "--strategy", "coarse_grain", "--workers", "4")
+    gpu = run("run", *args, "--strategy", "gpu", "--gpus", str(gpus), "--device", "0")
+    assert cpu.returncode == 0 and gpu.returncode == 0, (cpu.stderr, gpu.stderr)
+    assert cpu.stdout.splitlines()[1] == gpu.stdout.splitlines()[1]
+
+
+@needs_bin
+@pytest.mark.gpu
 def test_gpu_positivity_error_line_matches_reference():
     args = ["--case", "blast", "--nx", "64", "--ny", "64", "--steps", "5", "--cfl", "25"]
     cpu = run("run", *args, "--strategy", "sequential")
