@@ -144,7 +144,8 @@ extern "C" {
 
 int hydro_gpu_group_create(const hydro_gpu_cfg* cfg, int n_gpus, const int* devices,
                            hydro_gpu_group** out) {
-  if (!cfg || !out || n_gpus < 1 || n_gpus > kMaxSlabs || cfg->nx < n_gpus)
+  // every slab needs the 2 rows its neighbours' halos take from it
+  if (!cfg || !out || n_gpus < 1 || n_gpus > kMaxSlabs || cfg->nx < 2 * n_gpus)
     return HYDRO_GPU_ERR_CONFIG;
   *out = nullptr;
   auto* g = new hydro_gpu_group();
