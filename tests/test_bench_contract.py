@@ -65,3 +65,26 @@ def test_multi_rank_bench_code_path(gpu):
     assert "peer-memory" in d["config"]["halo"]
     for key in ("roofline", "e2e", "gpu_launches", "clocks", "ms_per_step"):
         assert key in d, key
+
+
+@pytest.mark.gpu
+def test_single_gpu_bench_line_carries_the_contract_keys(gpu):
+    """The driver's default N=1 run: one JSON line with the base contract's
+    keys plus roofline, e2e (host buffers), clocks, gpu_launches and the
+    result digest of config 1 (the reference's e00cb4cfa888c325)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1",
+                          "--warmup", "1", "--no-variants", "--no-cpu-baseline"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+                "roofline", "e2e", "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["n_gpus"] == 1 and d["dtype"] == "f64" and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 1
+    assert d["result_digest"] == "e00cb4cfa888c325"
+    assert d["gpu_launches"] > 0
