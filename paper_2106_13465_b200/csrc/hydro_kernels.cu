@@ -83,8 +83,10 @@ extern __shared__ __align__(128) uint8_t hb_smem[];
 // -- and its flux.  The solver is a pure function of the two states, so an
 // interface whose states repeat the previous one's (uniform flow, where the
 // exact solver is as expensive as anywhere) takes the stored flux: the same
-// bits without the Newton/log/exp work.  Reset at every walk (pass), so a
-// hit never skips a range test the pass has not already folded in.
+// bits without the Newton/log/exp work.  An entry is reused only while it
+// is exact: within a pass (whose range tests it is folded into), and across
+// the thread's work items only after an exact pass or a fast pass that kept
+// every range (walk_strip's memo_valid hand-over).
 struct Memo {
   uint32_t at;  // hb_smem offset of this thread's field 0 (fields 1 KB apart)
   bool valid;
@@ -200,7 +202,7 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
   using Mem = std::conditional_t<FLUX == 1, Memo, NoMemo>;
   Mem memo{};
   if constexpr (FLUX == 1) memo.at = src.memo_at;
-  memo.valid = false;
+  memo.valid = src.memo_valid;
   Window w;
   auto none = [] { return Cons{}; };
   int f = to_prim(m, src.load(ka - 2), g, w.wA);
@@ -255,6 +257,10 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
     w.frPrev = o.fr;
     w.fluxPrev = o.F;
   }
+  // the memo carries over to this thread's next work item only if its
+  // entries are exact: written by an exact pass, or by a fast pass that kept
+  // every range (this lane's own flag -- masked lanes included)
+  src.memo_valid = memo.valid && (!M::kFast || m.ok);
   return m.ok;
 }
 
@@ -402,6 +408,7 @@ struct Tiles {
   uint32_t base;        // offset of this warp's kNBuf consecutive kChunkBytes buffers
   uint32_t full;        // offset of this warp's kNBuf mbarriers
   uint32_t memo_at;     // this thread's exact-10 interface memo (Memo)
+  bool memo_valid;      // the memo holds an exact entry (kept across work items)
   int lane;
   int s0;               // first strip of the item: column j0 (AXIS 0) or row i0 (AXIS 1)
   int ka, kb;           // output strip cells
@@ -556,6 +563,7 @@ __device__ __forceinline__ Tiles<AXIS> make_tiles(const CUtensorMap* load_map,
   t.base = pad + warp * (kNBuf * kChunkBytes);
   t.full = pad + 4 * kNBuf * kChunkBytes + warp * kNBuf * 8;
   t.memo_at = pad + 4 * kNBuf * kChunkBytes + 4 * kNBuf * 8 + threadIdx.x * 8;
+  t.memo_valid = false;
   t.lane = lane;
   t.q0 = 0;
   // SWIZZLE_32B (row sweep): within each 256-byte atom the 16-byte half of a
