@@ -324,7 +324,8 @@ def test_one_cell_perturbation_stays_inside_the_stencil(gpu):
 @pytest.mark.parametrize("n,case,bc,flux", [
     (2, "sod_x", "transmit", "hllc"), (3, "random", "transmit", "hllc"),
     (5, "corner_blast", "reflect", "hllc"), (4, "blast", "reflect", "hllc"),
-    (3, "random", "reflect", "exact10"),
+    (3, "random", "reflect", "exact10"), (8, "random", "transmit", "hllc"),
+    (8, "corner_blast", "reflect", "exact10"),
 ])
 def test_single_process_group_equals_one_domain(gpu, n, case, bc, flux):
     """hydro_gpu_group (one host thread, n row slabs, peer-memory halo,
