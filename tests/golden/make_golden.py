@@ -6,6 +6,8 @@ oracle/_ref/libhydro_ref.so by ``make -C oracle``):
     python tests/golden/make_golden.py            # golden.json (seconds)
     python tests/golden/make_golden.py --full     # golden_full.json (minutes)
     python tests/golden/make_golden.py --full --only cfg1_sod_x_2048_200_exact10  # ~15 min
+    python tests/golden/make_golden.py --full --only cfg2_random_8192_50_exact10 \
+        --out /tmp/cfg2.json     # ~1.5 h single-threaded; --out lets runs go in parallel
 
 Every digest here is produced by the reference's own run_sequential /
 run_coarse_grain (bitwise equal to each other, acceptance_tests.cpp:48-113)
