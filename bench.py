@@ -136,7 +136,8 @@ def best_cpu_strategy(threads: int) -> str:
     return _BEST_STRATEGY
 
 
-def cpu_reference_sample(steps_per_chunk: int, threads: int, min_seconds: float = 0.0):
+def cpu_reference_sample(steps_per_chunk: int, threads: int, min_seconds: float = 0.0,
+                         strategy: str | None = None):
     """Times the reference's own CPU path (oracle/_ref, its fastest parallel
     strategy over `threads` host threads) -- or the C port if the compiled
     reference is absent -- on chunks of `steps_per_chunk` time steps of the
@@ -148,7 +149,9 @@ def cpu_reference_sample(steps_per_chunk: int, threads: int, min_seconds: float 
     kind = "reference" if O.ref_available() else "port"
     strat = "sequential"
     if kind == "reference":
-        strat = best_cpu_strategy(threads)
+        strat = strategy or best_cpu_strategy(threads)
+        if strat == "sequential":
+            threads = 1
         O.ref_run(g.copy(), 1, BC, strat, threads)  # warm-up (bench.cpp:112-117)
     else:
         threads = 1
@@ -430,6 +433,12 @@ def main():
         cpu = {"value": v, "unit": UNIT, "cores": used, "kind": kind,
                "sample": f"{nsteps} time steps of the {NX}x{NY} {args.workload} grid ({secs:.1f}s timed), "
                          f"reference {strat} (its fastest strategy here) over {used} host threads"}
+        if kind == "reference":  # the paper's single-core starting point, run_sequential
+            v1, _, secs1, _, n1, _ = cpu_reference_sample(2, 1, min_seconds=3.0,
+                                                          strategy="sequential")
+            cpu["sequential_1core"] = {
+                "value": v1, "unit": UNIT, "cores": 1,
+                "sample": f"{n1} time steps, reference run_sequential ({secs1:.1f}s timed)"}
 
     # ---- the other flux of BASELINE's configs (exact Riemann, 10 Newton
     # iterations) on the same workload, same protocol, reported beside the
