@@ -14,7 +14,10 @@ the dt reduction per time step).  ``value`` is device-resident (state in HBM
 before the timed region, CUDA events on the launch stream, max over ranks);
 ``e2e`` goes through the C-ABI with pinned host buffers: upload, run, download
 every bench step.  An hllc run also measures the exact-10 flux mode (BASELINE's
-stated solver) on the same workload under ``flux_variants``.
+stated solver) on the same workload under ``flux_variants``, and a bitwise run
+the tolerance math mode (``--math tolerance``: compare_tolerance max_rel <=
+1e-12 instead of bit-identical) under ``math_variants``, with
+its measured max_rel against the bitwise result.
 ``--impl reference`` times the reference's own CPU
 implementation (oracle/_ref, its fastest strategy over all host threads) on a
 bounded sample of the same workload.
@@ -208,8 +211,10 @@ def main():
                     help="BASELINE config (default cfg1, the metric's config)")
     ap.add_argument("--flux", default="hllc", choices=["hllc", "exact10"],
                     help="interface flux (hllc = the reference hot path)")
+    ap.add_argument("--math", default="bitwise", choices=["bitwise", "tolerance"],
+                    help="sweep arithmetic (bitwise = the reference's bits)")
     ap.add_argument("--no-variants", action="store_true",
-                    help="skip the exact-10 flux sub-measurement of an hllc run")
+                    help="skip the exact-10 flux / tolerance-math sub-measurements")
     args = ap.parse_args()
     global NX, NY, TSTEPS, CASE, BC, SEED, SCALING
     CASE, NX, NY, BC, TSTEPS, SEED, SCALING = WORKLOADS[args.workload]
@@ -250,11 +255,11 @@ def main():
 
     geo = S.SlabGeometry(global_nx, NY, rank, world)
     if world == 1:
-        grid = P.GpuGrid(NX, NY, dx, dy, model, BC, device=local, flux=args.flux)
+        grid = P.GpuGrid(NX, NY, dx, dy, model, BC, device=local, flux=args.flux, math=args.math)
         grid.set_stream(stream.cuda_stream)
         slab = None
     else:
-        slab = S.GpuSlab(geo, dx, dy, model, BC, local, flux=args.flux)
+        slab = S.GpuSlab(geo, dx, dy, model, BC, local, flux=args.flux, math=args.math)
         slab.bind_stream(stream)
         grid = slab.grid
         comm = S.TorchComm()
@@ -361,7 +366,8 @@ def main():
     e2e_pipe = None
     if world == 1:
         streams = [stream, torch.cuda.Stream()]
-        grids = [grid, P.GpuGrid(NX, NY, dx, dy, model, BC, device=local, flux=args.flux)]
+        grids = [grid, P.GpuGrid(NX, NY, dx, dy, model, BC, device=local, flux=args.flux,
+                                 math=args.math)]
         grids[1].set_stream(streams[1].cuda_stream)
         outs = [host, torch.zeros_like(host0).pin_memory()]
         optrs = [[o[v].data_ptr() for v in range(4)] for o in outs]
@@ -415,7 +421,7 @@ def main():
     # instructions of that kernel per cell (ncu, config 1 / hllc only) over
     # 148 SMs x 64 FP64 lanes x the SM clock sampled during the timed region
     fp64 = None
-    if os.path.exists(prof) and args.workload == "cfg1" and args.flux == "hllc":
+    if os.path.exists(prof) and args.workload == "cfg1" and args.flux == "hllc" and args.math == "bitwise":
         per_cell = json.load(open(prof)).get(f"sweep_{which}_fp64_instr_per_cell")
         sms = torch.cuda.get_device_properties(local).multi_processor_count
         mhz = (clock_info or {}).get("sm_mhz") or 1965.0
@@ -440,18 +446,19 @@ def main():
                 "value": v1, "unit": UNIT, "cores": 1,
                 "sample": f"{n1} time steps, reference run_sequential ({secs1:.1f}s timed)"}
 
-    # ---- the other flux of BASELINE's configs (exact Riemann, 10 Newton
-    # iterations) on the same workload, same protocol, reported beside the
-    # hot-path line ---------------------------------------------------------
-    variants = None
-    if args.flux == "hllc" and not args.no_variants:
-        vflux = "exact10"
+    # ---- variants on the same workload, same protocol, reported beside the
+    # headline line: the other flux of BASELINE's configs (exact Riemann, 10
+    # Newton iterations) and the tolerance math mode ---------------------------
+    vhost = torch.zeros_like(host0).pin_memory()
+    vptrs = [vhost[v].data_ptr() for v in range(4)]
+
+    def variant(vflux, vmath):
         if world == 1:
-            vgrid = P.GpuGrid(NX, NY, dx, dy, model, BC, device=local, flux=vflux)
+            vgrid = P.GpuGrid(NX, NY, dx, dy, model, BC, device=local, flux=vflux, math=vmath)
             vgrid.set_stream(stream.cuda_stream)
             vslab = None
         else:
-            vslab = S.GpuSlab(geo, dx, dy, model, BC, local, flux=vflux)
+            vslab = S.GpuSlab(geo, dx, dy, model, BC, local, flux=vflux, math=vmath)
             vslab.bind_stream(stream)
             vgrid = vslab.grid
             comm.setup_p2p(vslab)
@@ -480,24 +487,45 @@ def main():
         for _ in range(vsteps):
             vgrid.upload_ptr(ptrs0, NY + 4)
             vrun()
-            vgrid.download_ptr(ptrs, NY + 4)
+            vgrid.download_ptr(vptrs, NY + 4)
         torch.cuda.synchronize()
         ve2e = time.perf_counter() - t0
         if dist is not None:
             t = torch.tensor([vms, ve2e], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             vms, ve2e = float(t[0].item()), float(t[1].item())
-        vdigest = (P.grid_digest(P.Grid2D(geo.nx, NY, dx, dy, host.numpy()))
-                   if world == 1 else None)
-        variants = {vflux: {
-            "value": cells * TSTEPS * vsteps / (vms / 1e3), "unit": UNIT,
-            "steps": vsteps, "warmup": args.warmup, "ms_per_step": vms / vsteps,
-            "e2e": {"value": cells * TSTEPS * vsteps / ve2e, "unit": UNIT,
-                    "h2d_bytes_per_step": plane_bytes, "d2h_bytes_per_step": plane_bytes},
-            "note": "BASELINE's stated solver: exact Riemann flux, 10 Newton iterations "
-                    "(DESIGN.md 3.4); bitwise equal to the oracle's restatement",
-            "result_digest": f"{vdigest:016x}" if vdigest is not None else None}}
         vgrid.close()
+        vdigest = (P.grid_digest(P.Grid2D(geo.nx, NY, dx, dy, vhost.numpy()))
+                   if world == 1 else None)
+        return {"value": cells * TSTEPS * vsteps / (vms / 1e3), "unit": UNIT,
+                "steps": vsteps, "warmup": args.warmup, "ms_per_step": vms / vsteps,
+                "e2e": {"value": cells * TSTEPS * vsteps / ve2e, "unit": UNIT,
+                        "h2d_bytes_per_step": plane_bytes, "d2h_bytes_per_step": plane_bytes},
+                "result_digest": f"{vdigest:016x}" if vdigest is not None else None}
+
+    variants = mvariants = None
+    if args.flux == "hllc" and not args.no_variants:
+        v = variant("exact10", args.math)
+        v["note"] = ("BASELINE's stated solver: exact Riemann flux, 10 Newton iterations "
+                     "(DESIGN.md 3.4)" + ("; bitwise equal to the oracle's restatement"
+                                          if args.math == "bitwise" else ""))
+        variants = {"exact10": v}
+    if args.math == "bitwise" and not args.no_variants:
+        v = variant(args.flux, "tolerance")
+        # the tolerance run's final state against the bitwise one (this rank's
+        # slab; the bitwise result carries the reference's digest)
+        a_np, b_np = host.numpy()[:, 2:geo.nx + 2, 2:NY + 2], vhost.numpy()[:, 2:geo.nx + 2, 2:NY + 2]
+        rel = float((np.abs(a_np - b_np) / np.maximum(np.maximum(np.abs(a_np), np.abs(b_np)), 1.0)).max())
+        if dist is not None:
+            t = torch.tensor([rel], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            rel = float(t.item())
+        v["max_rel_vs_bitwise"] = rel
+        v["tolerance"] = 1e-12
+        v["note"] = ("tolerance math mode (hydro_gpu_set_math, DESIGN.md 3.6): FMA contraction and "
+                     "uncorrected reciprocal quotients; compare_tolerance max_rel against the bitwise "
+                     "result of this run (the reference's state) <= 1e-12")
+        mvariants = {"tolerance": v}
 
     if rank == 0:
         line = {
@@ -513,7 +541,7 @@ def main():
                                  if comm.p2p else "nccl send/recv") if world > 1 else None),
                        "l2": "inputs larger than L2 (2 x %.0f MB state per GPU)"
                              % (4 * (geo.nx + 4) * (NY + 4) * 8 / 1e6),
-                       "flux": args.flux, "seed": SEED},
+                       "flux": args.flux, "math": args.math, "seed": SEED},
             "roofline": {"bound": "hbm", "kernel": f"sweep_{which}", "achieved": achieved,
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -529,6 +557,7 @@ def main():
             "cpu_baseline": cpu,
             "result_digest": f"{digest:016x}" if digest is not None else None,
             "flux_variants": variants,
+            "math_variants": mvariants,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -68,6 +68,14 @@ enum hydro_gpu_bc { HYDRO_GPU_BC_REFLECT = 0, HYDRO_GPU_BC_TRANSMIT = 1 };
  * is a Validation error, as in exact_riemann.cpp:55-57. */
 enum hydro_gpu_flux { HYDRO_GPU_FLUX_HLLC = 0, HYDRO_GPU_FLUX_EXACT10 = 1 };
 
+/* Arithmetic of the sweeps.  BITWISE (the default) reproduces the reference's
+ * -ffp-contract=off IEEE arithmetic bit for bit.  TOLERANCE is the
+ * north-star contract instead: compare_tolerance max_rel <= 1e-12 against the
+ * reference (proj/src/audit.cpp:146) -- FMA contraction and quotients as
+ * a * (1/b) with one refined reciprocal per denominator.
+ * Every branch, fallback and error check of the reference is kept. */
+enum hydro_gpu_math { HYDRO_GPU_MATH_BITWISE = 0, HYDRO_GPU_MATH_TOLERANCE = 1 };
+
 /* Case ids for the initialisers (cases.cpp:11-69 + BASELINE configs). */
 enum hydro_gpu_case {
   HYDRO_GPU_CASE_UNIFORM = 0,
@@ -243,6 +251,10 @@ int hydro_gpu_reset_counters(hydro_gpu_ctx* ctx);
 /* Launch-geometry override (0 = default): strip segment length along the
  * column and row sweeps; block must be 0 or 128. */
 int hydro_gpu_tune(hydro_gpu_ctx* ctx, int seg_x, int seg_y, int block);
+/* Selects the sweeps' arithmetic (enum hydro_gpu_math) for later runs of
+ * this context; no reference equivalent (the reference has one arithmetic).
+ * Config error for an unknown mode. */
+int hydro_gpu_set_math(hydro_gpu_ctx* ctx, int math);
 /* Self-test of the device fp64 division (op 0), square root (op 1),
  * signed-zero-safe division (op 2) and density division (op 4: zero
  * numerators, denominators inside the fast-pass envelope [2^-256, 2^256))

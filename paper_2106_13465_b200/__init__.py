@@ -7,7 +7,7 @@ reference's stepping interface (hydro.py) and the multi-GPU slab driver
 (slab.py).
 """
 from .hydro import (  # noqa: F401
-    BC, CASES, FLUX, ConfigError, DeviceError, ErrorCategory, GasModel, GpuGrid, GpuGroup, Grid2D, HydroError,
+    BC, CASES, FLUX, MATH, ConfigError, DeviceError, ErrorCategory, GasModel, GpuGrid, GpuGroup, Grid2D, HydroError,
     PositivityError, ValidationError, advance_gpu, compute_dt_gpu, grid_digest, make_case, run_gpu,
     run_until_gpu,
 )

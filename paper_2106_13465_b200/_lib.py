@@ -91,6 +91,7 @@ def lib() -> C.CDLL:
                                     P(C.c_longlong)], i),
         "hydro_gpu_reset_counters": ([_ctx], i),
         "hydro_gpu_tune": ([_ctx, i, i, i], i),
+        "hydro_gpu_set_math": ([_ctx, i], i),
         "hydro_gpu_state": ([_ctx, P(_dp), P(sz)], i),
         "hydro_gpu_math_selftest": ([i, _dp, _dp, _dp, _dp, P(i), sz], i),
         "hydro_grid_digest": ([_planes, sz, i, i], u64),

@@ -38,6 +38,8 @@ struct hydro_gpu_ctx {
   hydro_gpu_error last{};
   int seg_x = 0, seg_y = 0, block = 128;
   hb::Geometry geo{};
+  hb::Geometry geo_tol{};  // occupancy of the tolerance-mode sweeps
+  int math = HYDRO_GPU_MATH_BITWISE;
   hb::TmaMaps maps{};
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -228,7 +230,8 @@ void enqueue_x(hydro_gpu_ctx* c, int step, int explicit_dt, double dt) {
   a.dt_value = dt;
   cudaEvent_t e0{};
   ev_begin(c, &e0);
-  hb::launch_sweep_x(a, c->maps, c->geo, c->stream);
+  if (c->math == HYDRO_GPU_MATH_TOLERANCE) hb::launch_sweep_x_tol(a, c->maps, c->geo_tol, c->stream);
+  else hb::launch_sweep_x(a, c->maps, c->geo, c->stream);
   ev_end(c, e0, 0);
 }
 
@@ -239,7 +242,8 @@ void enqueue_y(hydro_gpu_ctx* c, int step, int explicit_dt, double dt, int want_
   a.want_limit = want_limit;
   cudaEvent_t e0{};
   ev_begin(c, &e0);
-  hb::launch_sweep_y(a, c->maps, c->geo, c->stream);
+  if (c->math == HYDRO_GPU_MATH_TOLERANCE) hb::launch_sweep_y_tol(a, c->maps, c->geo_tol, c->stream);
+  else hb::launch_sweep_y(a, c->maps, c->geo, c->stream);
   ev_end(c, e0, 1);
 }
 
@@ -483,7 +487,7 @@ int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out) {
     return HYDRO_GPU_ERR_CUDA;
   }
   ctx->stream = ctx->own_stream;
-  if (hb::query_geometry(&ctx->geo) != 0 ||
+  if (hb::query_geometry(&ctx->geo) != 0 || hb::query_geometry_tol(&ctx->geo_tol) != 0 ||
       !hb::make_tma_maps(&ctx->maps, ctx->A, ctx->B, ctx->pitch, c.nx, c.ny)) {
     hydro_gpu_destroy(ctx);
     cudaGetLastError();
@@ -896,6 +900,15 @@ int hydro_gpu_tune(hydro_gpu_ctx* c, int seg_x, int seg_y, int block) {
   c->seg_x = seg_x;
   c->seg_y = seg_y;
   drop_graphs(c);  // launch geometry is baked into captured graphs
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_set_math(hydro_gpu_ctx* c, int math) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  if (math != HYDRO_GPU_MATH_BITWISE && math != HYDRO_GPU_MATH_TOLERANCE)
+    return set_err(c, HYDRO_GPU_ERR_CONFIG, "unknown math mode");
+  if (math != c->math) drop_graphs(c);  // the sweep kernels are baked into captured graphs
+  c->math = math;
   return HYDRO_GPU_OK;
 }
 

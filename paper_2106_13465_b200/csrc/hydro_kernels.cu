@@ -32,6 +32,15 @@
 #include "hydro_exact.cuh"
 #include "hydro_kernels.cuh"
 
+// The same sweeps are compiled a second time by hydro_kernels_tol.cu with
+// HB_TOLERANCE (tolerance math mode): only the sweep kernels
+// and their launchers, exported with a _tol suffix.
+#ifdef HB_TOLERANCE
+#define HB_SWEEP(name) name##_tol
+#else
+#define HB_SWEEP(name) name
+#endif
+
 namespace hb {
 
 namespace {
@@ -800,6 +809,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : HB_EX_MINB) sweep
   }
 }
 
+#ifndef HB_TOLERANCE
 // ---------------------------------------------------------------------------
 // Start-of-run pass: apply_boundary on the physical walls of the current
 // state and compute_dt's min-reduction for the first step.
@@ -1014,6 +1024,8 @@ __global__ void math_selftest_kernel(int op, const double* a, const double* b, d
   okv[t] = fm.ok ? 1 : 0;
 }
 
+#endif  // !HB_TOLERANCE
+
 // Segment length for the persistent sweeps: about kItemsPerWarp work items
 // per resident warp (dynamic balance), 16..128 cells, whole row-sweep chunks.
 constexpr int kItemsPerWarp = 8;
@@ -1037,7 +1049,7 @@ int pick_seg(int n, int strips, int warps) {
 
 }  // namespace
 
-int query_geometry(Geometry* g) {
+int HB_SWEEP(query_geometry)(Geometry* g) {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1059,6 +1071,7 @@ int query_geometry(Geometry* g) {
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
+#ifndef HB_TOLERANCE
 bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, int ny) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
@@ -1100,6 +1113,9 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
          enc(&maps->x_load, A, dim_load, box_x, sx) && enc(&maps->x_store, B, dim_xstore, box_x, sx);
 }
 
+#endif  // !HB_TOLERANCE
+
+namespace {
 template <class... KArgs, class... Args>
 void launch_sweep(void (*kernel)(KArgs...), int ctas, int smem, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg{};
@@ -1114,8 +1130,9 @@ void launch_sweep(void (*kernel)(KArgs...), int ctas, int smem, cudaStream_t s, 
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kernel, args...);
 }
+}  // namespace
 
-void launch_sweep_x(const SweepArgs& a0, const TmaMaps& maps, const Geometry& geo,
+void HB_SWEEP(launch_sweep_x)(const SweepArgs& a0, const TmaMaps& maps, const Geometry& geo,
                     cudaStream_t s) {
   SweepArgs a = a0;
   const int ctas = geo.sms * (a.flux == 1 ? geo.ctas_x_exact : geo.ctas_x_per_sm);
@@ -1128,7 +1145,7 @@ void launch_sweep_x(const SweepArgs& a0, const TmaMaps& maps, const Geometry& ge
     launch_sweep(sweep_x_tma_kernel<0>, ctas, kYSmemBytes, s, a, maps.x_load, maps.x_store);
 }
 
-void launch_sweep_y(const SweepArgs& a0, const TmaMaps& maps, const Geometry& geo,
+void HB_SWEEP(launch_sweep_y)(const SweepArgs& a0, const TmaMaps& maps, const Geometry& geo,
                     cudaStream_t s) {
   SweepArgs a = a0;
   const int ctas = geo.sms * (a.flux == 1 ? geo.ctas_y_exact : geo.ctas_y_per_sm);
@@ -1145,6 +1162,7 @@ void launch_sweep_y(const SweepArgs& a0, const TmaMaps& maps, const Geometry& ge
   }
 }
 
+#ifndef HB_TOLERANCE
 void launch_prologue(const PrologueArgs& a, cudaStream_t s) {
   // each thread walks ~nx/128 rows of its column: few enough warps that the
   // per-warp atomicMin of the dt limit does not serialise on one address
@@ -1172,5 +1190,7 @@ void launch_math_selftest(int op, const double* a, const double* b, double* fast
                           int* ok, size_t n, cudaStream_t s) {
   math_selftest_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(op, a, b, fast, ref, ok, n);
 }
+
+#endif  // !HB_TOLERANCE
 
 }  // namespace hb

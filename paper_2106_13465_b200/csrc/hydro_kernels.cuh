@@ -116,6 +116,11 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
 int query_geometry(Geometry* g);
 void launch_sweep_x(const SweepArgs& a, const TmaMaps& maps, const Geometry& geo, cudaStream_t s);
 void launch_sweep_y(const SweepArgs& a, const TmaMaps& maps, const Geometry& geo, cudaStream_t s);
+// Tolerance math mode (hydro_kernels_tol.cu): the same sweeps
+// built with FMA contraction and uncorrected reciprocal quotients.
+int query_geometry_tol(Geometry* g);
+void launch_sweep_x_tol(const SweepArgs& a, const TmaMaps& maps, const Geometry& geo, cudaStream_t s);
+void launch_sweep_y_tol(const SweepArgs& a, const TmaMaps& maps, const Geometry& geo, cudaStream_t s);
 void launch_prologue(const PrologueArgs& a, cudaStream_t s);
 void launch_finish(const FinishArgs& a, cudaStream_t s);
 void launch_init(const InitArgs& a, cudaStream_t s);

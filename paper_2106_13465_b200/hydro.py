@@ -109,6 +109,9 @@ class GasModel:
 
 BC = {"reflect": 0, "transmit": 1}
 FLUX = {"hllc": 0, "exact10": 1}
+# Sweep arithmetic (include/hydro_gpu.h, enum hydro_gpu_math): "bitwise" is the
+# reference's bits; "tolerance" holds compare_tolerance max_rel <= 1e-12.
+MATH = {"bitwise": 0, "tolerance": 1}
 CASES = {"uniform": 0, "blast": 1, "sod": 2, "corner_blast": 3, "sod_x": 4, "random": 5}
 RHO, MOM_X, MOM_Y, ENER = 0, 1, 2, 3
 
@@ -178,7 +181,8 @@ class GpuGrid:
 
     def __init__(self, nx: int, ny: int, dx: float, dy: float, model: GasModel = GasModel(),
                  bc: str = "reflect", device: int = -1, row0: int = 0, global_nx: int | None = None,
-                 wall_lo: bool = True, wall_hi: bool = True, flux: str = "hllc"):
+                 wall_lo: bool = True, wall_hi: bool = True, flux: str = "hllc",
+                 math: str = "bitwise"):
         if bc not in BC:
             raise ConfigError(f"unknown boundary '{bc}' (expected reflect or transmit)")
         if flux not in FLUX:
@@ -196,6 +200,9 @@ class GpuGrid:
         if rc:
             _raise_for(rc, message=f"hydro_gpu_create failed ({self._lib.hydro_gpu_status_string(rc).decode()}) "
                                    f"for a {nx}x{ny} grid")
+        self.math = "bitwise"
+        if math != "bitwise":
+            self.set_math(math)
 
     # -- lifetime ---------------------------------------------------------
     def close(self):
@@ -387,6 +394,13 @@ class GpuGrid:
     def tune(self, seg_x: int = 0, seg_y: int = 0, block: int = 0):
         self._check(self._lib.hydro_gpu_tune(self._ctx, seg_x, seg_y, block))
 
+    def set_math(self, math: str):
+        """hydro_gpu_set_math: "bitwise" (default) or "tolerance"."""
+        if math not in MATH:
+            raise ConfigError(f"unknown math mode '{math}' (expected bitwise or tolerance)")
+        self._check(self._lib.hydro_gpu_set_math(self._ctx, MATH[math]))
+        self.math = math
+
     def state(self) -> tuple[int, int]:
         p = L._dp()
         pitch = C.c_size_t()
@@ -465,16 +479,17 @@ class GpuGroup:
         return last.value
 
 
-def _context_for(grid: Grid2D, model: GasModel, bc: str, flux: str = "hllc") -> GpuGrid:
-    g = GpuGrid(grid.nx, grid.ny, grid.dx, grid.dy, model, bc, flux=flux)
+def _context_for(grid: Grid2D, model: GasModel, bc: str, flux: str = "hllc",
+                 math: str = "bitwise") -> GpuGrid:
+    g = GpuGrid(grid.nx, grid.ny, grid.dx, grid.dy, model, bc, flux=flux, math=math)
     g.upload(grid.planes)
     return g
 
 
 def run_gpu(grid: Grid2D, model: GasModel = GasModel(), steps: int = 1, bc: str = "reflect",
-            flux: str = "hllc") -> float:
+            flux: str = "hllc", math: str = "bitwise") -> float:
     """run_sequential(grid, model, steps) on the GPU, in place; returns the last dt."""
-    with _context_for(grid, model, bc, flux) as g:
+    with _context_for(grid, model, bc, flux, math) as g:
         try:
             last = g.run(steps)
         finally:

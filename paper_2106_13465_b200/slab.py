@@ -93,12 +93,12 @@ class GpuSlab:
     """One rank's slab, resident on one GPU (a hydro_gpu_ctx in slab mode)."""
 
     def __init__(self, geo: SlabGeometry, dx: float, dy: float, model: GasModel, bc: str,
-                 device: int, flux: str = "hllc"):
+                 device: int, flux: str = "hllc", math: str = "bitwise"):
         self.geo = geo
         self.device = torch.device("cuda", device)
         self.grid = GpuGrid(geo.nx, geo.ny, dx, dy, model, bc, device=device, row0=geo.row0,
                             global_nx=geo.global_nx, wall_lo=geo.wall_lo, wall_hi=geo.wall_hi,
-                            flux=flux)
+                            flux=flux, math=math)
         h = self.grid.halo()
         n = h["count"]
         self._halo = {k: device_tensor(h[k], n, device=self.device)

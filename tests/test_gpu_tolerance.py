@@ -1,0 +1,124 @@
+"""Tolerance math mode (hydro_gpu_set_math(HYDRO_GPU_MATH_TOLERANCE)).
+
+Bar: the north-star contract, compare_tolerance (proj/src/audit.cpp:137-154)
+max|a-b| / max(|a|,|b|,1) <= 1e-12 on the interior after N steps, against
+the C oracle at oracle-sized grids and, at BASELINE's full sizes, against the
+bitwise mode's result, whose digest is pinned to the reference's by
+tests/golden/golden_full.json (so it is the reference's state).  The dt of
+the last step is held to the same relative bound.  Errors keep the
+reference's category and message (the fast pass redoes a failing item with
+the exact arithmetic).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2106_13465_b200 as P
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN_FULL = json.load(open(os.path.join(HERE, "golden", "golden_full.json")))
+MODEL = P.GasModel()
+
+
+def max_rel(a: np.ndarray, b: np.ndarray) -> float:
+    """compare_tolerance's floored relative difference (audit.cpp:146)."""
+    return float((np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), 1.0)).max())
+
+
+def gpu_run(case, nx, ny, steps, bc, seed=0, flux="hllc", math="tolerance"):
+    grid = P.make_case(case, nx, ny, MODEL, seed=seed)
+    with P.GpuGrid(grid.nx, grid.ny, grid.dx, grid.dy, MODEL, bc, device=0, flux=flux,
+                   math=math) as g:
+        g.upload(grid.planes)
+        dt = g.run(steps)
+        g.download(grid.planes)
+    return grid, dt
+
+
+@pytest.mark.parametrize("flux", ["hllc", "exact10"])
+@pytest.mark.parametrize("case,nx,ny,steps,bc,seed", [
+    ("corner_blast", 256, 256, 100, "reflect", 0),   # BASELINE config 0
+    ("sod_x", 192, 160, 60, "transmit", 0),
+    ("random", 160, 224, 30, "transmit", 5),
+    ("random", 97, 65, 20, "reflect", 6),
+    ("blast", 37, 53, 9, "reflect", 0),
+])
+def test_tolerance_mode_within_1e12_of_oracle(gpu, flux, case, nx, ny, steps, bc, seed):
+    grid, dt = gpu_run(case, nx, ny, steps, bc, seed, flux)
+    ref = O.make_case(case, nx, ny, seed=seed)
+    with O.flux_mode(flux):
+        dt_ref = O.run_sequential(ref, steps, bc)
+    got, want = grid.interior(), ref.u[:, 2:nx + 2, 2:ny + 2]
+    mx, _ = O.compare_tolerance(O.Grid(nx, ny, grid.dx, grid.dy, grid.planes.copy()), ref)
+    assert mx <= TOL and max_rel(got, want) <= TOL, (mx, max_rel(got, want))
+    assert abs(dt - dt_ref) <= TOL * max(abs(dt), abs(dt_ref))
+
+
+@pytest.mark.parametrize("name", ["cfg1_sod_x_2048_200", "cfg1_sod_x_2048_200_exact10",
+                                  "random_1024_20_exact10"])
+def test_tolerance_mode_full_size(gpu, name):
+    """Full-size BASELINE workloads: the tolerance state against the bitwise
+    state, itself checked against the reference's digest."""
+    rec = GOLDEN_FULL[name]
+    nx, ny = rec["nx"], rec["ny"]
+    out = {}
+    for math in ("bitwise", "tolerance"):
+        planes = np.empty((4, nx + 4, ny + 4))
+        with P.GpuGrid(nx, ny, 1.0 / nx, 1.0 / ny, MODEL, rec["bc"], device=0,
+                       flux=rec.get("flux", "hllc"), math=math) as g:
+            g.init_case(rec["case"], rec["seed"])
+            dt = g.run(rec["steps"])
+            g.download(planes)
+        out[math] = (planes, dt)
+    exact = P.Grid2D(nx, ny, 1.0 / nx, 1.0 / ny, out["bitwise"][0])
+    assert f"{P.grid_digest(exact):016x}" == rec["digest"]
+    a, b = out["bitwise"][0][:, 2:nx + 2, 2:ny + 2], out["tolerance"][0][:, 2:nx + 2, 2:ny + 2]
+    assert max_rel(a, b) <= TOL
+    assert not np.array_equal(a, b), "tolerance mode ran the bitwise kernels"
+    assert abs(out["bitwise"][1] - out["tolerance"][1]) <= TOL * out["bitwise"][1]
+
+
+def test_mode_switch_on_one_context(gpu):
+    """set_math between runs re-captures the step graph: bitwise -> tolerance
+    -> bitwise on one context, the last run bitwise the oracle's."""
+    grid = P.make_case("random", 96, 80, MODEL, seed=12)
+    ref = O.make_case("random", 96, 80, seed=12)
+    with P.GpuGrid(96, 80, grid.dx, grid.dy, MODEL, "transmit", device=0) as g:
+        g.upload(grid.planes)
+        g.run(4)
+        g.set_math("tolerance")
+        g.run(4)
+        g.set_math("bitwise")
+        g.upload(grid.planes)
+        g.run(8)
+        g.download(grid.planes)
+    O.run_sequential(ref, 8, "transmit")
+    assert np.array_equal(grid.planes, ref.u)
+
+
+def test_tolerance_mode_positivity_error_matches_reference(gpu):
+    """The CFL=25 fault injection of test_schedulers.cpp:115-128 fails with the
+    reference's category and exact message in tolerance mode too."""
+    model = P.GasModel(cfl=25.0)
+    grid = P.make_case("blast", 64, 64, model)
+    ref = O.make_case("blast", 64, 64)
+    with pytest.raises(O.CheckerError) as e_ref:
+        O.run_sequential(ref, 5, "reflect", cfl=25.0)
+    with pytest.raises(P.PositivityError) as e_gpu:
+        P.run_gpu(grid, model, 5, "reflect", math="tolerance")
+    assert e_gpu.value.category == P.ErrorCategory.POSITIVITY
+    assert str(e_gpu.value) == str(e_ref.value)
+
+
+def test_unknown_math_mode_is_a_config_error(gpu):
+    with P.GpuGrid(16, 16, 1 / 16, 1 / 16, MODEL, "reflect", device=0) as g:
+        with pytest.raises(P.ConfigError):
+            g.set_math("fast")
+        rc = g._lib.hydro_gpu_set_math(g._ctx, 7)
+        assert rc == 1
