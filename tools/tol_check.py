@@ -1,7 +1,8 @@
 """Tolerance of a non-bitwise build against the bitwise one (experiment tool).
 
-    python tools/tol_check.py base.so other.so [...] -- runs each library in its
-    own process on the same cases, then prints compare_tolerance's max_rel
+    python tools/tol_check.py base.so other.so[:tolerance] [...] -- runs each
+    library (optionally in a math mode) in its own process on the same cases,
+    then prints compare_tolerance's max_rel
     (scale max(|a|,|b|,1), proj/src/audit.cpp:146) of every library's final
     interior against the first one's, plus event-timed sweep ms.
 """
@@ -18,9 +19,9 @@ CASES = [("sod_x", 2048, 200, "transmit", 0), ("random", 2048, 100, "transmit", 
 if len(sys.argv) > 2 and sys.argv[1] == "--run":
     sys.path.insert(0, ROOT)
     import paper_2106_13465_b200 as P
-    out = sys.argv[2]
+    out, math = sys.argv[2], sys.argv[3]
     for case, n, steps, bc, seed in CASES:
-        with P.GpuGrid(n, n, 1.0 / n, 1.0 / n, P.GasModel(), bc, device=0) as g:
+        with P.GpuGrid(n, n, 1.0 / n, 1.0 / n, P.GasModel(), bc, device=0, math=math) as g:
             g.init_case(case, seed)
             g.run(3)
             g.set_timing(True)
@@ -33,11 +34,12 @@ if len(sys.argv) > 2 and sys.argv[1] == "--run":
     sys.exit(0)
 
 libs = sys.argv[1:]
-for k, lib in enumerate(libs):
+for k, spec in enumerate(libs):
+    lib, _, math = spec.partition(":")
     env = dict(os.environ, HYDRO_B200_LIB=os.path.abspath(lib))
-    r = subprocess.run([sys.executable, __file__, "--run", f"/tmp/tol_{k}"], env=env,
+    r = subprocess.run([sys.executable, __file__, "--run", f"/tmp/tol_{k}", math or "bitwise"], env=env,
                        capture_output=True, text=True)
-    print(os.path.basename(lib), r.stdout.strip().replace("\n", " | "), r.stderr[-300:] if r.returncode else "")
+    print(os.path.basename(spec), r.stdout.strip().replace("\n", " | "), r.stderr[-300:] if r.returncode else "")
     if k:
         for case, *_ in CASES:
             a = np.load(f"/tmp/tol_0_{case}.npy")
