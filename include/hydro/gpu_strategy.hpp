@@ -42,6 +42,7 @@ struct GpuOptions {
                                       // all on `device` if it is >= 0
   int bc = HYDRO_GPU_BC_REFLECT;      // the reference's walls; TRANSMIT for BASELINE configs
   int flux = HYDRO_GPU_FLUX_HLLC;     // the reference hot path; EXACT10 = BASELINE's solver
+  int math = HYDRO_GPU_MATH_BITWISE;  // the reference's bits; TOLERANCE = max_rel <= 1e-12
 };
 
 namespace gpu_detail {
@@ -75,6 +76,11 @@ class Context {
     const int rc = hydro_gpu_create(&cfg, &ctx_);
     if (rc != HYDRO_GPU_OK)
       raise(rc, std::string("hydro_gpu_create: ") + hydro_gpu_status_string(rc));
+    const int mrc = o.math == HYDRO_GPU_MATH_BITWISE ? HYDRO_GPU_OK : hydro_gpu_set_math(ctx_, o.math);
+    if (mrc != HYDRO_GPU_OK) {
+      hydro_gpu_destroy(ctx_);
+      raise(mrc, "hydro_gpu_set_math: unknown math mode");
+    }
   }
   ~Context() { hydro_gpu_destroy(ctx_); }
   Context(const Context&) = delete;
@@ -132,6 +138,8 @@ inline double run_gpu_slabs(Grid2D& grid, const GasModel& model, int steps,
     hydro_gpu_group_destroy(g);
     gpu_detail::raise(status, e.message);
   };
+  if (opt.math != HYDRO_GPU_MATH_BITWISE && (rc = hydro_gpu_group_set_math(g, opt.math)) != HYDRO_GPU_OK)
+    fail(rc);
   const double* in[4];
   double* out[4];
   for (int v = 0; v < kNumVars; ++v) {

@@ -236,6 +236,8 @@ int hydro_gpu_group_upload(hydro_gpu_group* group, const double* const planes[4]
 int hydro_gpu_group_download(hydro_gpu_group* group, double* const planes[4],
                              size_t row_stride);
 int hydro_gpu_group_init_case(hydro_gpu_group* group, int case_id, uint64_t seed);
+/* hydro_gpu_set_math on every slab. */
+int hydro_gpu_group_set_math(hydro_gpu_group* group, int math);
 /* run_sequential over all slabs; *last_dt as hydro_gpu_run. */
 int hydro_gpu_group_run(hydro_gpu_group* group, int steps, double* last_dt);
 

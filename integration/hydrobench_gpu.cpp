@@ -10,7 +10,7 @@
 //   hydrobench_gpu run --case blast --nx 48 --ny 48 --steps 5 --strategy gpu
 //   hydrobench_gpu bench --case blast --nx 2048 --ny 2048 --steps 10 --strategy gpu
 //   extra: --case corner_blast|sod_x|random (BASELINE configs), --bc reflect|transmit,
-//          --flux hllc|exact10 (gpu strategy), --gpus N (row slabs on GPUs 0..N-1,
+//          --flux hllc|exact10 and --math bitwise|tolerance (gpu strategy), --gpus N (row slabs on GPUs 0..N-1,
 //          one host thread; with --device D all N slabs share GPU D),
 //          --seed N (random field), --device N
 #include <chrono>
@@ -33,6 +33,7 @@ struct Args {
   std::string command;
   std::string bc = "reflect";
   std::string flux = "hllc";
+  std::string math = "bitwise";
   int device = -1;
   int gpus = 1;
 };
@@ -58,6 +59,7 @@ Args parse(int argc, char** argv) {
     else if (key == "--output") c.output = val;
     else if (key == "--bc") a.bc = val;
     else if (key == "--flux") a.flux = val;
+    else if (key == "--math") a.math = val;
     else if (key == "--gpus") a.gpus = std::stoi(val);
     else if (key == "--device") a.device = std::stoi(val);
     else throw hydro::ConfigError("unknown option " + key);
@@ -95,6 +97,9 @@ void step(hydro::Grid2D& grid, const Args& a, int steps) {
     if (a.flux != "hllc" && a.flux != "exact10")
       throw hydro::ConfigError("unknown flux '" + a.flux + "'");
     opt.flux = a.flux == "exact10" ? HYDRO_GPU_FLUX_EXACT10 : HYDRO_GPU_FLUX_HLLC;
+    if (a.math != "bitwise" && a.math != "tolerance")
+      throw hydro::ConfigError("unknown math mode '" + a.math + "'");
+    opt.math = a.math == "tolerance" ? HYDRO_GPU_MATH_TOLERANCE : HYDRO_GPU_MATH_BITWISE;
     if (a.gpus < 1) throw hydro::ConfigError("--gpus must be at least 1");
     opt.gpus = a.gpus;
     hydro::run_gpu(grid, hydro::GasModel{c.gamma, c.cfl}, steps, opt);
@@ -103,6 +108,8 @@ void step(hydro::Grid2D& grid, const Args& a, int steps) {
       throw hydro::ConfigError("the CPU strategies only have reflective walls");
     if (a.flux != "hllc")
       throw hydro::ConfigError("the CPU strategies only have the HLLC flux");
+    if (a.math != "bitwise")
+      throw hydro::ConfigError("the CPU strategies only have the reference's arithmetic");
     hydro::run_strategy(grid, c, c.workers[0]);
   }
 }

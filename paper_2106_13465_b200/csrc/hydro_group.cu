@@ -301,6 +301,15 @@ int hydro_gpu_group_download(hydro_gpu_group* g, double* const planes[4], size_t
   return HYDRO_GPU_OK;
 }
 
+int hydro_gpu_group_set_math(hydro_gpu_group* g, int math) {
+  if (!g) return HYDRO_GPU_ERR_CONFIG;
+  for (int k = 0; k < g->n; ++k) {
+    const int rc = hydro_gpu_set_math(g->ctx[k], math);
+    if (rc) return slab_rc(g, k, rc);
+  }
+  return HYDRO_GPU_OK;
+}
+
 int hydro_gpu_group_init_case(hydro_gpu_group* g, int case_id, uint64_t seed) {
   if (!g) return HYDRO_GPU_ERR_CONFIG;
   for (int k = 0; k < g->n; ++k) {

@@ -105,3 +105,31 @@ def test_gpu_strategy_exact10_flux_equals_oracle():
         O.run_sequential(ref, 12, "transmit")
     assert digest == f"{O.digest(ref):016x}"
     assert np.isfinite(ref.u).all()
+
+
+@needs_bin
+def test_cpu_strategies_reject_the_tolerance_math():
+    out = run("run", "--case", "blast", "--nx", "32", "--ny", "32", "--steps", "1",
+              "--strategy", "sequential", "--math", "tolerance")
+    assert out.returncode == 1
+    assert out.stderr.startswith("error: config: the CPU strategies only have the reference's arithmetic")
+
+
+@needs_bin
+@pytest.mark.gpu
+@pytest.mark.parametrize("gpus", [1, 2])
+def test_gpu_strategy_tolerance_math_totals(gpus):
+    """--math tolerance through the C++ adaptor (GpuOptions::math, one context
+    or a 2-slab group on GPU 0): the checksum line's conserved totals are the
+    reference's within 1e-12 (relative, floored at 1)."""
+    args = ["run", "--case", "blast", "--nx", "48", "--ny", "48", "--steps", "5"]
+    ref = run(*args, "--strategy", "sequential")
+    tol = run(*args, "--strategy", "gpu", "--math", "tolerance", "--gpus", str(gpus), "--device", "0")
+    assert ref.returncode == 0 and tol.returncode == 0, tol.stderr
+
+    def totals(out):
+        fields = out.stdout.splitlines()[1].split()[2:]
+        return [float(f.split("=")[1]) for f in fields]
+
+    for a, b in zip(totals(ref), totals(tol)):
+        assert abs(a - b) <= 1e-12 * max(abs(a), abs(b), 1.0)

@@ -21,9 +21,11 @@ ap.add_argument("--seed", type=int, default=0)
 ap.add_argument("--seg", type=int, nargs=3, default=[0, 0, 0])
 ap.add_argument("--pre", type=int, default=2, help="untimed steps before the timed ones")
 ap.add_argument("--flux", default="hllc")
+ap.add_argument("--math", default="bitwise")
 a = ap.parse_args()
 ny = a.ny or a.nx
-with P.GpuGrid(a.nx, ny, 1.0 / a.nx, 1.0 / ny, P.GasModel(), a.bc, device=0, flux=a.flux) as g:
+with P.GpuGrid(a.nx, ny, 1.0 / a.nx, 1.0 / ny, P.GasModel(), a.bc, device=0, flux=a.flux,
+               math=a.math) as g:
     g.tune(*a.seg)
     g.init_case(a.case, a.seed)
     g.run(a.pre)  # warm-up / advance the flow: init, prologue, sweeps, finish
