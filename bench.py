@@ -200,6 +200,17 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def max_rel(a, b, rows: int = 1024) -> float:
+    """compare_tolerance's max |a-b| / max(|a|,|b|,1) (proj/src/audit.cpp:146)
+    over (4, nx, ny) planes, in row blocks to bound host memory."""
+    import numpy as np
+    out = 0.0
+    for i in range(0, a.shape[1], rows):
+        x, y = a[:, i:i + rows], b[:, i:i + rows]
+        out = max(out, float((np.abs(x - y) / np.maximum(np.maximum(np.abs(x), np.abs(y)), 1.0)).max()))
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -510,12 +521,13 @@ def main():
                      "(DESIGN.md 3.4)" + ("; bitwise equal to the oracle's restatement"
                                           if args.math == "bitwise" else ""))
         variants = {"exact10": v}
+        # kept for the tolerance/exact-10 comparison below (small grids only)
+        ex_state = vhost.numpy()[:, 2:geo.nx + 2, 2:NY + 2].copy() if geo.nx * NY <= (1 << 26) else None
     if args.math == "bitwise" and not args.no_variants:
         v = variant(args.flux, "tolerance")
         # the tolerance run's final state against the bitwise one (this rank's
         # slab; the bitwise result carries the reference's digest)
-        a_np, b_np = host.numpy()[:, 2:geo.nx + 2, 2:NY + 2], vhost.numpy()[:, 2:geo.nx + 2, 2:NY + 2]
-        rel = float((np.abs(a_np - b_np) / np.maximum(np.maximum(np.abs(a_np), np.abs(b_np)), 1.0)).max())
+        rel = max_rel(host.numpy()[:, 2:geo.nx + 2, 2:NY + 2], vhost.numpy()[:, 2:geo.nx + 2, 2:NY + 2])
         if dist is not None:
             t = torch.tensor([rel], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -526,6 +538,12 @@ def main():
                      "uncorrected reciprocal quotients; compare_tolerance max_rel against the bitwise "
                      "result of this run (the reference's state) <= 1e-12")
         mvariants = {"tolerance": v}
+        if args.flux == "hllc" and variants:
+            v = variant("exact10", "tolerance")
+            v["note"] = "tolerance math mode with the exact-10 flux (DESIGN.md 3.6)"
+            if ex_state is not None and world == 1:
+                v["max_rel_vs_bitwise"] = max_rel(ex_state, vhost.numpy()[:, 2:geo.nx + 2, 2:NY + 2])
+            mvariants["tolerance_exact10"] = v
 
     if rank == 0:
         line = {
