@@ -253,14 +253,28 @@ __device__ __forceinline__ bool sample0(M& m, const Face& fl, const Face& fr, co
         dfB = root * (1.0 - m.divn(0.5 * (p - hi.p), d));
       } else {
         low();
-        const double l = log_(m, m.divn(p, khi.rp));
+        const double x = m.divn(p, khi.rp);
+        const double l = log_(m, x);
+#ifdef HB_TOLERANCE
+        // tolerance mode: x^(z-1) = x^z / x, one exp fewer per step
+        const double xz = exp_(m, k.z * l);
+        fB = khi.cf * (xz - 1.0);
+        dfB = khi.dn * m.divnf(xz, x);
+#else
         fB = khi.cf * (exp_(m, k.z * l) - 1.0);
         dfB = khi.dn * exp_(m, k.zn * l);
+#endif
       }
       const double f = fA + fB + du;  // = f_L + f_R + du
       const double df = dfA + dfB;
       double next = p - m.divf(f, df);
       if (next < p_min) next = p_min;
+#ifdef HB_TOLERANCE
+      // tolerance mode: a Newton step below 2^-26 relative leaves an error
+      // of order its square, under one ulp -- stop there instead of at the
+      // rounding cycle the bitwise mode waits for
+      if (fabs(next - p) <= 0x1p-26 * next) { p = next; break; }
+#endif
       // p_10 = p_{j-T+((10-j) mod T)}; p_j itself equals p_{j-T}
       if (next == p) break;
       if (next == p1) { p = ((10 - j) & 1) ? p : next; break; }
