@@ -88,3 +88,22 @@ def test_single_gpu_bench_line_carries_the_contract_keys(gpu):
     assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 1
     assert d["result_digest"] == "e00cb4cfa888c325"
     assert d["gpu_launches"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_variants_tolerance_within_bound(gpu):
+    """The variants of a default run: exact-10 keeps the oracle's digest of
+    config 1 (tests/golden/golden_full.json), and the tolerance math mode's
+    measured max_rel against the bitwise state is within 1e-12 for both
+    fluxes."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1",
+                          "--warmup", "1", "--no-cpu-baseline"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([l for l in out.stdout.splitlines() if l.strip().startswith("{")][0])
+    assert d["config"]["math"] == "bitwise"
+    assert d["flux_variants"]["exact10"]["result_digest"] == "5bba80ba4684d325"
+    for name in ("tolerance", "tolerance_exact10"):
+        v = d["math_variants"][name]
+        assert v["value"] > 0 and v["e2e"]["value"] > 0
+        assert 0 < v["max_rel_vs_bitwise"] <= 1e-12, (name, v["max_rel_vs_bitwise"])
