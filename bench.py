@@ -534,8 +534,8 @@ def main():
             rel = float(t.item())
         v["max_rel_vs_bitwise"] = rel
         v["tolerance"] = 1e-12
-        v["note"] = ("tolerance math mode (hydro_gpu_set_math, DESIGN.md 3.6): FMA contraction and "
-                     "uncorrected reciprocal quotients; compare_tolerance max_rel against the bitwise "
+        v["note"] = ("tolerance math mode (hydro_gpu_set_math, DESIGN.md 3.6): uncorrected "
+                     "reciprocal quotients and square roots; compare_tolerance max_rel against the bitwise "
                      "result of this run (the reference's state) <= 1e-12")
         mvariants = {"tolerance": v}
         if args.flux == "hllc" and variants:

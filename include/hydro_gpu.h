@@ -71,9 +71,11 @@ enum hydro_gpu_flux { HYDRO_GPU_FLUX_HLLC = 0, HYDRO_GPU_FLUX_EXACT10 = 1 };
 /* Arithmetic of the sweeps.  BITWISE (the default) reproduces the reference's
  * -ffp-contract=off IEEE arithmetic bit for bit.  TOLERANCE is the
  * north-star contract instead: compare_tolerance max_rel <= 1e-12 against the
- * reference (proj/src/audit.cpp:146) -- FMA contraction and quotients as
- * a * (1/b) with one refined reciprocal per denominator.
- * Every branch, fallback and error check of the reference is kept. */
+ * reference (proj/src/audit.cpp:146) -- quotients as a * (1/b) with one
+ * Newton-refined reciprocal per denominator, square roots without the final
+ * correction.  Every branch, fallback and error check of the
+ * reference is kept, and the results do not depend on the launch geometry,
+ * the slab split or how a run is divided into calls. */
 enum hydro_gpu_math { HYDRO_GPU_MATH_BITWISE = 0, HYDRO_GPU_MATH_TOLERANCE = 1 };
 
 /* Case ids for the initialisers (cases.cpp:11-69 + BASELINE configs). */

@@ -507,9 +507,9 @@ def advance_gpu(grid: Grid2D, model: GasModel, dt: float, bc: str = "reflect") -
 
 
 def run_until_gpu(grid: Grid2D, model: GasModel, t_end: float, bc: str = "reflect",
-                  flux: str = "hllc") -> int:
+                  flux: str = "hllc", math: str = "bitwise") -> int:
     """run_until(grid, model, t_end) on the GPU, in place; returns steps taken."""
-    with _context_for(grid, model, bc, flux) as g:
+    with _context_for(grid, model, bc, flux, math) as g:
         try:
             steps = g.run_until(t_end)
         finally:

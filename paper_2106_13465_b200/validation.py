@@ -2,7 +2,7 @@
 suite (proj/src/validation.cpp:25-215) with every time step run by
 libhydro_b200.so.
 
-    python -m paper_2106_13465_b200.validation [--flux hllc|exact10]
+    python -m paper_2106_13465_b200.validation [--flux hllc|exact10] [--math bitwise|tolerance]
 
 prints one PASS/FAIL line per check and "N/M checks passed" like the
 reference CLI (tools/hydrobench.cpp:77-88).  The ground truth is a host-side
@@ -197,12 +197,16 @@ def check_riemann_solver() -> list[CheckResult]:
     return out
 
 
-def check_sod_profile(flux: str = "hllc") -> CheckResult:
+def _tag(flux: str, math: str) -> str:
+    return ("" if flux == "hllc" else "-" + flux) + ("" if math == "bitwise" else "-" + math)
+
+
+def check_sod_profile(flux: str = "hllc", math: str = "bitwise") -> CheckResult:
     """validation.cpp:105-139: the 4-row Sod tube to t=0.2 on the GPU."""
     model = H.GasModel()
     n = 200
     grid = H.make_case("sod", 4, n, model)
-    H.run_until_gpu(grid, model, 0.2, "reflect", flux=flux)
+    H.run_until_gpu(grid, model, 0.2, "reflect", flux=flux, math=math)
     inner = grid.interior()
     transverse = float(np.max(np.abs(inner[:, 1:, :] - inner[:, :1, :])))
     ws = exact_riemann((1.0, 0.0, 0.0, 1.0), (0.125, 0.0, 0.0, 0.1))
@@ -211,7 +215,7 @@ def check_sod_profile(flux: str = "hllc") -> CheckResult:
     for j in range(1, n + 1):
         xi = ((j - 0.5) * dy - 0.5) / 0.2
         l1 += abs(inner[0, 0, j - 1] - sample(ws, (1.0, 0.0, 0.0, 1.0), (0.125, 0.0, 0.0, 0.1), xi)[0]) * dy
-    return CheckResult(f"sod-density-l1{'' if flux == 'hllc' else '-' + flux}",
+    return CheckResult(f"sod-density-l1{_tag(flux, math)}",
                        transverse <= 1e-13 and l1 < 1e-2,
                        f"L1={l1:.5f} (tol 1e-2), transverse spread {transverse:.3g} (tol 1e-13)")
 
@@ -246,14 +250,14 @@ def _asymmetry(grid: H.Grid2D) -> float:
     return worst
 
 
-def check_conservation(flux: str = "hllc") -> list[CheckResult]:
+def check_conservation(flux: str = "hllc", math: str = "bitwise") -> list[CheckResult]:
     """validation.cpp:141-172: blast, 10 blocks of 10 GPU steps."""
     model = H.GasModel()
     grid = H.make_case("blast", 64, 64, model)
     start = _totals(grid)
     mass = energy = 0.0
     asym = _asymmetry(grid)
-    with H.GpuGrid(64, 64, grid.dx, grid.dy, model, "reflect", flux=flux) as g:
+    with H.GpuGrid(64, 64, grid.dx, grid.dy, model, "reflect", flux=flux, math=math) as g:
         g.upload(grid.planes)
         for _ in range(10):
             g.run(10)
@@ -262,7 +266,7 @@ def check_conservation(flux: str = "hllc") -> list[CheckResult]:
             mass = max(mass, abs(now[0] - start[0]) / abs(start[0]))
             energy = max(energy, abs(now[3] - start[3]) / abs(start[3]))
             asym = max(asym, _asymmetry(grid))
-    tag = "" if flux == "hllc" else "-" + flux
+    tag = _tag(flux, math)
     return [CheckResult("conservation-mass" + tag, mass <= 1e-11,
                         f"relative drift {mass:.3g} over 100 steps (tol 1e-11)"),
             CheckResult("conservation-energy" + tag, energy <= 1e-11,
@@ -279,7 +283,7 @@ def _first_diff(a: np.ndarray, b: np.ndarray) -> str:
     return f"first difference at plane {v} ({i - 1},{j - 1})"
 
 
-def check_execution_equivalence() -> list[CheckResult]:
+def check_execution_equivalence(math: str = "bitwise") -> list[CheckResult]:
     """The GPU analogue of validation.cpp:174-207: every execution variant of
     the GPU path (work-item segmentation, CUDA-graph replay vs single launches,
     row-slab decomposition with halo swaps) must give the same bits."""
@@ -287,34 +291,36 @@ def check_execution_equivalence() -> list[CheckResult]:
     steps = 10
     base = H.make_case("blast", 64, 64, model)
     ref = base.copy()
-    with H.GpuGrid(64, 64, ref.dx, ref.dy, model) as g:
+    with H.GpuGrid(64, 64, ref.dx, ref.dy, model, math=math) as g:
         g.upload(ref.planes)
         g.run(steps)
         g.download(ref.planes)
     out = []
     for seg in ((16, 16), (5, 8), (64, 64)):
         grid = base.copy()
-        with H.GpuGrid(64, 64, grid.dx, grid.dy, model) as g:
+        with H.GpuGrid(64, 64, grid.dx, grid.dy, model, math=math) as g:
             g.tune(seg[0], seg[1], 0)
             g.upload(grid.planes)
             g.run(steps)
             g.download(grid.planes)
-        out.append(CheckResult(f"equivalence-segments-{seg[0]}x{seg[1]}",
+        out.append(CheckResult(f"equivalence-segments-{seg[0]}x{seg[1]}{_tag('hllc', math)}",
                                np.array_equal(grid.planes, ref.planes),
                                _first_diff(grid.planes, ref.planes)))
     grid = base.copy()
-    with H.GpuGrid(64, 64, grid.dx, grid.dy, model) as g:
+    with H.GpuGrid(64, 64, grid.dx, grid.dy, model, math=math) as g:
         g.upload(grid.planes)
         for _ in range(steps):  # single steps: no graph, one prologue per call
             g.run(1)
         g.download(grid.planes)
-    out.append(CheckResult("equivalence-stepwise", np.array_equal(grid.interior(), ref.interior()),
+    out.append(CheckResult("equivalence-stepwise" + _tag("hllc", math),
+                           np.array_equal(grid.interior(), ref.interior()),
                            _first_diff(grid.interior(), ref.interior())))
     import torch
     for world, p2p in ((2, False), (4, False), (4, True)):
         slabs = []
         for r in range(world):
-            sl = S.GpuSlab(S.SlabGeometry(64, 64, r, world), base.dx, base.dy, model, "reflect", 0)
+            sl = S.GpuSlab(S.SlabGeometry(64, 64, r, world), base.dx, base.dy, model, "reflect", 0,
+                           math=math)
             sl.bind_stream(torch.cuda.current_stream())
             sl.grid.upload(S.slab_planes(base.planes, 64, world, r))
             slabs.append(sl)
@@ -326,24 +332,25 @@ def check_execution_equivalence() -> list[CheckResult]:
             sl.grid.download(p)
             parts.append(p)
         got = S.gather_planes(parts, 64, 64)
-        name = f"equivalence-slabs-{world}" + ("-peer-halo" if p2p else "")
+        name = f"equivalence-slabs-{world}" + ("-peer-halo" if p2p else "") + _tag("hllc", math)
         out.append(CheckResult(name, np.array_equal(got, ref.planes), _first_diff(got, ref.planes)))
     return out
 
 
-def run_validation_suite(flux: str = "hllc") -> list[CheckResult]:
+def run_validation_suite(flux: str = "hllc", math: str = "bitwise") -> list[CheckResult]:
     results = check_riemann_solver()
-    results.append(check_sod_profile(flux))
-    results += check_conservation(flux)
-    results += check_execution_equivalence()
+    results.append(check_sod_profile(flux, math))
+    results += check_conservation(flux, math)
+    results += check_execution_equivalence(math)
     return results
 
 
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--flux", default="hllc", choices=sorted(H.FLUX))
+    ap.add_argument("--math", default="bitwise", choices=sorted(H.MATH))
     args = ap.parse_args(argv)
-    results = run_validation_suite(args.flux)
+    results = run_validation_suite(args.flux, args.math)
     failed = 0
     for r in results:
         print(f"{'PASS' if r.passed else 'FAIL'} {r.name}: {r.detail}")

@@ -32,9 +32,10 @@ def test_host_exact_solver_matches_reference_flux():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("math", ["bitwise", "tolerance"])
 @pytest.mark.parametrize("flux", ["hllc", "exact10"])
-def test_gpu_validation_suite_passes(gpu, flux):
-    results = V.run_validation_suite(flux)
+def test_gpu_validation_suite_passes(gpu, flux, math):
+    results = V.run_validation_suite(flux, math)
     failed = [(r.name, r.detail) for r in results if not r.passed]
     assert not failed, failed
     assert len(results) >= 13
