@@ -122,3 +122,37 @@ def test_unknown_math_mode_is_a_config_error(gpu):
             g.set_math("fast")
         rc = g._lib.hydro_gpu_set_math(g._ctx, 7)
         assert rc == 1
+
+
+@pytest.mark.parametrize("scale,bc", [(1e-310, "reflect"), (1e-300, "transmit"), (1e200, "transmit")])
+def test_tolerance_mode_redo_items_are_decomposition_invariant(gpu, scale, bc):
+    """Denormal / tiny / huge momenta send work items through the redo pass.
+    In tolerance mode the redo pass repeats the fast pass's arithmetic (only
+    the reference's branches differ), so the result is within 1e-12 of the
+    oracle and bitwise independent of the segment lengths."""
+    grid = P.make_case("random", 72, 40, MODEL, seed=17)
+    grid.planes[1:3, 10:40, :] *= scale  # momenta of a band of rows
+    ref = O.Grid(grid.nx, grid.ny, grid.dx, grid.dy, grid.planes.copy())
+    msg_ref = None
+    try:
+        O.run_sequential(ref, 6, bc)
+    except O.CheckerError as e:  # huge momenta: the reference's positivity error
+        msg_ref = str(e)
+    outs, msgs = [], []
+    for seg in ((0, 0), (8, 4), (40, 72)):
+        planes = grid.planes.copy()
+        with P.GpuGrid(72, 40, grid.dx, grid.dy, MODEL, bc, device=0, math="tolerance") as g:
+            g.tune(seg[0], seg[1], 0)
+            g.upload(planes)
+            try:
+                g.run(6)
+                msgs.append(None)
+            except P.PositivityError as e:
+                msgs.append(str(e))
+            g.download(planes)
+        outs.append(planes)
+    assert msgs == [msg_ref] * 3
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    if msg_ref is None:
+        assert max_rel(outs[0][:, 2:74, 2:42], ref.u[:, 2:74, 2:42]) <= TOL
