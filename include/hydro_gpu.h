@@ -255,6 +255,10 @@ int hydro_gpu_reset_counters(hydro_gpu_ctx* ctx);
 /* Launch-geometry override (0 = default): strip segment length along the
  * column and row sweeps; block must be 0 or 128. */
 int hydro_gpu_tune(hydro_gpu_ctx* ctx, int seg_x, int seg_y, int block);
+/* Claim-order override of the column / row sweep: work items run in bands of
+ * `band` strip groups (32 strips each) x all segments; 0 = automatic, a value
+ * >= the number of strip groups = segment-major over the whole grid. */
+int hydro_gpu_tune_order(hydro_gpu_ctx* ctx, int band_x, int band_y);
 /* Selects the sweeps' arithmetic (enum hydro_gpu_math) for later runs of
  * this context; no reference equivalent (the reference has one arithmetic).
  * Config error for an unknown mode. */
@@ -269,8 +273,11 @@ int hydro_gpu_set_math(hydro_gpu_ctx* ctx, int math);
  * in_range[k] = 1 where the fast path applied. */
 int hydro_gpu_math_selftest(int op, const double* a, const double* b, double* fast,
                             double* exact, int* in_range, size_t n);
-/* Device pointer to plane-interleaved storage and its pitch (doubles). */
+/* Device pointer to plane-interleaved storage and its pitch (doubles): cell
+ * (i, j) of variable v, i and j in [-1, n+2], is element
+ * ((i + 1) * 4 + v) * pitch + j + hydro_gpu_col_offset(). */
 int hydro_gpu_state(hydro_gpu_ctx* ctx, double** dev_ptr, size_t* pitch);
+int hydro_gpu_col_offset(void);
 
 /* ---- device-side audit (no grid download) ------------------------------ */
 /* Per (variable, interior row) FNV-1a hash and plain sum of the current
@@ -290,6 +297,12 @@ int hydro_gpu_totals(hydro_gpu_ctx* ctx, double out[4]);
 /* FNV-1a digest of the interior bytes (proj/src/audit.cpp:53-76). */
 uint64_t hydro_grid_digest(const double* const planes[4], size_t row_stride,
                            int nx, int ny);
+/* The same FNV-1a continued from state h over interior rows 1..nx of one
+ * plane: the digest of a grid split into row slabs is the chain over
+ * (plane, slab) in plane-major, slab order, starting from the FNV offset
+ * basis 14695981039346656037. */
+uint64_t hydro_fnv1a_rows(uint64_t h, const double* plane, size_t row_stride, int nx,
+                          int ny);
 /* The state hash of host Grid2D planes, and its combining step. */
 uint64_t hydro_grid_state_hash(const double* const planes[4], size_t row_stride, int nx,
                                int ny);

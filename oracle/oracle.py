@@ -101,6 +101,8 @@ def ref():
         R = C.CDLL(REF_SO)
         i, d, u64 = C.c_int, C.c_double, C.c_uint64
         R.ref_run.argtypes = [_dp, i, i, d, d, d, d, i, i, i, i, _dp, C.c_char_p, i]
+        R.ref_run_windows.argtypes = [_dp, i, i, d, d, d, d, i, i, C.POINTER(C.c_int), i, i,
+                                      _dp, C.c_char_p, i]
         R.ref_advance.argtypes = [_dp, i, i, d, d, d, i, d, C.c_char_p, i]
         R.ref_run_until.argtypes = [_dp, i, i, d, d, d, d, i, d, C.POINTER(C.c_int), C.c_char_p, i]
         R.ref_compute_dt.argtypes = [_dp, i, i, d, d, d, d]
@@ -286,6 +288,21 @@ def ref_run(g: Grid, steps: int, bc="reflect", strategy="sequential", workers=1,
     if rc:
         raise CheckerError(rc, msg.value.decode())
     return secs.value
+
+
+def ref_run_windows(g: Grid, steps_per, bc="reflect", strategy="sequential", workers=1,
+                    gamma=1.4, cfl=0.8) -> list:
+    """ref_run over consecutive windows of one flow (grid loaded once);
+    returns the stepping seconds of each window."""
+    n = len(steps_per)
+    arr = (C.c_int * n)(*steps_per)
+    secs = (C.c_double * n)()
+    msg = C.create_string_buffer(512)
+    rc = ref().ref_run_windows(_ptr(g.u), g.nx, g.ny, g.dx, g.dy, gamma, cfl, BCS[bc], n, arr,
+                               STRATEGIES[strategy], workers, secs, msg, 512)
+    if rc:
+        raise CheckerError(rc, msg.value.decode())
+    return list(secs)
 
 
 def ref_advance(g: Grid, dt: float, bc="reflect", gamma=1.4) -> None:

@@ -117,6 +117,41 @@ int ref_run(double* u, int nx, int ny, double dx, double dy, double gamma,
   }
 }
 
+// ref_run over consecutive windows of one flow: the grid is loaded once, then
+// window w runs steps_per[w] steps with the strategy (bench.cpp:53-90
+// dispatch) and secs[w] gets the steady_clock time of its stepping only.
+// Splitting a run into windows does not change the result (every step
+// recomputes dt), so the final state is the one of a single run.
+int ref_run_windows(double* u, int nx, int ny, double dx, double dy, double gamma,
+                    double cfl, int bc, int nwin, const int* steps_per, int strategy,
+                    int workers, double* secs, char* msg, int cap) {
+  try {
+    g_bc = bc;
+    Grid2D g = load(u, nx, ny, dx, dy);
+    const GasModel model{gamma, cfl};
+    auto [pr, pc] = auto_decompose(workers);
+    const DomainDecomposition d = decompose(nx, ny, pr, pc);
+    for (int w = 0; w < nwin; ++w) {
+      const int steps = steps_per[w];
+      const auto t0 = std::chrono::steady_clock::now();
+      if (steps > 0) {
+        if (strategy == 0) run_sequential(g, model, steps);
+        else if (strategy == 1) run_fine_grain(g, model, steps, workers);
+        else if (strategy == 2) run_coarse_grain(g, model, steps, d);
+        else run_task_graph(g, model, steps, d, workers);
+      }
+      const auto t1 = std::chrono::steady_clock::now();
+      secs[w] = std::chrono::duration<double>(t1 - t0).count();
+    }
+    store(g, u);
+    g_bc = 0;
+    return 0;
+  } catch (const Error& e) {
+    g_bc = 0;
+    return report(e, msg, cap);
+  }
+}
+
 int ref_advance(double* u, int nx, int ny, double dx, double dy, double gamma,
                 int bc, double dt, char* msg, int cap) {
   try {

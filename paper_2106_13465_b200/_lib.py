@@ -91,11 +91,14 @@ def lib() -> C.CDLL:
                                     P(C.c_longlong)], i),
         "hydro_gpu_reset_counters": ([_ctx], i),
         "hydro_gpu_tune": ([_ctx, i, i, i], i),
+        "hydro_gpu_tune_order": ([_ctx, i, i], i),
         "hydro_gpu_set_math": ([_ctx, i], i),
         "hydro_gpu_state": ([_ctx, P(_dp), P(sz)], i),
+        "hydro_gpu_col_offset": ([], i),
         "hydro_gpu_math_selftest": ([i, _dp, _dp, _dp, _dp, P(i), sz], i),
         "hydro_grid_digest": ([_planes, sz, i, i], u64),
         "hydro_grid_state_hash": ([_planes, sz, i, i], u64),
+        "hydro_fnv1a_rows": ([u64, _dp, sz, i, i], u64),
         "hydro_combine_row_hashes": ([P(u64), sz], u64),
         "hydro_pairwise_sum": ([_dp, sz], d),
         "hydro_gpu_row_audit": ([_ctx, P(u64), _dp], i),

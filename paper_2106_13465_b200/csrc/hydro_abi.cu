@@ -37,6 +37,7 @@ struct hydro_gpu_ctx {
   unsigned long long* slots = nullptr;
   hydro_gpu_error last{};
   int seg_x = 0, seg_y = 0, block = 128;
+  int band_x = 0, band_y = 0;  // claim-order bands (0 = automatic)
   hb::Geometry geo{};
   hb::Geometry geo_tol{};  // occupancy of the tolerance-mode sweeps
   int math = HYDRO_GPU_MATH_BITWISE;
@@ -211,10 +212,12 @@ hb::SweepArgs sweep_args(hydro_gpu_ctx* c, int axis, int step) {
     a.src = c->A;
     a.dst = c->B;
     a.seg = c->seg_x;
+    a.band = c->band_x;
   } else {
     a.src = c->B;
     a.dst = c->A;
     a.seg = c->seg_y;
+    a.band = c->band_y;
     // rows produced by this step's row sweep feed the neighbours' column
     // sweep of step+1: inbox parity (step+1)&1
     const size_t blk = 8 * c->pitch, par = (size_t)((step + 1) & 1);
@@ -269,7 +272,8 @@ void enqueue_prologue(hydro_gpu_ctx* c, int wall_bc, int full_bc, int limit_step
   p.dt_err = c->slots + kSlotDtErr;
   cudaEvent_t e0{};
   ev_begin(c, &e0);
-  hb::launch_prologue(p, c->stream);
+  if (c->math == HYDRO_GPU_MATH_TOLERANCE) hb::launch_prologue_tol(p, c->stream);
+  else hb::launch_prologue(p, c->stream);
   ev_end(c, e0, 2);
 }
 
@@ -903,6 +907,14 @@ int hydro_gpu_tune(hydro_gpu_ctx* c, int seg_x, int seg_y, int block) {
   return HYDRO_GPU_OK;
 }
 
+int hydro_gpu_tune_order(hydro_gpu_ctx* c, int band_x, int band_y) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  c->band_x = band_x;
+  c->band_y = band_y;
+  drop_graphs(c);
+  return HYDRO_GPU_OK;
+}
+
 int hydro_gpu_set_math(hydro_gpu_ctx* c, int math) {
   if (!c) return HYDRO_GPU_ERR_CONFIG;
   if (math != HYDRO_GPU_MATH_BITWISE && math != HYDRO_GPU_MATH_TOLERANCE)
@@ -981,6 +993,8 @@ int hydro_gpu_math_selftest(int op, const double* a, const double* b, double* fa
   cudaGetLastError();
   return rc;
 }
+
+int hydro_gpu_col_offset(void) { return hb::kColOff; }
 
 int hydro_gpu_state(hydro_gpu_ctx* c, double** p, size_t* pitch) {
   if (!c) return HYDRO_GPU_ERR_CONFIG;

@@ -61,6 +61,21 @@ uint64_t hydro_grid_digest(const double* const planes[4], size_t stride, int nx,
   return h;
 }
 
+uint64_t hydro_fnv1a_rows(uint64_t h, const double* plane, size_t stride, int nx, int ny) {
+  for (int i = 1; i <= nx; ++i) {
+    const double* row = plane + (size_t)(i + 1) * stride + 2;
+    for (int j = 0; j < ny; ++j) {
+      uint64_t bits;
+      std::memcpy(&bits, row + j, 8);
+      for (int b = 0; b < 8; ++b) {
+        h ^= (bits >> (8 * b)) & 0xffu;
+        h *= 1099511628211ull;
+      }
+    }
+  }
+  return h;
+}
+
 uint64_t hydro_combine_row_hashes(const uint64_t* row_hashes, size_t n) {
   uint64_t h = 14695981039346656037ull;
   for (size_t k = 0; k < n; ++k)

@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "hydro_exact.cuh"
@@ -172,8 +174,9 @@ __device__ __forceinline__ void step_cell(M& m, const Window& w, const Cons& uC,
   if (STAGE >= 2 && upd) {
     o.un = old();
     Recip rn;
-    o.fU = update_cell(m, o.un, w.fluxPrev, o.F, dtdx, rn);
-    if (WANT_DT) o.fD = dt_speed(m, o.un, rn, g, o.spd);
+    double eint;
+    o.fU = update_cell(m, o.un, w.fluxPrev, o.F, dtdx, rn, eint);
+    if (WANT_DT) o.fD = dt_speed(m, o.un, rn, eint, g, o.spd);
   }
 }
 
@@ -305,6 +308,23 @@ __device__ __forceinline__ double step_dt(const SweepArgs& a) {
 // dynamic claiming keeps all SMs busy when the active region is localised
 // (shock tubes, blasts).  Each sweep resets the other sweep's counter for
 // the next launch on the stream.
+// Claim order: items run band by band, a band being `band` consecutive strip
+// groups x all segments, segment-major inside the band (so neighbouring warps
+// work on neighbouring strips).  The resident warps therefore stream through a
+// compact part of the grid: on large grids a segment-major order over all
+// strips (band >= groups) spreads the concurrent accesses of the row sweep
+// over every grid row -- the whole state -- at once.
+__device__ __forceinline__ void item_coords(int item, int groups, int nseg, int band, int& grp,
+                                            int& sg) {
+  const int per = band * nseg;
+  const int b = item / per;
+  const int r = item - b * per;
+  const int rem = groups - b * band;
+  const int gb = rem < band ? rem : band;  // the last band may be partial
+  sg = r / gb;
+  grp = b * band + (r - sg * gb);
+}
+
 __device__ __forceinline__ int claim(unsigned* counter) {
   int item = 0;
   if ((threadIdx.x & 31) == 0) item = (int)atomicAdd(counter, 1u);
@@ -382,46 +402,54 @@ __device__ __forceinline__ void fence_async_smem() {
 }
 
 // TMA staging (both sweeps): a warp (one strip per lane) walks a segment in
-// chunks of kChunk cells.  Chunk Q holds strip cells [ka-4+4Q, ka-1+4Q] of
-// all four variables:
-//   AXIS 1 (row sweep):    one box {kChunk cols, 1 var, 32 rows} per
-//                          variable, smem [var][row][col]
-//   AXIS 0 (column sweep): one box {32 cols, 4 vars, kChunk rows},
+// chunks of C = Staging<AXIS, FLUX>::C cells.  Chunk Q holds strip cells
+// [ka-C+CQ, ka-1+CQ] of all four variables:
+//   AXIS 1 (row sweep):    one box {C cols, 1 var, 32 rows} per variable,
+//                          smem [var][row][col] (C = 8: 64-byte box rows,
+//                          SWIZZLE_64B)
+//   AXIS 0 (column sweep): one box {32 cols, 4 vars, C rows},
 //                          smem [row][var][col]
-// so a lane's cell is 8 bytes at stride 32 B (row sweep) or consecutive
-// lanes read consecutive 8-byte words (column sweep).  Box rows are 32 or
-// 256 bytes: whole DRAM sectors.  A ring of kNBuf buffers is used in place:
+// so a lane's cell is 8 bytes at stride 8C bytes (row sweep) or consecutive
+// lanes read consecutive 8-byte words (column sweep).  Box rows are 64 or
+// 256 bytes at 64-byte aligned addresses (kColOff): whole TMA fetch units,
+// so no fetched byte is wasted.  A ring of NBUF buffers is used in place:
 // once a cell has been read into registers its slot receives the updated
 // cell (2 iterations later), and a completed chunk leaves with TMA
-// bulk-tensor stores before its buffer is refilled kNBuf-1 chunks ahead.
-// Chunk numbering runs on across the warp's items so buffer/phase
-// bookkeeping never resets.
-constexpr int kVarBytes = 32 * kChunk * 8;
+// bulk-tensor stores before its buffer is refilled.  With three buffers the
+// refill goes to the buffer stored one chunk earlier (its store has long
+// left shared memory); with two, the buffer just stored is refilled with the
+// chunk after next once that store has read it out.  Chunk numbering runs on
+// across the warp's items so buffer/phase bookkeeping never resets.
 
 // The staged sweeps' dynamic shared memory (hb_smem, declared above):
 // addressing it as hb_smem + offset (rather than through generic pointers)
 // lets the compiler emit LDS/STS with 32-bit addresses.
 
-template <int AXIS>
+template <int AXIS, int FLUX>
 struct Tiles {
+  static constexpr int C = Staging<AXIS, FLUX>::C;
+  static constexpr int NBUF = Staging<AXIS, FLUX>::NBUF;
+  static constexpr int kChunkBytes = Staging<AXIS, FLUX>::kChunkBytes;
+  static constexpr int kVarBytes = 32 * C * 8;  // row sweep: one variable of a chunk
+  static_assert(NBUF >= 2 && NBUF <= 4, "ring of 2-4 buffers");
   // smem bytes between consecutive cells of a strip / adjacent strips
-  // AXIS 0: one box {32 cols, 4 vars, kChunk rows} per chunk, slot
-  //   [pos][var][lane]; AXIS 1: one box {kChunk cols, 1 var, 32 rows} per
+  // AXIS 0: one box {32 cols, 4 vars, C rows} per chunk, slot
+  //   [pos][var][lane]; AXIS 1: one box {C cols, 1 var, 32 rows} per
   //   variable, slot [var][lane][pos].
   static constexpr uint32_t kPosBytes = AXIS == 0 ? 4 * 32 * 8 : 8;
-  static constexpr uint32_t kLaneBytes = AXIS == 0 ? 8 : kChunk * 8;
+  static constexpr uint32_t kLaneBytes = AXIS == 0 ? 8 : C * 8;
   static constexpr uint32_t kVarStride = AXIS == 0 ? 32 * 8 : kVarBytes;
 
   const CUtensorMap* load_map;
   const CUtensorMap* store_map;
-  uint32_t base;        // offset of this warp's kNBuf consecutive kChunkBytes buffers
-  uint32_t full;        // offset of this warp's kNBuf mbarriers
+  uint32_t base;        // offset of this warp's NBUF consecutive kChunkBytes buffers
+  uint32_t full;        // offset of this warp's NBUF mbarriers
   uint32_t memo_at;     // this thread's exact-10 interface memo (Memo)
   bool memo_valid;      // the memo holds an exact entry (kept across work items)
   int lane;
   int s0;               // first strip of the item: column j0 (AXIS 0) or row i0 (AXIS 1)
   int ka, kb;           // output strip cells
-  int nq;               // chunks of this item (cells ka-4 .. kb+2)
+  int nq;               // chunks of this item (cells ka-C .. kb+2)
   unsigned q0;          // running chunk number of this item's chunk 0
   int T;                // next chunk to complete (flush)
   bool active;
@@ -430,15 +458,18 @@ struct Tiles {
   // walker visits cells in order, so they advance by one slot per cell
   // instead of recomputing chunk/buffer indices.
   uint32_t lo_addr, wr_addr;
-  uint32_t sw;          // this lane's TMA swizzle term (row sweep, SWIZZLE_32B)
+  uint32_t sw;          // this lane's TMA swizzle term (row sweep)
   int lo_pos, lo_buf, wr_pos, wr_buf;
   unsigned lo_par;      // mbarrier phase parity of the load cursor's buffer
 
+  __device__ __forceinline__ static int chunks(int ka_, int kb_) {
+    return (kb_ + 2 - (ka_ - C) + C) / C;
+  }
   __device__ __forceinline__ uint8_t* buf(int q) {
-    return hb_smem + base + ((q0 + q) % kNBuf) * kChunkBytes;
+    return hb_smem + base + ((q0 + q) % NBUF) * kChunkBytes;
   }
   __device__ __forceinline__ uint64_t* bar(int q) {
-    return (uint64_t*)(hb_smem + full) + (q0 + q) % kNBuf;
+    return (uint64_t*)(hb_smem + full) + (q0 + q) % NBUF;
   }
   // Tensor coordinates {column offset, variable, plane row} of the chunk
   // whose first strip cell is k (cell k is grid index k-1 along the strip).
@@ -448,13 +479,24 @@ struct Tiles {
   __device__ __forceinline__ void issue(int q) {  // lane 0 only
     if (q >= nq) return;
     mbar_expect_tx(bar(q), kChunkBytes);
-    const int k = ka - 4 + q * kChunk;
+    const int k = ka - C + q * C;
     if constexpr (AXIS == 0) {
       tma_load(buf(q), load_map, bar(q), c0(k), 0, c2(k));
     } else {
 #pragma unroll
       for (int v = 0; v < 4; ++v) tma_load(buf(q) + v * kVarBytes, load_map, bar(q), c0(k), v, c2(k));
     }
+  }
+
+  __device__ __forceinline__ void store(int t) {  // lane 0 only
+    const int k = ka - C + t * C;
+    if constexpr (AXIS == 0) {
+      tma_store(store_map, buf(t), c0(k), 0, c2(k));
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) tma_store(store_map, buf(t) + v * kVarBytes, c0(k), v, c2(k));
+    }
+    bulk_commit();
   }
 
   // sweep orientation: mom_a is the momentum along the strip
@@ -472,12 +514,12 @@ struct Tiles {
     if (lo_pos == 0) mbar_wait((uint64_t*)(hb_smem + full) + lo_buf, lo_par);
     const Cons u = get(lo_addr);
     lo_addr += kPosBytes;
-    if (++lo_pos == kChunk) {
+    if (++lo_pos == C) {
       lo_pos = 0;
-      lo_addr += kChunkBytes - kChunk * kPosBytes;
-      if (++lo_buf == kNBuf) {
+      lo_addr += kChunkBytes - C * kPosBytes;
+      if (++lo_buf == NBUF) {
         lo_buf = 0;
-        lo_addr -= kNBuf * kChunkBytes;
+        lo_addr -= NBUF * kChunkBytes;
         lo_par ^= 1u;
       }
     }
@@ -498,57 +540,60 @@ struct Tiles {
   }
 
   // After iteration c (cell c-1 updated for c > ka): advance the update
-  // cursor; chunk boundaries fall on c - ka = 4T.
+  // cursor; chunk boundaries fall on c - ka = C*T.
   __device__ __forceinline__ void boundary(int c) {
     if (c > ka) {
       wr_addr += kPosBytes;
-      if (++wr_pos == kChunk) {
+      if (++wr_pos == C) {
         wr_pos = 0;
-        wr_addr += kChunkBytes - kChunk * kPosBytes;
-        if (++wr_buf == kNBuf) {
+        wr_addr += kChunkBytes - C * kPosBytes;
+        if (++wr_buf == NBUF) {
           wr_buf = 0;
-          wr_addr -= kNBuf * kChunkBytes;
+          wr_addr -= NBUF * kChunkBytes;
         }
       }
     }
     if (c >= ka && wr_pos == 0) flush(T++);
   }
 
-  // Chunk T's outputs are complete: store it, refill the buffer of chunk
-  // T-1 (stored at the previous boundary) with chunk T+kNBuf-1.
+  // Chunk t's outputs are complete (the load cursor is 2 cells into chunk
+  // t+1): store it and refill a free buffer.
   __device__ __forceinline__ void flush(int t) {
-    if (lane == 0) bulk_wait_read0();  // chunk t-1's stores have left smem
-    fence_async_smem();                // this lane's slot writes -> async proxy
-    __syncwarp();
-    if (lane == 0) {
-      if (t >= 1) {
-        const int k = ka - 4 + t * kChunk;
-        if constexpr (AXIS == 0) {
-          tma_store(store_map, buf(t), c0(k), 0, c2(k));
-        } else {
-#pragma unroll
-          for (int v = 0; v < 4; ++v) tma_store(store_map, buf(t) + v * kVarBytes, c0(k), v, c2(k));
+    if constexpr (NBUF == 2) {
+      fence_async_smem();  // this lane's slot writes -> async proxy
+      __syncwarp();
+      if (lane == 0) {
+        if (t >= 1) {
+          store(t);
+          bulk_wait_read0();  // chunk t's store has read its buffer
         }
-        bulk_commit();
+        issue(t + 2);         // ... which now receives chunk t+2
       }
-      issue(t + kNBuf - 1);
+    } else {
+      if (lane == 0) bulk_wait_read0();  // chunk t-1's stores have left smem
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (t >= 1) store(t);
+        issue(t + NBUF - 1);  // into the buffer of chunk t-1
+      }
     }
   }
 
-  // Stage the first chunks of an item (the first load is cell ka-2, slot 2
+  // Stage the first chunks of an item (the first load is cell ka-2, slot C-2
   // of chunk 0; the first update is cell ka, slot 0 of chunk 1) / drain it.
   __device__ __forceinline__ void begin() {
     T = 0;
-    const int b0 = (int)(q0 % kNBuf), b1 = (b0 + 1) % kNBuf;
+    const int b0 = (int)(q0 % NBUF), b1 = (b0 + 1) % NBUF;
     lo_buf = b0;
-    lo_pos = 2;
-    lo_par = (q0 / kNBuf) & 1u;
-    lo_addr = base + b0 * kChunkBytes + 2 * kPosBytes + lane * kLaneBytes;
+    lo_pos = C - 2;
+    lo_par = (q0 / NBUF) & 1u;
+    lo_addr = base + b0 * kChunkBytes + (C - 2) * kPosBytes + lane * kLaneBytes;
     wr_buf = b1;
     wr_pos = 0;
     wr_addr = base + b1 * kChunkBytes + lane * kLaneBytes;
     if (lane == 0)
-      for (int q = 0; q < kNBuf - 1; ++q) issue(q);
+      for (int q = 0; q < (NBUF == 2 ? 2 : NBUF - 1); ++q) issue(q);
     mbar_wait((uint64_t*)(hb_smem + full) + lo_buf, lo_par);
   }
   __device__ __forceinline__ void end() {
@@ -559,27 +604,34 @@ struct Tiles {
   }
 };
 
-// Shared-memory carve-up of the staged sweeps: 4 warps x kNBuf chunk
-// buffers, then 4 x kNBuf mbarriers.
-template <int AXIS>
-__device__ __forceinline__ Tiles<AXIS> make_tiles(const CUtensorMap* load_map,
-                                                  const CUtensorMap* store_map) {
-  const uint32_t pad = (256u - (smem_u32(hb_smem) & 255u)) & 255u;  // swizzle atoms
+// Shared-memory carve-up of the staged sweeps: 4 warps x NBUF chunk
+// buffers, then 4 x NBUF mbarriers (then the exact-10 memos).
+template <int AXIS, int FLUX>
+__device__ __forceinline__ Tiles<AXIS, FLUX> make_tiles(const CUtensorMap* load_map,
+                                                        const CUtensorMap* store_map) {
+  using Tl = Tiles<AXIS, FLUX>;
+  // swizzle atoms repeat every 256 (32B) / 512 (64B) bytes
+  const uint32_t pad = (1024u - (smem_u32(hb_smem) & 1023u)) & 1023u;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  Tiles<AXIS> t;
+  Tl t;
   t.load_map = load_map;
   t.store_map = store_map;
-  t.base = pad + warp * (kNBuf * kChunkBytes);
-  t.full = pad + 4 * kNBuf * kChunkBytes + warp * kNBuf * 8;
-  t.memo_at = pad + 4 * kNBuf * kChunkBytes + 4 * kNBuf * 8 + threadIdx.x * 8;
+  t.base = pad + warp * (Tl::NBUF * Tl::kChunkBytes);
+  t.full = pad + 4 * Tl::NBUF * Tl::kChunkBytes + warp * Tl::NBUF * 8;
+  t.memo_at = pad + 4 * Tl::NBUF * Tl::kChunkBytes + 4 * Tl::NBUF * 8 + threadIdx.x * 8;
   t.memo_valid = false;
   t.lane = lane;
   t.q0 = 0;
-  // SWIZZLE_32B (row sweep): within each 256-byte atom the 16-byte half of a
-  // 32-byte box row flips with address bit 7, i.e. with bit 2 of the row
-  t.sw = AXIS == 1 ? (uint32_t)((lane >> 2) & 1) << 4 : 0u;
+  // row sweep, lane = box row of 8C bytes: SWIZZLE_32B (C = 4) flips the
+  // 16-byte half of a row with address bit 7 (bit 2 of the row); SWIZZLE_64B
+  // (C = 8) XORs the 16-byte unit index (bits 4-5) with bits 7-8 (row bits 1-2)
+  if constexpr (AXIS == 1) {
+    t.sw = Tl::C == 4 ? (uint32_t)((lane >> 2) & 1) << 4 : (uint32_t)((lane >> 1) & 3) << 4;
+  } else {
+    t.sw = 0u;
+  }
   if (lane == 0) {
-    for (int q = 0; q < kNBuf; ++q) mbar_init((uint64_t*)(hb_smem + t.full) + q, 1);
+    for (int q = 0; q < Tl::NBUF; ++q) mbar_init((uint64_t*)(hb_smem + t.full) + q, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
@@ -592,7 +644,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : HB_EX_MINB)
     sweep_x_tma_kernel(SweepArgs a, const __grid_constant__ CUtensorMap load_map,
                        const __grid_constant__ CUtensorMap store_map) {
   pdl_launch_dependents();
-  Tiles<0> t = make_tiles<0>(&load_map, &store_map);
+  auto t = make_tiles<0, FLUX>(&load_map, &store_map);
   const int lane = t.lane;
   const Gas g = make_gas(a.gamma);
   pdl_wait();
@@ -614,7 +666,8 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : HB_EX_MINB)
   const int items = groups * a.nseg;
   double* __restrict__ dst = a.dst;
   for (int item = claim(a.counter); item < items; item = claim(a.counter)) {
-    const int grp = item % groups, sg = item / groups;
+    int grp, sg;
+    item_coords(item, groups, a.nseg, a.band, grp, sg);
     const int j0 = (grp << 5) + 1;
     const int j = j0 + lane;
     const bool active = j <= ny;
@@ -623,7 +676,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : HB_EX_MINB)
     t.s0 = j0;
     t.ka = i_lo + 1;
     t.kb = i_hi + 1;
-    t.nq = (t.kb + 2 - (t.ka - 4) + kChunk) / kChunk;
+    t.nq = t.chunks(t.ka, t.kb);
     t.active = active;
     // warps holding a y-wall column (1, 2, ny-1 or ny) write the ghost columns
     const bool edge = grp == 0 || (grp << 5) + 32 >= ny - 1;
@@ -683,7 +736,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : HB_EX_MINB) sweep
                                                        const __grid_constant__ CUtensorMap load_map,
                                                        const __grid_constant__ CUtensorMap store_map) {
   pdl_launch_dependents();
-  Tiles<1> t = make_tiles<1>(&load_map, &store_map);
+  auto t = make_tiles<1, FLUX>(&load_map, &store_map);
   const int lane = t.lane;
   const Gas g = make_gas(a.gamma);
   pdl_wait();
@@ -701,7 +754,8 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : HB_EX_MINB) sweep
   bool wrote_peer = false;
 
   for (int item = claim(a.counter); item < items; item = claim(a.counter)) {
-    const int grp = item % groups, sg = item / groups;
+    int grp, sg;
+    item_coords(item, groups, a.nseg, a.band, grp, sg);
     const int i0 = (grp << 5) + 1;
     const int i = i0 + lane;
     const bool active = i <= nx;
@@ -710,7 +764,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : HB_EX_MINB) sweep
     t.s0 = i0;
     t.ka = j_lo + 1;
     t.kb = j_hi + 1;
-    t.nq = (t.kb + 2 - (t.ka - 4) + kChunk) / kChunk;
+    t.nq = t.chunks(t.ka, t.kb);
     t.active = active;
     // warps holding x-wall rows write the ghost rows of the next step
     const bool mirror_lo = a.wall_lo && grp == 0;
@@ -809,11 +863,10 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : HB_EX_MINB) sweep
   }
 }
 
-#ifndef HB_TOLERANCE
 // ---------------------------------------------------------------------------
 // Start-of-run pass: apply_boundary on the physical walls of the current
 // state and compute_dt's min-reduction for the first step.
-__global__ void __launch_bounds__(256) prologue_kernel(PrologueArgs a) {
+__global__ void __launch_bounds__(256) HB_SWEEP(prologue_kernel)(PrologueArgs a) {
   const int j = 1 + blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = j <= a.ny;
   const size_t pitch = a.pitch;
@@ -821,6 +874,9 @@ __global__ void __launch_bounds__(256) prologue_kernel(PrologueArgs a) {
   const bool refl = a.bc == 0;
   const Gas g = make_gas(a.gamma);
   double lim = __longlong_as_double(0x7ff0000000000000ll);
+#ifdef HB_TOLERANCE
+  double spd = 0.0;  // the largest signal speed (speeds are >= +0)
+#endif
   unsigned long long key = kNoError;
   const int nx = a.nx, ny = a.ny;
   for (int i = 1 + blockIdx.y; active && i <= nx; i += gridDim.y) {
@@ -850,6 +906,22 @@ __global__ void __launch_bounds__(256) prologue_kernel(PrologueArgs a) {
       }
     }
     if (a.want_limit) {
+#ifdef HB_TOLERANCE
+      // the row sweep's dt speed (cell_speed == its epilogue's dt_speed)
+      double sp;
+      FastMath fm;
+      int f = cell_speed(fm, c, g, sp);
+      if (!fm.ok) {
+        ExactMath em;
+        f = cell_speed(em, c, g, sp);
+      }
+      if (f >= 0) {
+        const unsigned long long k = error_key(a.step, 0, a.row0 + i, 0, j, f);
+        key = k < key ? k : key;
+      } else {
+        spd = smax(spd, sp);
+      }
+#else
       double l;
       FastMath fm;
       int f = dt_limit(fm, c, fm.recip(c.r), a.spacing, g, l);
@@ -863,9 +935,16 @@ __global__ void __launch_bounds__(256) prologue_kernel(PrologueArgs a) {
       } else {
         lim = smin(lim, l);
       }
+#endif
     }
   }
   if (a.want_limit) {
+#ifdef HB_TOLERANCE
+    // largest speed of the warp -> spacing / speed, as the row sweep does
+    const double smx = __longlong_as_double(
+        (long long)~warp_min_u64(~(unsigned long long)__double_as_longlong(spd)));
+    if (smx > 0.0) lim = a.spacing / smx;
+#endif
     const unsigned long long m = warp_min_u64((unsigned long long)__double_as_longlong(lim));
     const unsigned long long e = warp_min_u64(key);
     if ((threadIdx.x & 31) == 0) {
@@ -875,6 +954,7 @@ __global__ void __launch_bounds__(256) prologue_kernel(PrologueArgs a) {
   }
 }
 
+#ifndef HB_TOLERANCE
 // End-of-run ghosts: the reference's last apply_boundary ran on the column
 // sweep output, so every ghost band mirrors U_b (grid.cpp:23-60).
 __global__ void finish_kernel(FinishArgs a) {
@@ -1029,22 +1109,35 @@ __global__ void math_selftest_kernel(int op, const double* a, const double* b, d
 // Segment length for the persistent sweeps: about kItemsPerWarp work items
 // per resident warp (dynamic balance), 16..128 cells, whole row-sweep chunks.
 constexpr int kItemsPerWarp = 8;
-int pick_seg(int n, int strips, int warps) {
+int pick_seg(int n, int strips, int warps, int chunk) {
   const long long groups = (strips + 31) / 32;
   long long segs = (long long)warps * kItemsPerWarp / (groups > 0 ? groups : 1);
   if (segs < 1) segs = 1;
   long long seg = (n + segs - 1) / segs;
   if (seg < 16) seg = 16;
   if (seg > 128) seg = 128;
-  seg = (seg + kChunk - 1) / kChunk * kChunk;
+  seg = (seg + chunk - 1) / chunk * chunk;
   // small grids: 16-cell segments leave warps without work, and a segment
   // is a sequential walk, so trade halo recomputation for parallelism --
   // segments down to one chunk, about one item per resident warp
   if (groups * ((n + seg - 1) / seg) < warps) {
-    long long s2 = (long long)n * groups / (warps > 0 ? warps : 1) / kChunk * kChunk;
-    seg = s2 < kChunk ? kChunk : s2;
+    long long s2 = (long long)n * groups / (warps > 0 ? warps : 1) / chunk * chunk;
+    seg = s2 < chunk ? chunk : s2;
   }
   return (int)seg;
+}
+
+// Band width of the claim order (item_coords): band <= 0 picks about two
+// bands' worth of items per wave of resident warps (the resident warps then
+// touch ~2 x warps/nseg strip groups at a time), band > 0 is an override
+// (>= groups: segment-major over all strips).
+int pick_band(int band, int strips, int nseg, int warps) {
+  const int groups = (strips + 31) / 32;
+  if (band > 0) return band < groups ? band : groups;
+  long long b = ((long long)warps + nseg - 1) / nseg;
+  b = (b + 1) / 2;
+  if (b < 1) b = 1;
+  return (int)(b < groups ? b : groups);
 }
 
 }  // namespace
@@ -1054,16 +1147,16 @@ int HB_SWEEP(query_geometry)(Geometry* g) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncSetAttribute(sweep_y_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
-  cudaFuncSetAttribute(sweep_y_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExSmemBytes);
+  cudaFuncSetAttribute(sweep_y_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExYSmemBytes);
   cudaFuncSetAttribute(sweep_y_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
-  cudaFuncSetAttribute(sweep_y_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExSmemBytes);
+  cudaFuncSetAttribute(sweep_y_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExYSmemBytes);
   int ox = 0, oy = 0, ox1 = 0, oy1 = 0;
-  cudaFuncSetAttribute(sweep_x_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kYSmemBytes);
-  cudaFuncSetAttribute(sweep_x_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExSmemBytes);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, sweep_x_tma_kernel<0>, 128, kYSmemBytes);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox1, sweep_x_tma_kernel<1>, 128, kExSmemBytes);
+  cudaFuncSetAttribute(sweep_x_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kXSmemBytes);
+  cudaFuncSetAttribute(sweep_x_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExXSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, sweep_x_tma_kernel<0>, 128, kXSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox1, sweep_x_tma_kernel<1>, 128, kExXSmemBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy, sweep_y_kernel<0, false>, 128, kYSmemBytes);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy1, sweep_y_kernel<1, false>, 128, kExSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oy1, sweep_y_kernel<1, false>, 128, kExYSmemBytes);
   g->ctas_x_per_sm = ox > 0 ? ox : 1;
   g->ctas_y_per_sm = oy > 0 ? oy : 1;
   g->ctas_x_exact = ox1 > 0 ? ox1 : 1;
@@ -1096,21 +1189,32 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
   // ghost value (sweep_x_tma_kernel)
   const cuuint64_t dim_xstore[3] = {((cuuint64_t)ny + 2 + kColOff) & ~(cuuint64_t)1, 4,
                                     (cuuint64_t)nx + 2};
+  // L2 promotion per map (experiment knob HB_PROMO="x_load,x_store,y_load,y_store",
+  // 0 none, 1 64B, 2 128B, 3 256B; default 128B everywhere)
+  int promo[4] = {2, 2, 2, 2};
+  if (const char* e = getenv("HB_PROMO")) sscanf(e, "%d,%d,%d,%d", &promo[0], &promo[1], &promo[2], &promo[3]);
+  const CUtensorMapL2promotion pk[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
   auto enc = [&](CUtensorMap* m, double* base, const cuuint64_t* dim, const cuuint32_t* box,
-                 CUtensorMapSwizzle swz) {
+                 CUtensorMapSwizzle swz, int which) {
     return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dim, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+                  pk[promo[which] & 3], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
            CUDA_SUCCESS;
   };
-  const cuuint32_t box_y[3] = {(cuuint32_t)kChunk, 1, 32};  // row sweep: 4 cols x 32 rows
-  const cuuint32_t box_x[3] = {32, 4, (cuuint32_t)kChunk};  // column sweep: 32 cols x 4 vars x 4 rows
+  const cuuint32_t box_y[3] = {(cuuint32_t)Staging<1>::C, 1, 32};  // row sweep: C cols x 32 rows
+  const cuuint32_t box_ey[3] = {(cuuint32_t)Staging<1, 1>::C, 1, 32};
+  const cuuint32_t box_x[3] = {32, 4, (cuuint32_t)Staging<0>::C};  // column sweep: 32 cols x 4 vars x C rows
   // row sweep: 32-byte box rows swizzled (halves the smem bank conflicts of
   // lane-per-row accesses); column sweep: 256-byte rows are conflict-free
-  const CUtensorMapSwizzle sy = CU_TENSOR_MAP_SWIZZLE_32B, sx = CU_TENSOR_MAP_SWIZZLE_NONE;
-  return enc(&maps->y_load, B, dim_load, box_y, sy) &&
-         enc(&maps->y_store, A, dim_store, box_y, sy) &&
-         enc(&maps->x_load, A, dim_load, box_x, sx) && enc(&maps->x_store, B, dim_xstore, box_x, sx);
+  auto swz = [](int c) { return c == 4 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B; };
+  const CUtensorMapSwizzle sy = swz(Staging<1>::C), sey = swz(Staging<1, 1>::C),
+                           sx = CU_TENSOR_MAP_SWIZZLE_NONE;
+  return enc(&maps->ey_load, B, dim_load, box_ey, sey, 2) &&
+         enc(&maps->ey_store, A, dim_store, box_ey, sey, 3) &&
+         enc(&maps->y_load, B, dim_load, box_y, sy, 2) &&
+         enc(&maps->y_store, A, dim_store, box_y, sy, 3) &&
+         enc(&maps->x_load, A, dim_load, box_x, sx, 0) && enc(&maps->x_store, B, dim_xstore, box_x, sx, 1);
 }
 
 #endif  // !HB_TOLERANCE
@@ -1136,39 +1240,44 @@ void HB_SWEEP(launch_sweep_x)(const SweepArgs& a0, const TmaMaps& maps, const Ge
                     cudaStream_t s) {
   SweepArgs a = a0;
   const int ctas = geo.sms * (a.flux == 1 ? geo.ctas_x_exact : geo.ctas_x_per_sm);
-  if (a.seg <= 0) a.seg = pick_seg(a.nx, a.ny, ctas * 4);
-  a.seg = (a.seg + kChunk - 1) / kChunk * kChunk;  // chunks never straddle segments
+  const int C = Staging<0>::C;
+  if (a.seg <= 0) a.seg = pick_seg(a.nx, a.ny, ctas * 4, C);
+  a.seg = (a.seg + C - 1) / C * C;  // chunks never straddle segments
   a.nseg = (a.nx + a.seg - 1) / a.seg;
+  a.band = pick_band(a.band, a.ny, a.nseg, ctas * 4);
   if (a.flux == 1)
-    launch_sweep(sweep_x_tma_kernel<1>, ctas, kExSmemBytes, s, a, maps.x_load, maps.x_store);
+    launch_sweep(sweep_x_tma_kernel<1>, ctas, kExXSmemBytes, s, a, maps.x_load, maps.x_store);
   else
-    launch_sweep(sweep_x_tma_kernel<0>, ctas, kYSmemBytes, s, a, maps.x_load, maps.x_store);
+    launch_sweep(sweep_x_tma_kernel<0>, ctas, kXSmemBytes, s, a, maps.x_load, maps.x_store);
 }
 
 void HB_SWEEP(launch_sweep_y)(const SweepArgs& a0, const TmaMaps& maps, const Geometry& geo,
                     cudaStream_t s) {
   SweepArgs a = a0;
   const int ctas = geo.sms * (a.flux == 1 ? geo.ctas_y_exact : geo.ctas_y_per_sm);
-  if (a.seg <= 0) a.seg = pick_seg(a.ny, a.nx, ctas * 4);
-  a.seg = (a.seg + kChunk - 1) / kChunk * kChunk;  // chunks never straddle segments
+  const int C = a.flux == 1 ? Staging<1, 1>::C : Staging<1>::C;
+  if (a.seg <= 0) a.seg = pick_seg(a.ny, a.nx, ctas * 4, C);
+  a.seg = (a.seg + C - 1) / C * C;  // chunks never straddle segments
   a.nseg = (a.ny + a.seg - 1) / a.seg;
+  a.band = pick_band(a.band, a.nx, a.nseg, ctas * 4);
   const bool peer = a.halo_up || a.halo_dn;
   if (a.flux == 1) {
-    if (peer) launch_sweep(sweep_y_kernel<1, true>, ctas, kExSmemBytes, s, a, maps.y_load, maps.y_store);
-    else launch_sweep(sweep_y_kernel<1, false>, ctas, kExSmemBytes, s, a, maps.y_load, maps.y_store);
+    if (peer) launch_sweep(sweep_y_kernel<1, true>, ctas, kExYSmemBytes, s, a, maps.ey_load, maps.ey_store);
+    else launch_sweep(sweep_y_kernel<1, false>, ctas, kExYSmemBytes, s, a, maps.ey_load, maps.ey_store);
   } else {
     if (peer) launch_sweep(sweep_y_kernel<0, true>, ctas, kYSmemBytes, s, a, maps.y_load, maps.y_store);
     else launch_sweep(sweep_y_kernel<0, false>, ctas, kYSmemBytes, s, a, maps.y_load, maps.y_store);
   }
 }
 
-#ifndef HB_TOLERANCE
-void launch_prologue(const PrologueArgs& a, cudaStream_t s) {
+void HB_SWEEP(launch_prologue)(const PrologueArgs& a, cudaStream_t s) {
   // each thread walks ~nx/128 rows of its column: few enough warps that the
   // per-warp atomicMin of the dt limit does not serialise on one address
   dim3 grid((a.ny + 255) / 256, a.nx < 128 ? a.nx : 128);
-  prologue_kernel<<<grid, 256, 0, s>>>(a);
+  HB_SWEEP(prologue_kernel)<<<grid, 256, 0, s>>>(a);
 }
+
+#ifndef HB_TOLERANCE
 
 void launch_finish(const FinishArgs& a, cudaStream_t s) {
   const int n = a.nx + a.ny;

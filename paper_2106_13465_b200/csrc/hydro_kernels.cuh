@@ -13,30 +13,49 @@ namespace hb {
 // HBM layout ("row-interleaved planes"): for each grid row i in [-1, nx+2]
 // the four variable rows rho, mom_x, mom_y, ener are stored back to back,
 // each `pitch` doubles long; column j in [-1, ny+2] sits at offset j + kColOff,
-// so interior column 1 starts on a 32-byte sector.  Two consecutive grid rows
-// (all four variables) are therefore one contiguous block of 8*pitch
-// doubles -- a slab halo is a single contiguous send/recv.
-constexpr int kColOff = 3;
+// so interior column 1 starts a 64-byte DRAM access unit (the granule TMA
+// fetches: column-sweep box rows of 32 columns are then exactly four units,
+// row-sweep chunks of 8 columns one).  Two consecutive grid rows (all four
+// variables) are one contiguous block of 8*pitch doubles -- a slab halo is a
+// single contiguous send/recv.
+constexpr int kColOff = 7;
 
-// Row-sweep tiling: every warp stages kChunk columns x 32 rows x 4 variables
-// per chunk into its own ring of kNBuf buffers (4 warps per CTA).
+// Staging (both sweeps): every warp stages chunks of all four variables for
+// its 32 strips into its own ring of buffers (4 warps per CTA).
+//   column sweep: kChunkX grid rows x 32 columns per chunk, kNBufX buffers;
+//   row sweep:    kChunkY columns x 32 grid rows per chunk, kNBufY buffers.
 #ifndef HB_NBUF
 #define HB_NBUF 3
 #endif
-constexpr int kChunk = 4;
-constexpr int kNBuf = HB_NBUF;
-constexpr int kChunkBytes = 32 * 4 * kChunk * 8;                         // 4 KB
-constexpr int kYSmemBytes = 4 * kNBuf * kChunkBytes + 256 + 4 * kNBuf * 8;  // + align, mbarriers
+#ifndef HB_YCHUNK
+#define HB_YCHUNK 8
+#endif
+#ifndef HB_YNBUF
+#define HB_YNBUF 2
+#endif
+// The exact-10 row sweep keeps 4-cell chunks in three buffers: with its
+// interface memo an 8-cell ring would cost it a resident CTA per SM.
+template <int AXIS, int FLUX = 0>
+struct Staging {
+  static constexpr bool kWide = AXIS == 1 && FLUX == 0;
+  static constexpr int C = kWide ? HB_YCHUNK : 4;          // cells per strip per chunk
+  static constexpr int NBUF = kWide ? HB_YNBUF : HB_NBUF;  // ring buffers per warp
+  static constexpr int kChunkBytes = 32 * 4 * C * 8;
+  static constexpr int kSmem = 4 * NBUF * kChunkBytes + 1024 + 4 * NBUF * 8;  // + align, mbarriers
+};
+constexpr int kXSmemBytes = Staging<0>::kSmem;
+constexpr int kYSmemBytes = Staging<1>::kSmem;
 // exact-10 sweeps: + one 13-double interface memo per thread
 constexpr int kMemoBytes = 13 * 128 * 8;
-constexpr int kExSmemBytes = kYSmemBytes + kMemoBytes;
+constexpr int kExXSmemBytes = Staging<0, 1>::kSmem + kMemoBytes;
+constexpr int kExYSmemBytes = Staging<1, 1>::kSmem + kMemoBytes;
 
 __host__ __device__ __forceinline__ size_t cell_index(size_t pitch, int v, int i, int j) {
   return ((size_t)(i + 1) * 4 + (size_t)v) * pitch + (size_t)(j + kColOff);
 }
 
 inline size_t pitch_for(int ny) {
-  const size_t need = (size_t)ny + 6;  // offsets 0..ny+5
+  const size_t need = (size_t)ny + 3 + kColOff;  // offsets 0..ny+2+kColOff
   return (need + 15) / 16 * 16;        // 128-byte rows
 }
 
@@ -47,6 +66,7 @@ struct SweepArgs {
   int nx, ny;                 // local interior extent
   int seg;                    // strip segment length per thread
   int nseg;                   // segments per strip
+  int band;                   // strip groups per band of the claim order (item_coords)
   double dx;                  // spacing along the sweep
   double spacing;             // min(dx, dy) for the dt limit
   double gamma, cfl;
@@ -69,10 +89,12 @@ struct SweepArgs {
 };
 
 struct TmaMaps {
-  CUtensorMap y_load;         // U_b, box {kChunk cols, 1 var, 32 rows}
+  CUtensorMap y_load;         // U_b, box {Staging<1>::C cols, 1 var, 32 rows}
   CUtensorMap y_store;        // U_a interior rows/cols only (clips ghosts)
-  CUtensorMap x_load;         // U_a, box {32 cols, 1 var, kChunk rows}
+  CUtensorMap x_load;         // U_a, box {32 cols, 4 vars, 4 rows}
   CUtensorMap x_store;        // U_b interior only
+  CUtensorMap ey_load;        // the exact-10 row sweep's maps: box {4 cols, 1 var, 32 rows}
+  CUtensorMap ey_store;
 };
 
 struct PrologueArgs {
@@ -122,6 +144,7 @@ int query_geometry_tol(Geometry* g);
 void launch_sweep_x_tol(const SweepArgs& a, const TmaMaps& maps, const Geometry& geo, cudaStream_t s);
 void launch_sweep_y_tol(const SweepArgs& a, const TmaMaps& maps, const Geometry& geo, cudaStream_t s);
 void launch_prologue(const PrologueArgs& a, cudaStream_t s);
+void launch_prologue_tol(const PrologueArgs& a, cudaStream_t s);  // the tolerance mode's dt
 void launch_finish(const FinishArgs& a, cudaStream_t s);
 void launch_init(const InitArgs& a, cudaStream_t s);
 void launch_row_audit(const double* u, size_t pitch, int nx, int ny, unsigned long long* hashes,

@@ -165,6 +165,17 @@ def grid_digest(grid: Grid2D) -> int:
     return int(L.lib().hydro_grid_digest(L.planes_of(grid.planes), grid.ny + 4, grid.nx, grid.ny))
 
 
+FNV_BASIS = 14695981039346656037
+
+
+def fnv1a_rows(h: int, plane: np.ndarray, nx: int, ny: int) -> int:
+    """FNV-1a of grid_digest continued from state h over interior rows 1..nx of
+    one (nx+4, ny+4) plane; chaining it over (plane, row slab) in plane-major,
+    slab order from FNV_BASIS gives the whole grid's digest."""
+    assert plane.dtype == np.float64 and plane.flags.c_contiguous
+    return int(L.lib().hydro_fnv1a_rows(h, plane.ctypes.data_as(L._dp), plane.shape[1], nx, ny))
+
+
 def grid_state_hash(grid: Grid2D) -> int:
     """Composable state hash (FNV-1a over per-row FNV-1a hashes) of host planes;
     equals GpuGrid.state_hash() of the same state."""
@@ -394,12 +405,21 @@ class GpuGrid:
     def tune(self, seg_x: int = 0, seg_y: int = 0, block: int = 0):
         self._check(self._lib.hydro_gpu_tune(self._ctx, seg_x, seg_y, block))
 
+    def tune_order(self, band_x: int = 0, band_y: int = 0):
+        """hydro_gpu_tune_order: claim-order bands of the sweeps (0 = automatic)."""
+        self._check(self._lib.hydro_gpu_tune_order(self._ctx, band_x, band_y))
+
     def set_math(self, math: str):
         """hydro_gpu_set_math: "bitwise" (default) or "tolerance"."""
         if math not in MATH:
             raise ConfigError(f"unknown math mode '{math}' (expected bitwise or tolerance)")
         self._check(self._lib.hydro_gpu_set_math(self._ctx, MATH[math]))
         self.math = math
+
+    def col_offset(self) -> int:
+        """Column offset of the device layout (state()): cell (i, j) of variable
+        v is element ((i + 1) * 4 + v) * pitch + j + col_offset()."""
+        return int(self._lib.hydro_gpu_col_offset())
 
     def state(self) -> tuple[int, int]:
         p = L._dp()

@@ -333,6 +333,27 @@ def run_loopback(slabs, steps: int, p2p: bool = False) -> None:
         slabs[0].raise_error(key)
 
 
+def chained_digest(planes, nx: int, ny: int, rank: int, world: int, send, recv) -> int | None:
+    """The reference's grid digest (audit.cpp:53-76) of a grid held as row
+    slabs, without gathering it: FNV-1a is a byte-serial chain, so each rank
+    continues the state of the rank above over its own rows, plane by plane
+    (send(h, to_rank) / recv(from_rank) -> h carry the 64-bit state).
+    Returns the digest on rank world-1, None elsewhere."""
+    from .hydro import FNV_BASIS, fnv1a_rows
+    h = FNV_BASIS
+    if world == 1:
+        for v in range(4):
+            h = fnv1a_rows(h, planes[v], nx, ny)
+        return h
+    for v in range(4):
+        if not (v == 0 and rank == 0):
+            h = recv(rank - 1 if rank > 0 else world - 1)
+        h = fnv1a_rows(h, planes[v], nx, ny)
+        if not (v == 3 and rank == world - 1):
+            send(h, rank + 1 if rank < world - 1 else 0)
+    return h if rank == world - 1 else None
+
+
 def gather_planes(slabs_or_planes, global_nx: int, ny: int):
     """Assembles full Grid2D planes from per-slab planes (rank order).  Ghost
     rows of the global grid come from the outer slabs."""
