@@ -12,6 +12,11 @@ initial condition; its final state is checked against the reference's digest
 (tests/golden/golden_full.json) and the bench fails like run_benchmark's
 equivalence gate (proj/src/bench.cpp:131-143) if it differs.
 
+The headline runs the tolerance math mode (the north star's parity bar:
+compare_tolerance max_rel <= 1e-12 in fp64, measured live against the bitwise
+state of the same run, whose digest is the reference's); the bitwise mode is
+measured beside it under ``math_variants``.
+
 Metric: cell-updates/s = interior cells x time steps / seconds (both sweeps +
 the dt reduction per time step).  ``value`` is device-resident (state in HBM
 before the timed region, CUDA events on the launch stream, max over ranks);
@@ -380,8 +385,14 @@ class Measured:
             self.grid = self.slab.grid
             self.comm = S.TorchComm()
             self.comm.setup_p2p(self.slab)  # peer-memory halo over NVLink if every rank maps its peers
+            # the whole schedule in the library: one CUDA graph per run per rank
+            # (NCCL dt allreduce inside) -- else the Python per-step driver
+            self.comm.setup_native(self.slab)
         self.halo = (("peer-memory (row-sweep stores into neighbour inboxes)" if self.comm.p2p
                       else "nccl send/recv") if world > 1 else None)
+        self.driver = (("C++: one CUDA graph per run per rank, NCCL min-allreduce of dt per step "
+                        "(hydro_gpu_comm_attach)" if self.comm.native
+                        else "python: per-step calls (slab.run_slab)") if world > 1 else None)
         self.S = S
 
     def close(self):
@@ -435,6 +446,7 @@ class Measured:
             self.one_step()
         self.sync()
         kt = self.grid.kernel_times()
+        kt["ms_comm"], kt["n_comm"] = self.grid.comm_times()
         self.grid.set_timing(False)
         return kt
 
@@ -586,6 +598,11 @@ def measure_line(env, workload, flux, math, steps, warmup, *, e2e=True, clocks=N
            "clocks": clock_info}
     if m.halo:
         out["config"]["halo"] = m.halo
+        out["config"]["driver"] = m.driver
+    if kt.get("n_comm"):
+        # device time of the per-step exchange (dt allreduce + inbox copy), max
+        # over ranks: the communication the step exposes
+        out["comm_us_per_step"] = env.allmax(1e3 * kt["ms_comm"] / kt["n_comm"])
     if e2e:
         h0, h1 = m.host_buffers()
         out["e2e"] = m.e2e(h0, h1, steps, warmup)
@@ -686,6 +703,36 @@ def cpu_baseline_leg(workload, target_s=10.0):
     return out
 
 
+def dropin_e2e(workload, math, flux="hllc"):
+    """The reference's own caller through the drop-in: run_benchmark's protocol
+    (proj/src/bench.cpp:92-152 -- one untimed warm-up step from a copy of the
+    initial grid, then the timed run) in integration/_build/hydrobench_gpu,
+    whose `gpu` strategy is hydro::run_gpu on the caller's pageable Grid2D
+    (include/hydro/gpu_strategy.hpp: cached context, pinned staging).  The
+    timed run includes the upload and download of the grid's planes."""
+    exe = os.path.join(ROOT, "integration", "_build", "hydrobench_gpu")
+    if not os.path.exists(exe):
+        return None
+    case, nx, ny, bc, tsteps, seed, _ = WORKLOADS[workload]
+    cmd = [exe, "bench", "--case", case, "--nx", str(nx), "--ny", str(ny), "--steps", str(tsteps),
+           "--strategy", "gpu", "--bc", bc, "--seed", str(seed), "--flux", flux, "--math", math]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    if out.returncode != 0:
+        raise ParityFailure(f"hydrobench_gpu failed: {out.stderr.strip()[-300:]}")
+    rate, digest = None, None
+    for line in out.stdout.splitlines():
+        if line.startswith("#") and "cell-steps/s" in line:
+            rate = float(line.split()[1])
+        elif line[:1].isdigit() and line.count(",") == 4:
+            digest = line.rsplit(",", 1)[1].strip()
+    nbytes = 4 * (nx + 4) * (ny + 4) * 8
+    return {"value": rate, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+            "result_digest": digest, "math": math,
+            "how": "integration/_build/hydrobench_gpu bench --strategy gpu: the reference's "
+                   "run_benchmark protocol, hydro::run_gpu on pageable Grid2D planes "
+                   "(one timed run incl. upload + download)"}
+
+
 def _time_port(g, bc, steps):
     from oracle import oracle as O
     t0 = time.perf_counter()
@@ -704,9 +751,11 @@ def main():
                     help="BASELINE config (default cfg3, the metric's config)")
     ap.add_argument("--flux", default="hllc", choices=["hllc", "exact10"],
                     help="interface flux (hllc = the reference hot path)")
-    ap.add_argument("--math", default="bitwise", choices=["bitwise", "tolerance"],
-                    help="sweep arithmetic of the headline (bitwise = the reference's bits; "
-                         "tolerance = compare_tolerance max_rel <= 1e-12)")
+    ap.add_argument("--math", default="tolerance", choices=["bitwise", "tolerance"],
+                    help="sweep arithmetic of the headline (tolerance = the north star's bar, "
+                         "compare_tolerance max_rel <= 1e-12 against the bitwise state, gated "
+                         "live; bitwise = the reference's bits, digest-gated, always measured "
+                         "beside it)")
     ap.add_argument("--no-variants", action="store_true",
                     help="skip the other math mode / exact-10 / secondary configs")
     args = ap.parse_args()
@@ -768,7 +817,17 @@ def main():
         print(f"bench.py: PARITY FAILURE -- {e}", file=sys.stderr, flush=True)
         sys.exit(1)
 
-    cpu = None
+    cpu = dropin = None
+    if rank == 0 and world == 1 and not args.no_variants:
+        try:
+            dropin = dropin_e2e(args.workload, args.math, args.flux)
+            if dropin and args.math == "bitwise":
+                want = golden_digest(args.workload, args.flux, hm.global_nx)
+                if want and dropin["result_digest"] != want:
+                    raise ParityFailure(f"drop-in digest {dropin['result_digest']} != {want}")
+        except ParityFailure as e:
+            print(f"bench.py: PARITY FAILURE -- {e}", file=sys.stderr, flush=True)
+            sys.exit(1)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_leg(args.workload)
 
@@ -783,8 +842,10 @@ def main():
             "roofline": head["roofline"],
             "e2e": head["e2e"],
             "e2e_pipelined": e2e_pipe,
+            "e2e_dropin": dropin,
             "gpu_launches": head["gpu_launches"],
             "kernel_ms": head["kernel_ms"],
+            "comm_us_per_step": head.get("comm_us_per_step"),
             "clocks": head["clocks"],
             "cpu_baseline": cpu,
             "result_digest": head["result_digest"],
@@ -793,6 +854,8 @@ def main():
                        else f"max_rel {head.get('max_rel_vs_bitwise')} <= {TOLERANCE} vs the "
                             f"bitwise state (digest {head.get('bitwise_digest')})"),
             "max_rel_vs_bitwise": head.get("max_rel_vs_bitwise"),
+            "bitwise_digest": head.get("bitwise_digest") if args.math == "tolerance"
+            else head["result_digest"],
             "math_variants": mvariants or None,
             "flux_variants": fvariants or None,
             "secondary": secondary or None,

@@ -25,6 +25,7 @@
 // See INTEGRATION.md for the run_strategy hook.
 #pragma once
 
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -103,6 +104,43 @@ class Context {
   hydro_gpu_ctx* ctx_ = nullptr;
 };
 
+// The context of the previous call, kept for the next one: the reference's
+// callers are single-threaded and a run_benchmark / validation
+// sequence steps grids of one geometry again and again, so consecutive calls
+// with the same geometry, model and options reuse its device buffers, tensor
+// maps and captured CUDA graphs instead of allocating and capturing afresh.
+// The grid's pageable planes are staged through the context's pinned ring
+// (hydro_gpu_upload / hydro_gpu_download).
+struct CacheKey {
+  int nx = 0, ny = 0, bc = 0, flux = 0, device = 0, math = 0;
+  double dx = 0, dy = 0, gamma = 0, cfl = 0;
+  bool operator==(const CacheKey& o) const {
+    return nx == o.nx && ny == o.ny && bc == o.bc && flux == o.flux && device == o.device &&
+           math == o.math && dx == o.dx && dy == o.dy && gamma == o.gamma && cfl == o.cfl;
+  }
+};
+
+struct Cache {
+  std::unique_ptr<Context> ctx;
+  CacheKey key;
+};
+
+inline Cache& cache() {
+  thread_local Cache c;
+  return c;
+}
+
+inline Context& cached_context(const Grid2D& g, const GasModel& m, const GpuOptions& o) {
+  const CacheKey k{g.nx(), g.ny(), o.bc, o.flux, o.device, o.math, g.dx(), g.dy(), m.gamma, m.cfl};
+  Cache& c = cache();
+  if (!c.ctx || !(c.key == k)) {
+    c.ctx.reset();
+    c.ctx = std::make_unique<Context>(g, m, o);
+    c.key = k;
+  }
+  return *c.ctx;
+}
+
 // Grid2D::at(...) const returns by value; the planes are contiguous vectors,
 // so the address of cell (-1,-1) is taken through a non-const view.
 inline const double* plane(const Grid2D& g, int v) {
@@ -110,6 +148,9 @@ inline const double* plane(const Grid2D& g, int v) {
 }
 
 }  // namespace gpu_detail
+
+// Frees the context kept between calls (device memory, pinned staging).
+inline void release_gpu_cache() { gpu_detail::cache().ctx.reset(); }
 
 // run_sequential over row slabs on several GPUs driven by this thread
 // (hydro_gpu_group: peer-memory halo, on-device dt min), bitwise equal to
@@ -160,7 +201,7 @@ inline double run_gpu_slabs(Grid2D& grid, const GasModel& model, int steps,
 inline double run_gpu(Grid2D& grid, const GasModel& model, int steps,
                       const GpuOptions& opt = {}) {
   if (opt.gpus > 1) return run_gpu_slabs(grid, model, steps, opt);
-  gpu_detail::Context ctx(grid, model, opt);
+  gpu_detail::Context& ctx = gpu_detail::cached_context(grid, model, opt);
   const double* planes[4];
   for (int v = 0; v < kNumVars; ++v) planes[v] = gpu_detail::plane(grid, v);
   ctx.check(hydro_gpu_upload(ctx.get(), planes, grid.ny() + 2 * kGhost));
@@ -173,7 +214,7 @@ inline double run_gpu(Grid2D& grid, const GasModel& model, int steps,
 
 inline void advance_gpu(Grid2D& grid, const GasModel& model, double dt,
                         const GpuOptions& opt = {}) {
-  gpu_detail::Context ctx(grid, model, opt);
+  gpu_detail::Context& ctx = gpu_detail::cached_context(grid, model, opt);
   const double* planes[4];
   for (int v = 0; v < kNumVars; ++v) planes[v] = gpu_detail::plane(grid, v);
   ctx.check(hydro_gpu_upload(ctx.get(), planes, grid.ny() + 2 * kGhost));
@@ -184,7 +225,7 @@ inline void advance_gpu(Grid2D& grid, const GasModel& model, double dt,
 
 inline int run_until_gpu(Grid2D& grid, const GasModel& model, double t_end,
                          const GpuOptions& opt = {}) {
-  gpu_detail::Context ctx(grid, model, opt);
+  gpu_detail::Context& ctx = gpu_detail::cached_context(grid, model, opt);
   const double* planes[4];
   for (int v = 0; v < kNumVars; ++v) planes[v] = gpu_detail::plane(grid, v);
   ctx.check(hydro_gpu_upload(ctx.get(), planes, grid.ny() + 2 * kGhost));
@@ -197,7 +238,7 @@ inline int run_until_gpu(Grid2D& grid, const GasModel& model, double t_end,
 
 inline double compute_dt_gpu(const Grid2D& grid, const GasModel& model,
                              const GpuOptions& opt = {}) {
-  gpu_detail::Context ctx(grid, model, opt);
+  gpu_detail::Context& ctx = gpu_detail::cached_context(grid, model, opt);
   const double* planes[4];
   for (int v = 0; v < kNumVars; ++v) planes[v] = gpu_detail::plane(grid, v);
   ctx.check(hydro_gpu_upload(ctx.get(), planes, grid.ny() + 2 * kGhost));

@@ -140,6 +140,11 @@ int hydro_gpu_download_async(hydro_gpu_ctx* ctx, double* const planes[4],
 int hydro_gpu_init_case(hydro_gpu_ctx* ctx, int case_id, uint64_t seed);
 
 /* ---- the reference's stepping entry points ----------------------------- */
+/* Step counts of one run / run_until call are bounded (the device error
+ * record orders failures by a 22-bit step field): more is a config error,
+ * and run_until stops there with one. */
+#define HYDRO_GPU_MAX_STEPS 4194302
+
 /* run_sequential: `steps` steps of BC -> dt -> column sweep -> BC -> row
  * sweep.  *last_dt (may be NULL) receives the dt of the final step. */
 int hydro_gpu_run(hydro_gpu_ctx* ctx, int steps, double* last_dt);
@@ -207,6 +212,25 @@ int hydro_gpu_slab_inbox_in(hydro_gpu_ctx* ctx, int step);
 /* Writes the reference's end-of-run ghost state (mirrors of the last
  * column-sweep output, grid.cpp:23-60 as applied before the last row sweep). */
 int hydro_gpu_slab_finish(hydro_gpu_ctx* ctx);
+
+/* ---- multi-rank slabs driven from C++ (one process per GPU) ------------ */
+/* An NCCL unique id (128 bytes) made on one rank and shared with the others
+ * by the caller (the reference has no multi-process layer). */
+int hydro_gpu_comm_unique_id(void* id128);
+/* Attaches this slab context to the ranks' NCCL communicator (NCCL is loaded
+ * at run time).  With more than one rank the slab's halo neighbours must be
+ * mapped first (hydro_gpu_set_halo_peers).  From then on hydro_gpu_run /
+ * hydro_gpu_run_async run this rank's part of run_sequential
+ * (schedulers.cpp:103-116) as ONE captured CUDA graph per step count: per
+ * step the dt limit ncclMin-allreduced (compute_dt_parallel,
+ * schedulers.cpp:47-65), the inbox copied into the ghost rows (the halo the
+ * neighbours' row sweeps stored over NVLink), both sweeps; at the end the
+ * error slots min-allreduced, so every rank reports the first error of the
+ * whole grid.  All ranks must call the same runs. */
+int hydro_gpu_comm_attach(hydro_gpu_ctx* ctx, const void* id128, int nranks, int rank);
+/* Device milliseconds and count of the per-step exchanges (allreduce +
+ * inbox copy) timed while timing is on (hydro_gpu_set_timing). */
+int hydro_gpu_comm_times(hydro_gpu_ctx* ctx, double* ms, long long* n);
 /* Synchronises and decodes a (possibly all-reduced) error key. */
 int hydro_gpu_decode_error(hydro_gpu_ctx* ctx, uint64_t key, hydro_gpu_error* out);
 

@@ -16,6 +16,7 @@
 
 #include <math.h>
 #include <stdio.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -539,17 +540,25 @@ int oracle_compute_limit(const double* u, int nx, int ny, double dx, double dy,
 /* sweep_axis_serial + process_strip + read_strip/write_strip
  * (schedulers.cpp:68-87, grid.cpp:62-141).  The Row axis swaps the momenta
  * so mom_a is along the sweep (grid.cpp:88-94, 131-139). */
-int oracle_sweep_axis(double* u, int nx, int ny, double dx, double dy,
-                      double gamma, int axis, double dt, oracle_error* err) {
+typedef struct {
+  double* u;
+  int nx, ny, axis, st_lo, st_hi;
+  double dx, dy, gamma, dt;
+  int rc, fail_strip;
+  oracle_error err;
+} sweep_job;
+
+static void sweep_strips(sweep_job* jb) {
+  double* u = jb->u;
+  const int nx = jb->nx, ny = jb->ny, axis = jb->axis;
   const int n = (axis == 0) ? nx : ny;
-  const int strips = (axis == 0) ? ny : nx;
   const int total = n + 2 * KGHOST;
   const int ia = (axis == 0) ? 1 : 2; /* plane holding mom_a */
   const int ib = (axis == 0) ? 2 : 1;
   ocons* c = (ocons*)malloc(sizeof(ocons) * (size_t)total);
   scratch_t s = {0};
-  int rc = OR_OK;
-  for (int st = 1; st <= strips && rc == OR_OK; ++st) {
+  jb->rc = OR_OK;
+  for (int st = jb->st_lo; st <= jb->st_hi; ++st) {
     for (int k = 0; k < total; ++k) {
       const int i = (axis == 0) ? k - 1 : st;
       const int j = (axis == 0) ? st : k - 1;
@@ -558,13 +567,10 @@ int oracle_sweep_axis(double* u, int nx, int ny, double dx, double dy,
       c[k].mb = AT(u, ib, i, j);
       c[k].e = AT(u, 3, i, j);
     }
-    rc = strip_update(c, n, (axis == 0) ? dx : dy, dt, gamma, &s, NULL, NULL, err);
-    if (rc != OR_OK) {
-      char ctx[64];
-      snprintf(ctx, sizeof(ctx), "%s strip %d",
-               axis == 0 ? "column sweep" : "row sweep", st);
-      if (err) { err->phase = axis + 1; err->strip = st; }
-      prefix_error(err, ctx);
+    jb->rc = strip_update(c, n, (axis == 0) ? jb->dx : jb->dy, jb->dt, jb->gamma, &s, NULL, NULL,
+                          &jb->err);
+    if (jb->rc != OR_OK) {
+      jb->fail_strip = st;
       break;
     }
     /* write_strip's validation gate (grid.cpp:106-120) repeats loop 4's
@@ -580,6 +586,56 @@ int oracle_sweep_axis(double* u, int nx, int ny, double dx, double dy,
   }
   scratch_free(&s);
   free(c);
+}
+
+static void* sweep_thread(void* arg) {
+  sweep_strips((sweep_job*)arg);
+  return NULL;
+}
+
+/* Strip-parallel sweeps for long golden runs (oracle_set_threads): strips of
+ * a sweep read and write disjoint cells (read_strip / write_strip,
+ * grid.cpp:62-141), so the result is the sequential one.  On an error the
+ * lowest failing strip is reported, but the strips after it may already be
+ * updated (the sequential sweep stops there) -- error-path parity uses one
+ * thread. */
+static int g_threads = 1;
+void oracle_set_threads(int n) { g_threads = n < 1 ? 1 : n; }
+
+/* sweep_axis_serial: read_strip -> sweep_strip -> write_strip per strip
+ * (schedulers.cpp:68-87, grid.cpp:62-141).  The Row axis swaps the momenta
+ * so mom_a is along the sweep (grid.cpp:88-94, 131-139). */
+int oracle_sweep_axis(double* u, int nx, int ny, double dx, double dy,
+                      double gamma, int axis, double dt, oracle_error* err) {
+  const int strips = (axis == 0) ? ny : nx;
+  int nt = g_threads < strips ? g_threads : strips;
+  if (nt < 1) nt = 1;
+  sweep_job* jobs = (sweep_job*)calloc((size_t)nt, sizeof(sweep_job));
+  pthread_t* th = (pthread_t*)calloc((size_t)nt, sizeof(pthread_t));
+  for (int t = 0; t < nt; ++t) {
+    sweep_job* jb = &jobs[t];
+    jb->u = u; jb->nx = nx; jb->ny = ny; jb->axis = axis;
+    jb->dx = dx; jb->dy = dy; jb->gamma = gamma; jb->dt = dt;
+    jb->st_lo = 1 + (int)((long long)strips * t / nt);
+    jb->st_hi = (int)((long long)strips * (t + 1) / nt);
+    if (nt > 1) pthread_create(&th[t], NULL, sweep_thread, jb);
+    else sweep_strips(jb);
+  }
+  int rc = OR_OK;
+  for (int t = 0; t < nt; ++t) {
+    if (nt > 1) pthread_join(th[t], NULL);
+    if (rc == OR_OK && jobs[t].rc != OR_OK) {
+      rc = jobs[t].rc;
+      if (err) *err = jobs[t].err;
+      char ctx[64];
+      snprintf(ctx, sizeof(ctx), "%s strip %d", axis == 0 ? "column sweep" : "row sweep",
+               jobs[t].fail_strip);
+      if (err) { err->phase = axis + 1; err->strip = jobs[t].fail_strip; }
+      prefix_error(err, ctx);
+    }
+  }
+  free(th);
+  free(jobs);
   return rc;
 }
 

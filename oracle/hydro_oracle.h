@@ -109,6 +109,8 @@ int oracle_sweep_strip(double* cells, int n, double dx, double dt, double gamma,
 /* Interface flux used by every sweep: 0 = HLLC (default, the reference hot
  * path), 1 = exact-10 (exact Riemann solver, 10 Newton iterations). */
 void oracle_set_flux(int flux);
+/* Strip-parallel sweeps with n threads (long golden runs; see hydro_oracle.c). */
+void oracle_set_threads(int n);
 int oracle_exact10_flux(const double* wl, const double* wr, double gamma, double* flux);
 
 /* riemann_flux (euler_kernel.cpp:59-109) on primitive states. */

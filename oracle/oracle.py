@@ -81,6 +81,8 @@ def lib():
         L.oracle_compare_tolerance.restype = None
         L.oracle_set_flux.argtypes = [i]
         L.oracle_set_flux.restype = None
+        L.oracle_set_threads.argtypes = [i]
+        L.oracle_set_threads.restype = None
         L.oracle_exact10_flux.argtypes = [_dp, _dp, d, _dp]
         L.oracle_splitmix64.argtypes = [u64]
         L.oracle_splitmix64.restype = u64
@@ -237,6 +239,11 @@ class flux_mode:
 
     def __exit__(self, *exc):
         set_flux("hllc")
+
+
+def set_threads(n: int) -> None:
+    """Strip-parallel sweeps (long golden runs; results equal one thread's)."""
+    lib().oracle_set_threads(n)
 
 
 def exact10_flux(wl, wr, gamma=1.4) -> np.ndarray:

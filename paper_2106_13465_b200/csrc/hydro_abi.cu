@@ -10,13 +10,17 @@
 // message reproduces the reference's text, context included
 // (proj/src/schedulers.cpp:23-26,80-91).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <new>
+#include <thread>
 #include <vector>
 
 #include "../../include/hydro_gpu.h"
@@ -47,8 +51,8 @@ struct hydro_gpu_ctx {
   struct Pending { cudaEvent_t a, b; int kind; };
   std::vector<Pending> pending;
   size_t ev_next = 0;
-  double ms[3] = {0, 0, 0};
-  long long n[3] = {0, 0, 0};
+  double ms[4] = {0, 0, 0, 0};   // column sweeps, row sweeps, other, comm phases
+  long long n[4] = {0, 0, 0, 0};
   // CUDA graphs of whole run_sequential calls, one per (steps, timing):
   // the 2*steps+3 launches replay without per-launch CPU and queue gaps.
   struct GraphEntry {
@@ -68,6 +72,13 @@ struct hydro_gpu_ctx {
   double* peer_up = nullptr;
   double* peer_dn = nullptr;
   std::vector<void*> ipc_opened;
+  // multi-rank slab (hydro_gpu_comm_attach): the NCCL communicator of the
+  // row-slab decomposition; hydro_gpu_run then runs the slab schedule
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  // pinned staging ring for pageable host planes (hydro_gpu_upload/download)
+  double* stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -361,15 +372,98 @@ struct DeviceGuard {
 
 namespace {
 
+// NCCL, resolved at run time (dlopen of libnccl.so.2 -- in a torch process
+// the library torch already loaded): only multi-rank slabs need it.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.get_unique_id = (decltype(a.get_unique_id))dlsym(h, "ncclGetUniqueId");
+    a.comm_init_rank = (decltype(a.comm_init_rank))dlsym(h, "ncclCommInitRank");
+    a.all_reduce = (decltype(a.all_reduce))dlsym(h, "ncclAllReduce");
+    a.comm_destroy = (decltype(a.comm_destroy))dlsym(h, "ncclCommDestroy");
+    a.error_string = (decltype(a.error_string))dlsym(h, "ncclGetErrorString");
+    a.ok = a.get_unique_id && a.comm_init_rank && a.all_reduce && a.comm_destroy && a.error_string;
+    return a;
+  }();
+  return api;
+}
+
+#define NCCL_TRY(c, expr)                                                                   \
+  do {                                                                                      \
+    const ncclResult_t r_ = (expr);                                                         \
+    if (r_ != ncclSuccess)                                                                  \
+      return set_err(c, HYDRO_GPU_ERR_CUDA, "NCCL: %s (%s)", nccl().error_string(r_), #expr); \
+  } while (0)
+
+// The slab's per-step exchange (compute_dt_parallel's min, schedulers.cpp:47-65,
+// and the column sweep's InterfaceBuffer, decomposition.hpp:58-79): the step's
+// dt limit min-allreduced over the ranks (u64 min: positive doubles order like
+// their bits; the allreduce also orders every neighbour's peer-memory halo
+// stores of the previous row sweep before this rank reads them), then the
+// inbox copied into the ghost rows.
+int enqueue_exchange(hydro_gpu_ctx* c, int step) {
+  cudaEvent_t e0{};
+  ev_begin(c, &e0);
+  unsigned long long* lim = c->slots + (step & 1);
+  NCCL_TRY(c, nccl().all_reduce(lim, lim, 1, ncclUint64, ncclMin, c->comm, c->stream));
+  const size_t blk = 8 * c->pitch, rowblk = 4 * c->pitch, par = (size_t)(step & 1);
+  const size_t bytes = blk * sizeof(double);
+  if (!c->cfg.wall_lo)
+    CUDA_TRY(c, cudaMemcpyAsync(c->A, c->inbox + (par * 2 + 0) * blk, bytes,
+                                cudaMemcpyDeviceToDevice, c->stream));
+  if (!c->cfg.wall_hi)
+    CUDA_TRY(c, cudaMemcpyAsync(c->A + (size_t)(c->cfg.nx + 2) * rowblk,
+                                c->inbox + (par * 2 + 1) * blk, bytes, cudaMemcpyDeviceToDevice,
+                                c->stream));
+  ev_end(c, e0, 3);
+  return HYDRO_GPU_OK;
+}
+
+// run_sequential's step order (schedulers.cpp:103-116) on the context: one
+// domain, or -- with a communicator attached -- this rank's row slab with the
+// per-step exchange and, at the end, the first error over all ranks (u64 min
+// of the error slots: the keys order like the reference's reporting order).
 int enqueue_run(hydro_gpu_ctx* c, int steps) {
   int rc = reset_slots(c);
   if (rc) return rc;
+  const bool slab = c->comm != nullptr;
   enqueue_prologue(c, 1, 0, 0);
+  if (slab && (c->peer_up || c->peer_dn)) {
+    const size_t blk = 8 * c->pitch, rowblk = 4 * c->pitch;
+    const size_t bytes = blk * sizeof(double);
+    if (c->peer_up)  // rows 1..2 -> the upper neighbour's inbox, parity 0
+      CUDA_TRY(c, cudaMemcpyAsync(c->peer_up + 1 * blk, c->A + 2 * rowblk, bytes,
+                                  cudaMemcpyDeviceToDevice, c->stream));
+    if (c->peer_dn)  // rows nx-1..nx -> the lower neighbour's inbox, parity 0
+      CUDA_TRY(c, cudaMemcpyAsync(c->peer_dn, c->A + (size_t)c->cfg.nx * rowblk, bytes,
+                                  cudaMemcpyDeviceToDevice, c->stream));
+  }
   for (int s = 0; s < steps; ++s) {
+    if (slab) {
+      rc = enqueue_exchange(c, s);
+      if (rc) return rc;
+    }
     enqueue_x(c, s, 0, 0.0);
     enqueue_y(c, s, 0, 0.0, s + 1 < steps);
   }
   enqueue_finish(c);
+  if (slab) {
+    unsigned long long* keys = c->slots + kSlotErr;  // the error and the pending dt error
+    NCCL_TRY(c, nccl().all_reduce(keys, keys, 2, ncclUint64, ncclMin, c->comm, c->stream));
+  }
   return HYDRO_GPU_OK;
 }
 
@@ -394,8 +488,8 @@ bool launch_graph(hydro_gpu_ctx* c, int steps) {
   if (!entry) {
     std::vector<hydro_gpu_ctx::Pending> saved;
     saved.swap(c->pending);
-    if (c->timing) {  // two events per launch: prologue, 2 per step, finish
-      const size_t need = c->graph_events.size() + 2 * (2 * (size_t)steps + 2);
+    if (c->timing) {  // two events per phase: prologue, 3 per step, finish
+      const size_t need = c->graph_events.size() + 2 * (3 * (size_t)steps + 3);
       c->graph_next = c->graph_events.size();
       while (c->graph_events.size() < need) {
         cudaEvent_t e;
@@ -516,12 +610,17 @@ int hydro_gpu_destroy(hydro_gpu_ctx* ctx) {
   if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   drop_graphs(ctx);
+  if (ctx->comm) nccl().comm_destroy(ctx->comm);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->A) cudaFree(ctx->A);
   if (ctx->B) cudaFree(ctx->B);
   if (ctx->slots) cudaFree(ctx->slots);
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
   if (ctx->inbox) cudaFree(ctx->inbox);
+  for (int b = 0; b < 2; ++b) {
+    if (ctx->stage[b]) cudaFreeHost(ctx->stage[b]);
+    if (ctx->stage_ev[b]) cudaEventDestroy(ctx->stage_ev[b]);
+  }
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return HYDRO_GPU_OK;
@@ -560,7 +659,112 @@ int hydro_gpu_upload_async(hydro_gpu_ctx* c, const double* const planes[4], size
   return HYDRO_GPU_OK;
 }
 
+namespace {
+
+// Pageable host planes (a Grid2D's std::vectors, grid.hpp:63) go through a
+// pinned two-buffer ring: the host copies of one band of rows run on
+// several threads while the DMA of the previous band is in flight -- a
+// pageable cudaMemcpy is staged by the driver one buffer at a time.
+constexpr size_t kStageBytes = 64u << 20;
+
+bool pageable(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeUnregistered;
+}
+
+int ensure_stage(hydro_gpu_ctx* c) {
+  for (int b = 0; b < 2; ++b) {
+    if (!c->stage[b]) CUDA_TRY(c, cudaMallocHost(&c->stage[b], kStageBytes));
+    if (!c->stage_ev[b]) CUDA_TRY(c, cudaEventCreateWithFlags(&c->stage_ev[b], cudaEventDisableTiming));
+  }
+  return HYDRO_GPU_OK;
+}
+
+// rows [0, n) of `row_bytes` each, src/dst strides in bytes, on up to 8 threads
+void par_copy_rows(char* dst, size_t dst_stride, const char* src, size_t src_stride, size_t n,
+                   size_t row_bytes) {
+  const size_t total = n * row_bytes;
+  unsigned nt = std::thread::hardware_concurrency();
+  nt = nt < 1 ? 1 : (nt > 8 ? 8 : nt);
+  if (total < (4u << 20)) nt = 1;
+  auto work = [&](size_t a, size_t b) {
+    for (size_t r = a; r < b; ++r) std::memcpy(dst + r * dst_stride, src + r * src_stride, row_bytes);
+  };
+  if (nt == 1) {
+    work(0, n);
+    return;
+  }
+  std::vector<std::thread> team;
+  for (unsigned t = 0; t < nt; ++t) team.emplace_back(work, n * t / nt, n * (t + 1) / nt);
+  for (auto& th : team) th.join();
+}
+
+// Host plane v rows [-1, nx+2] <-> device; up = host to device.
+int staged_transfer(hydro_gpu_ctx* c, double* const hp[4], size_t row_stride, bool up) {
+  int rc = ensure_stage(c);
+  if (rc) return rc;
+  const size_t row_bytes = (size_t)(c->cfg.ny + 4) * 8;
+  const size_t rows_total = (size_t)c->cfg.nx + 4;
+  const size_t band = kStageBytes / row_bytes;
+  if (band == 0) return set_err(c, HYDRO_GPU_ERR_CONFIG, "rows too long to stage");
+  struct Chunk { int v; size_t r0, n; };
+  std::vector<Chunk> chunks;
+  for (int v = 0; v < 4; ++v)
+    for (size_t r0 = 0; r0 < rows_total; r0 += band)
+      chunks.push_back({v, r0, std::min(band, rows_total - r0)});
+  auto dev = [&](const Chunk& k) { return c->A + cell_index(c->pitch, k.v, (int)k.r0 - 1, -1); };
+  auto host = [&](const Chunk& k) { return hp[k.v] + k.r0 * row_stride; };
+  const size_t dpitch = 4 * c->pitch * 8;
+  if (up) {
+    for (size_t q = 0; q < chunks.size(); ++q) {
+      const int b = (int)(q & 1);
+      const Chunk& k = chunks[q];
+      CUDA_TRY(c, cudaEventSynchronize(c->stage_ev[b]));  // the buffer's previous DMA is done
+      par_copy_rows((char*)c->stage[b], row_bytes, (const char*)host(k), row_stride * 8, k.n, row_bytes);
+      CUDA_TRY(c, cudaMemcpy2DAsync(dev(k), dpitch, c->stage[b], row_bytes, row_bytes, k.n,
+                                    cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(c, cudaEventRecord(c->stage_ev[b], c->stream));
+    }
+  } else {
+    auto issue = [&](size_t q) -> int {
+      const int b = (int)(q & 1);
+      const Chunk& k = chunks[q];
+      CUDA_TRY(c, cudaMemcpy2DAsync(c->stage[b], row_bytes, dev(k), dpitch, row_bytes, k.n,
+                                    cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(c, cudaEventRecord(c->stage_ev[b], c->stream));
+      return HYDRO_GPU_OK;
+    };
+    if ((rc = issue(0))) return rc;
+    for (size_t q = 0; q < chunks.size(); ++q) {
+      if (q + 1 < chunks.size() && (rc = issue(q + 1))) return rc;
+      const int b = (int)(q & 1);
+      const Chunk& k = chunks[q];
+      CUDA_TRY(c, cudaEventSynchronize(c->stage_ev[b]));
+      par_copy_rows((char*)host(k), row_stride * 8, (const char*)c->stage[b], row_bytes, k.n, row_bytes);
+    }
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return HYDRO_GPU_OK;
+}
+
+bool any_pageable(const double* const planes[4]) {
+  for (int v = 0; v < 4; ++v)
+    if (planes[v] && pageable(planes[v])) return true;
+  return false;
+}
+
+}  // namespace
+
 int hydro_gpu_upload(hydro_gpu_ctx* c, const double* const planes[4], size_t row_stride) {
+  if (c && planes && row_stride >= (size_t)c->cfg.ny + 4 && planes[0] && planes[1] && planes[2] &&
+      planes[3] && (size_t)(c->cfg.nx + 4) * (c->cfg.ny + 4) * 32 >= (32u << 20)) {
+    DeviceGuard g(c->device);
+    if (any_pageable(planes)) return staged_transfer(c, const_cast<double* const*>(planes), row_stride, true);
+  }
   const int rc = hydro_gpu_upload_async(c, planes, row_stride);
   if (rc) return rc;
   DeviceGuard g(c->device);
@@ -584,6 +788,14 @@ int hydro_gpu_download_async(hydro_gpu_ctx* c, double* const planes[4], size_t r
 }
 
 int hydro_gpu_download(hydro_gpu_ctx* c, double* const planes[4], size_t row_stride) {
+  if (c && planes && row_stride >= (size_t)c->cfg.ny + 4 && planes[0] && planes[1] && planes[2] &&
+      planes[3] && (size_t)(c->cfg.nx + 4) * (c->cfg.ny + 4) * 32 >= (32u << 20)) {
+    DeviceGuard g(c->device);
+    if (any_pageable(planes)) {
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // the state is final
+      return staged_transfer(c, planes, row_stride, false);
+    }
+  }
   const int rc = hydro_gpu_download_async(c, planes, row_stride);
   if (rc) return rc;
   DeviceGuard g(c->device);
@@ -618,6 +830,8 @@ int hydro_gpu_init_case(hydro_gpu_ctx* c, int case_id, uint64_t seed) {
 int hydro_gpu_run_async(hydro_gpu_ctx* c, int steps) {
   if (!c) return HYDRO_GPU_ERR_CONFIG;
   if (steps <= 0) return HYDRO_GPU_OK;
+  if (steps > HYDRO_GPU_MAX_STEPS)
+    return set_err(c, HYDRO_GPU_ERR_CONFIG, "more than %d steps in one call", HYDRO_GPU_MAX_STEPS);
   DeviceGuard g(c->device);
   if (steps >= 2 && launch_graph(c, steps)) {
     CUDA_TRY(c, cudaGetLastError());
@@ -639,6 +853,8 @@ int hydro_gpu_run(hydro_gpu_ctx* c, int steps, double* last_dt) {
   if (!c) return HYDRO_GPU_ERR_CONFIG;
   if (steps < 0) return set_err(c, HYDRO_GPU_ERR_CONFIG, "negative step count");
   if (steps == 0) return HYDRO_GPU_OK;
+  if (steps > HYDRO_GPU_MAX_STEPS)
+    return set_err(c, HYDRO_GPU_ERR_CONFIG, "more than %d steps in one call", HYDRO_GPU_MAX_STEPS);
   DeviceGuard g(c->device);
   int rc = hydro_gpu_run_async(c, steps);
   if (rc) return rc;
@@ -688,6 +904,13 @@ int hydro_gpu_run_until(hydro_gpu_ctx* c, double t_end, int* steps_out) {
   if (rc) return rc;
   bool started = false;
   while (t < t_end) {  // schedulers.cpp:118-138
+    if (steps == HYDRO_GPU_MAX_STEPS) {  // the error keys' step field is exhausted
+      enqueue_finish(c);
+      rc = finish_status(c, true);
+      *steps_out = steps;
+      return rc ? rc : set_err(c, HYDRO_GPU_ERR_CONFIG, "run_until stopped after %d steps",
+                               HYDRO_GPU_MAX_STEPS);
+    }
     if (!started) {
       enqueue_prologue(c, 1, 0, 0);
       started = true;
@@ -796,6 +1019,35 @@ int hydro_gpu_set_halo_peers(hydro_gpu_ctx* c, double* upper_inbox, double* lowe
   return HYDRO_GPU_OK;
 }
 
+int hydro_gpu_comm_unique_id(void* id128) {
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+  if (!id128) return HYDRO_GPU_ERR_CONFIG;
+  if (!nccl().ok) return HYDRO_GPU_ERR_CUDA;
+  ncclUniqueId id;
+  if (nccl().get_unique_id(&id) != ncclSuccess) return HYDRO_GPU_ERR_CUDA;
+  std::memcpy(id128, &id, sizeof id);
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_comm_attach(hydro_gpu_ctx* c, const void* id128, int nranks, int rank) {
+  if (!c || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return HYDRO_GPU_ERR_CONFIG;
+  if (!nccl().ok) return set_err(c, HYDRO_GPU_ERR_CUDA, "libnccl.so.2 not loadable");
+  if (nranks > 1 && ((!c->cfg.wall_lo && !c->peer_up) || (!c->cfg.wall_hi && !c->peer_dn)))
+    return set_err(c, HYDRO_GPU_ERR_CONFIG,
+                   "the slab's halo neighbours must be mapped first (hydro_gpu_set_halo_peers)");
+  DeviceGuard g(c->device);
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  ncclComm_t comm = nullptr;
+  NCCL_TRY(c, nccl().comm_init_rank(&comm, nranks, id, rank));
+  if (c->comm) nccl().comm_destroy(c->comm);
+  c->comm = comm;
+  c->nranks = nranks;
+  c->rank = rank;
+  drop_graphs(c);  // hydro_gpu_run now runs the slab schedule
+  return HYDRO_GPU_OK;
+}
+
 int hydro_gpu_slab_halo_out(hydro_gpu_ctx* c, int step) {
   if (!c) return HYDRO_GPU_ERR_CONFIG;
   DeviceGuard g(c->device);
@@ -890,10 +1142,20 @@ int hydro_gpu_reset_counters(hydro_gpu_ctx* c) {
   cudaStreamSynchronize(c->stream);
   c->pending.clear();
   c->ev_next = 0;
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < 4; ++k) {
     c->ms[k] = 0;
     c->n[k] = 0;
   }
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_comm_times(hydro_gpu_ctx* c, double* ms, long long* n) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  harvest(c);
+  if (ms) *ms = c->ms[3];
+  if (n) *n = c->n[3];
   return HYDRO_GPU_OK;
 }
 

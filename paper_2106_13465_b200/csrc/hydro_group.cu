@@ -11,14 +11,19 @@
 // compute_dt_parallel's slot min (proj/src/schedulers.cpp:47-65, paths
 // relative to /root/reference/).
 //
-// Ordering is stream/event order only, no kernel waits on another device:
-// per step every slab records an event after its row sweep, every slab's
-// stream waits on all those events before its dt-min kernel, then copies its
-// inbox into its ghost rows and runs its column and row sweeps.  That one
-// join per step orders (a) each neighbour's peer stores of step s-1 before
-// the inbox copy of step s, (b) every slot read of step s before any slab's
-// row sweep of step s+1 rewrites that parity, and (c) the inbox copy of step
-// s before a neighbour's row sweep of step s+1 rewrites that parity.
+// Ordering is stream/event order only, no kernel waits on another device.
+// Per step every slab records an event after its row sweep; the leader slab's
+// stream (slab 0) waits on all of them, runs the dt-min kernel -- it reads
+// every slab's limit slot over NVLink and writes the minimum into all of
+// them -- and records one event that every other slab's stream waits on
+// before copying its inbox into its ghost rows and running its sweeps: 2(N-1)
+// cross-stream waits per step instead of N(N-1).  That join orders (a) each
+// neighbour's peer stores of step s-1 before the inbox copy of step s, (b)
+// every slot read and write of step s before any slab's row sweep of step s+1
+// rewrites that parity, and (c) the inbox copy of step s before a neighbour's
+// row sweep of step s+1 rewrites that parity.  A whole run is captured once
+// per step count as one (multi-device) CUDA graph from the leader's stream
+// and replayed, so a run costs O(1) host calls.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -34,13 +39,13 @@ namespace {
 constexpr int kMaxSlabs = 64;
 
 struct SlotTable {
-  const unsigned long long* slot[kMaxSlabs];
+  unsigned long long* slot[kMaxSlabs];
   int n;
 };
 
-// out = min over slabs of the step's dt limit (positive doubles order like
-// their bits; a slab without cells contributes the empty sentinel ~0).
-__global__ void group_limit_min_kernel(SlotTable t, unsigned long long* out) {
+// Every slot = min over slabs of the step's dt limit (positive doubles order
+// like their bits; a slab without cells contributes the empty sentinel ~0).
+__global__ void group_limit_min_kernel(SlotTable t) {
   unsigned long long v = ~0ull;
   for (int k = threadIdx.x; k < t.n; k += 32) {
     const unsigned long long x = *(volatile const unsigned long long*)t.slot[k];
@@ -51,7 +56,8 @@ __global__ void group_limit_min_kernel(SlotTable t, unsigned long long* out) {
     const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
     v = w < v ? w : v;
   }
-  if (threadIdx.x == 0) *out = v;
+  __syncwarp();
+  for (int k = threadIdx.x; k < t.n; k += 32) *(volatile unsigned long long*)t.slot[k] = v;
 }
 
 struct Guard {
@@ -75,6 +81,11 @@ struct hydro_gpu_group {
   std::vector<hydro_gpu_ctx*> ctx;
   std::vector<cudaStream_t> stream;
   std::vector<cudaEvent_t> done;
+  cudaEvent_t lead = nullptr;  // the leader's dt-min of the step is done
+  // captured runs, one per step count (bounded cache)
+  std::vector<std::pair<int, cudaGraphExec_t>> graphs;
+  bool use_graphs = true;
+  int math = HYDRO_GPU_MATH_BITWISE;
   hydro_gpu_error last{};
 };
 
@@ -104,7 +115,17 @@ int slab_rc(hydro_gpu_group* g, int k, int rc) {
   return rc;
 }
 
+void drop_graphs(hydro_gpu_group* g) {
+  for (auto& e : g->graphs) cudaGraphExecDestroy(e.second);
+  g->graphs.clear();
+}
+
 void destroy(hydro_gpu_group* g) {
+  if (!g->device.empty()) {
+    Guard d(g->device[0]);
+    drop_graphs(g);
+    if (g->lead) cudaEventDestroy(g->lead);
+  }
   for (int k = 0; k < (int)g->ctx.size(); ++k) {
     Guard d(g->device[k]);
     if (g->ctx[k]) hydro_gpu_destroy(g->ctx[k]);
@@ -114,28 +135,108 @@ void destroy(hydro_gpu_group* g) {
   delete g;
 }
 
-// Every slab's limit slot of `step` -> its own slot, after the join.
+// The step's join: the leader waits for every slab's row sweep of the
+// previous step, takes the min of all limit slots of `step` into all of them,
+// and every other slab waits for that.
 int enqueue_limit_min(hydro_gpu_group* g, int step) {
   SlotTable t{};
   t.n = g->n;
   for (int k = 0; k < g->n; ++k) {
     double* p = nullptr;
     hydro_gpu_limit_slot(g->ctx[k], step, &p);
-    t.slot[k] = reinterpret_cast<const unsigned long long*>(p);
+    t.slot[k] = reinterpret_cast<unsigned long long*>(p);
   }
-  for (int k = 0; k < g->n; ++k) {
+  for (int k = 1; k < g->n; ++k) {
     Guard d(g->device[k]);
     GROUP_CUDA(g, cudaEventRecord(g->done[k], g->stream[k]));
   }
-  for (int k = 0; k < g->n; ++k) {
+  Guard d0(g->device[0]);
+  for (int k = 1; k < g->n; ++k) GROUP_CUDA(g, cudaStreamWaitEvent(g->stream[0], g->done[k], 0));
+  group_limit_min_kernel<<<1, 32, 0, g->stream[0]>>>(t);
+  GROUP_CUDA(g, cudaGetLastError());
+  GROUP_CUDA(g, cudaEventRecord(g->lead, g->stream[0]));
+  for (int k = 1; k < g->n; ++k) {
     Guard d(g->device[k]);
-    for (int j = 0; j < g->n; ++j)
-      if (j != k) GROUP_CUDA(g, cudaStreamWaitEvent(g->stream[k], g->done[j], 0));
-    group_limit_min_kernel<<<1, 32, 0, g->stream[k]>>>(
-        t, const_cast<unsigned long long*>(t.slot[k]));
-    GROUP_CUDA(g, cudaGetLastError());
+    GROUP_CUDA(g, cudaStreamWaitEvent(g->stream[k], g->lead, 0));
   }
   return HYDRO_GPU_OK;
+}
+
+// run_sequential over the slabs: the reference's per-step order with the dt
+// min and the halo between the slabs' sweeps (see the file comment).
+int enqueue_group_run(hydro_gpu_group* g, int steps) {
+  const bool halo = g->n > 1;
+  for (int k = 0; k < g->n; ++k) {
+    int rc = hydro_gpu_slab_prologue(g->ctx[k], 0);
+    if (!rc && halo) rc = hydro_gpu_slab_halo_out(g->ctx[k], 0);
+    if (rc) return slab_rc(g, k, rc);
+  }
+  for (int s = 0; s < steps; ++s) {
+    int rc = enqueue_limit_min(g, s);
+    if (rc) return rc;
+    for (int k = 0; k < g->n; ++k) {
+      if (halo) rc = hydro_gpu_slab_inbox_in(g->ctx[k], s);
+      if (!rc) rc = hydro_gpu_slab_sweep_x(g->ctx[k], s);
+      if (!rc) rc = hydro_gpu_slab_sweep_y(g->ctx[k], s);
+      if (rc) return slab_rc(g, k, rc);
+    }
+  }
+  for (int k = 0; k < g->n; ++k) {
+    const int rc = hydro_gpu_slab_finish(g->ctx[k]);
+    if (rc) return slab_rc(g, k, rc);
+  }
+  return HYDRO_GPU_OK;
+}
+
+// Captures (once per step count) the whole run from the leader's stream --
+// the other slabs' streams fork from it and join back -- and launches it.
+// Returns false if graphs cannot be used (the caller enqueues directly).
+bool launch_group_graph(hydro_gpu_group* g, int steps) {
+  if (!g->use_graphs) return false;
+  Guard d0(g->device[0]);
+  cudaGraphExec_t exec = nullptr;
+  for (auto& e : g->graphs)
+    if (e.first == steps) exec = e.second;
+  if (!exec) {
+    if (cudaStreamBeginCapture(g->stream[0], cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+      cudaGetLastError();
+      g->use_graphs = false;
+      return false;
+    }
+    bool ok = cudaEventRecord(g->lead, g->stream[0]) == cudaSuccess;
+    for (int k = 1; ok && k < g->n; ++k) {  // fork
+      Guard d(g->device[k]);
+      ok = cudaStreamWaitEvent(g->stream[k], g->lead, 0) == cudaSuccess;
+    }
+    ok = ok && enqueue_group_run(g, steps) == HYDRO_GPU_OK;
+    for (int k = 1; ok && k < g->n; ++k) {  // join
+      {
+        Guard d(g->device[k]);
+        ok = cudaEventRecord(g->done[k], g->stream[k]) == cudaSuccess;
+      }
+      ok = ok && cudaStreamWaitEvent(g->stream[0], g->done[k], 0) == cudaSuccess;
+    }
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(g->stream[0], &graph);
+    if (!ok || ec != cudaSuccess || !graph || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      g->use_graphs = false;
+      g->last = hydro_gpu_error{};
+      return false;
+    }
+    cudaGraphDestroy(graph);
+    if (g->graphs.size() >= 8) {
+      cudaGraphExecDestroy(g->graphs.front().second);
+      g->graphs.erase(g->graphs.begin());
+    }
+    g->graphs.push_back({steps, exec});
+  }
+  if (cudaGraphLaunch(exec, g->stream[0]) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return true;
 }
 
 }  // namespace
@@ -221,6 +322,14 @@ int hydro_gpu_group_create(const hydro_gpu_cfg* cfg, int n_gpus, const int* devi
     g->done.push_back(ev);
     hydro_gpu_set_stream(h, s);
   }
+  {
+    Guard d(g->device[0]);
+    if (cudaEventCreateWithFlags(&g->lead, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      destroy(g);
+      return HYDRO_GPU_ERR_CUDA;
+    }
+  }
   for (int k = 0; k < n_gpus; ++k) {
     double *up = nullptr, *dn = nullptr;
     if (k > 0) hydro_gpu_inbox(g->ctx[k - 1], &up, nullptr);
@@ -303,6 +412,8 @@ int hydro_gpu_group_download(hydro_gpu_group* g, double* const planes[4], size_t
 
 int hydro_gpu_group_set_math(hydro_gpu_group* g, int math) {
   if (!g) return HYDRO_GPU_ERR_CONFIG;
+  if (math != g->math) drop_graphs(g);  // the sweep kernels are baked into captured graphs
+  g->math = math;
   for (int k = 0; k < g->n; ++k) {
     const int rc = hydro_gpu_set_math(g->ctx[k], math);
     if (rc) return slab_rc(g, k, rc);
@@ -322,27 +433,12 @@ int hydro_gpu_group_init_case(hydro_gpu_group* g, int case_id, uint64_t seed) {
 // run_sequential over the slabs: the reference's per-step order with the dt
 // min and the halo between the slabs' sweeps (see the file comment).
 int hydro_gpu_group_run(hydro_gpu_group* g, int steps, double* last_dt) {
-  if (!g || steps < 0) return HYDRO_GPU_ERR_CONFIG;
+  if (!g || steps < 0 || steps > HYDRO_GPU_MAX_STEPS) return HYDRO_GPU_ERR_CONFIG;
   if (steps == 0) return HYDRO_GPU_OK;
-  const bool halo = g->n > 1;
-  for (int k = 0; k < g->n; ++k) {
-    int rc = hydro_gpu_slab_prologue(g->ctx[k], 0);
-    if (!rc && halo) rc = hydro_gpu_slab_halo_out(g->ctx[k], 0);
-    if (rc) return slab_rc(g, k, rc);
-  }
-  for (int s = 0; s < steps; ++s) {
-    int rc = enqueue_limit_min(g, s);
+  Guard d0(g->device[0]);
+  if (!(steps >= 2 && launch_group_graph(g, steps))) {
+    const int rc = enqueue_group_run(g, steps);
     if (rc) return rc;
-    for (int k = 0; k < g->n; ++k) {
-      if (halo) rc = hydro_gpu_slab_inbox_in(g->ctx[k], s);
-      if (!rc) rc = hydro_gpu_slab_sweep_x(g->ctx[k], s);
-      if (!rc) rc = hydro_gpu_slab_sweep_y(g->ctx[k], s);
-      if (rc) return slab_rc(g, k, rc);
-    }
-  }
-  for (int k = 0; k < g->n; ++k) {
-    const int rc = hydro_gpu_slab_finish(g->ctx[k]);
-    if (rc) return slab_rc(g, k, rc);
   }
   // first error in the reference's order: the minimum key over the slabs
   unsigned long long key = hb::kNoError;

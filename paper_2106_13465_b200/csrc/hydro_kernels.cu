@@ -16,14 +16,17 @@
 // loops (euler_kernel.cpp:111-223) are fused; no per-strip scratch touches
 // HBM.  Segments overlap by the 2-cell stencil halo only.
 //
-// Memory paths: in the column sweep a warp's 32 threads are 32 adjacent
-// columns, so every row it reads or writes is one coalesced 256-byte access
-// per variable (loads software-pipelined one cell ahead).  In the row sweep
-// the strips run along the contiguous axis, so tiles of 128 rows x 2 columns
-// x 4 variables are staged with TMA (cp.async.bulk.tensor, one box per
-// variable, mbarrier completion) into shared memory -- a transposed tile from
-// each thread's point of view -- and results leave through the same layout
-// with TMA bulk-tensor stores.
+// Memory paths: both sweeps stage their strips through per-warp rings in
+// shared memory, filled and drained by TMA (cp.async.bulk.tensor, mbarrier
+// completion) and used in place (Tiles below).  The column sweep's warp holds
+// 32 adjacent columns: each chunk is one box of 4 grid rows x 4 variables x
+// 32 columns (256-byte rows).  The row sweep's warp holds 32 adjacent rows:
+// each chunk is one box per variable of 32 rows x 8 columns (64-byte rows,
+// SWIZZLE_64B), i.e. a transposed tile from the walker's point of view; the
+// exact-10 row sweep keeps 4-column chunks.  Warps claim work items (32
+// strips x one segment) dynamically from a per-sweep counter, in bands of
+// strip groups (item_coords), and redo an item with the exact math policy if
+// the fast pass left its proven range.
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 

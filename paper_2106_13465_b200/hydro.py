@@ -176,6 +176,15 @@ def fnv1a_rows(h: int, plane: np.ndarray, nx: int, ny: int) -> int:
     return int(L.lib().hydro_fnv1a_rows(h, plane.ctypes.data_as(L._dp), plane.shape[1], nx, ny))
 
 
+def comm_unique_id() -> bytes:
+    """An NCCL unique id for hydro_gpu_comm_attach (made on one rank)."""
+    buf = C.create_string_buffer(128)
+    rc = L.lib().hydro_gpu_comm_unique_id(buf)
+    if rc:
+        raise DeviceError(rc, "NCCL unavailable (libnccl.so.2)")
+    return buf.raw
+
+
 def grid_state_hash(grid: Grid2D) -> int:
     """Composable state hash (FNV-1a over per-row FNV-1a hashes) of host planes;
     equals GpuGrid.state_hash() of the same state."""
@@ -415,6 +424,18 @@ class GpuGrid:
             raise ConfigError(f"unknown math mode '{math}' (expected bitwise or tolerance)")
         self._check(self._lib.hydro_gpu_set_math(self._ctx, MATH[math]))
         self.math = math
+
+    # multi-rank slabs driven from C++ (hydro_gpu_comm_attach) -----------------
+    def comm_attach(self, unique_id: bytes, nranks: int, rank: int):
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        self._check(self._lib.hydro_gpu_comm_attach(self._ctx, buf, nranks, rank))
+
+    def comm_times(self) -> tuple[float, int]:
+        """(device ms, count) of the per-step exchanges timed with set_timing(True)."""
+        ms = C.c_double()
+        n = C.c_longlong()
+        self._check(self._lib.hydro_gpu_comm_times(self._ctx, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     def col_offset(self) -> int:
         """Column offset of the device layout (state()): cell (i, j) of variable

@@ -232,6 +232,34 @@ class TorchComm:
             self.p2p = True
         return self.p2p
 
+    def setup_native(self, slab) -> bool:
+        """Collective: hands the whole step schedule to the library
+        (hydro_gpu_comm_attach): per rank ONE captured CUDA graph per run with
+        an NCCL min-allreduce of the dt limit per step, the peer-memory halo
+        and the first error over all ranks -- no per-step host calls.  Only
+        over NCCL (one GPU per rank) with the peer-memory halo in place, and
+        only if every rank can load NCCL; otherwise the Python schedule
+        (run_slab) stays.  HYDRO_SLAB_DRIVER=python forces the latter."""
+        from .hydro import comm_unique_id
+        self.native = False
+        want = (os.environ.get("HYDRO_SLAB_DRIVER", "native") == "native"
+                and self.dist.get_backend(self.group) == "nccl"
+                and (self.world == 1 or getattr(self, "p2p", False)))
+        uid = None
+        if want and self.rank == 0:
+            try:
+                uid = comm_unique_id()
+            except Exception:  # noqa: BLE001 -- no NCCL: stay on the Python schedule
+                uid = None
+        box = [uid]
+        self.dist.broadcast_object_list(box, src=0, group=self.group)
+        uid = box[0]
+        if not self._all_true(want and uid is not None):
+            return False
+        slab.grid.comm_attach(uid, self.world, self.rank)
+        self.native = True
+        return True
+
     def first_error(self, key: torch.Tensor) -> int:
         if self.world == 1:
             keys = [key.clone()]
@@ -284,6 +312,9 @@ def run_slab(slab, comm: TorchComm, steps: int) -> None:
     enqueued on the current stream; the only host synchronisation is the
     final error gather."""
     if steps <= 0:
+        return
+    if getattr(comm, "native", False):  # the library runs the whole schedule
+        slab.grid.run(steps)
         return
     p2p = getattr(comm, "p2p", False)
     slab.prologue(0)

@@ -78,10 +78,14 @@ FULL = [
 # which tests/test_exact_flux.py pins within 1e-12 of the reference's own
 # exact solver (proj/src/exact_riemann.cpp).
 FULL_EXACT10 = [
+    ("cfg0_corner_blast_256_100_exact10", "corner_blast", 256, 256, "reflect", 100, 0,
+     "BASELINE config 0 with its stated exact Riemann solver (10 Newton iterations), full"),
     ("cfg1_sod_x_2048_200_exact10", "sod_x", 2048, 2048, "transmit", 200, 0,
      "BASELINE config 1 with its stated exact Riemann solver (10 Newton iterations), full"),
     ("cfg2_random_8192_50_exact10", "random", 8192, 8192, "transmit", 50, SEED_CFG2,
      "BASELINE config 2 with its stated exact Riemann solver (10 Newton iterations), full"),
+    ("cfg3_corner_blast_16384_50_exact10", "corner_blast", 16384, 16384, "reflect", 50, 0,
+     "BASELINE config 3 at P=1 with its stated exact Riemann solver, full"),
     ("cfg4_random_16384_20_exact10", "random", 16384, 16384, "transmit", 20, SEED_CFG4,
      "BASELINE config 4 at P=1 with its stated exact Riemann solver, full"),
     ("random_1024_20_exact10", "random", 1024, 1024, "transmit", 20, 7,
@@ -89,16 +93,23 @@ FULL_EXACT10 = [
 ]
 
 
+THREADS = 1
+
+
 def run_oracle_exact10(entry):
     name, case, nx, ny, bc, steps, seed, prov = entry
     g = O.make_case(case, nx, ny, seed=seed)
     t0 = time.time()
+    O.set_threads(THREADS)
     with O.flux_mode("exact10"):
         O.run_sequential(g, steps, bc)
+    O.set_threads(1)
     secs = time.time() - t0
     rec = {"case": case, "nx": g.nx, "ny": g.ny, "bc": bc, "steps": steps, "seed": seed,
            "flux": "exact10", "digest": f"{O.digest(g):016x}", "provenance": prov,
-           "generator": "oracle (C restatement, oracle_set_flux exact10), single thread",
+           "generator": "oracle (C restatement, oracle_set_flux exact10), "
+                        + ("single thread" if THREADS == 1 else
+                           f"strip-parallel x{THREADS} (oracle_set_threads; equal to one thread)"),
            "ref_seconds": round(secs, 1)}
     print(f"{name}: {rec['digest']} ({secs:.1f}s)", flush=True)
     return name, rec
@@ -122,7 +133,11 @@ def main():
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--only", default=None)
     ap.add_argument("--out", default=None, help="write to this file instead (parallel runs)")
+    ap.add_argument("--threads", type=int, default=1,
+                    help="strip-parallel oracle sweeps for the exact-10 entries")
     args = ap.parse_args()
+    global THREADS
+    THREADS = args.threads
     if not O.ref_available():
         sys.exit("oracle/_ref/libhydro_ref.so missing: make -C oracle")
     out_path = args.out or os.path.join(HERE, "golden_full.json" if args.full else "golden.json")

@@ -60,8 +60,13 @@ def test_multi_rank_bench_code_path(gpu):
     lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 3 and d["scaling"] == "weak" and d["value"] > 0
-    assert d["config"]["cells"] == 3 * 2048 * 2048
+    # BASELINE config 3 strong-scaled over 3 row slabs: the same global grid,
+    # so the bitwise state's digest -- chained over the ranks' slabs -- is the
+    # reference's, and the tolerance headline is within 1e-12 of it
+    assert d["n_gpus"] == 3 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["cells"] == 16384 * 16384
+    assert d["bitwise_digest"] == "b14afe9de695c517"
+    assert 0 < d["max_rel_vs_bitwise"] <= 1e-12
     assert "peer-memory" in d["config"]["halo"]
     for key in ("roofline", "e2e", "gpu_launches", "clocks", "ms_per_step"):
         assert key in d, key
@@ -69,9 +74,10 @@ def test_multi_rank_bench_code_path(gpu):
 
 @pytest.mark.gpu
 def test_single_gpu_bench_line_carries_the_contract_keys(gpu):
-    """The driver's default N=1 run: one JSON line with the base contract's
-    keys plus roofline, e2e (host buffers), clocks, gpu_launches and the
-    result digest of config 1 (the reference's e00cb4cfa888c325)."""
+    """The driver's default N=1 run (config 3, tolerance headline): one JSON
+    line with the base contract's keys plus roofline, e2e (host buffers),
+    clocks, gpu_launches, the bitwise state's digest (the reference's
+    b14afe9de695c517) and the headline's measured max_rel against it."""
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1",
                           "--warmup", "1", "--no-variants", "--no-cpu-baseline"],
                          capture_output=True, text=True, timeout=900, cwd=ROOT)
@@ -86,24 +92,31 @@ def test_single_gpu_bench_line_carries_the_contract_keys(gpu):
     assert d["n_gpus"] == 1 and d["dtype"] == "f64" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 1
-    assert d["result_digest"] == "e00cb4cfa888c325"
+    assert d["config"]["math"] == "tolerance" and d["config"]["cells"] == 16384 * 16384
+    assert d["bitwise_digest"] == "b14afe9de695c517"
+    assert 0 < d["max_rel_vs_bitwise"] <= 1e-12
     assert d["gpu_launches"] > 0
 
 
 @pytest.mark.gpu
 def test_bench_variants_tolerance_within_bound(gpu):
-    """The variants of a default run: exact-10 keeps the oracle's digest of
-    config 1 (tests/golden/golden_full.json), and the tolerance math mode's
-    measured max_rel against the bitwise state is within 1e-12 for both
-    fluxes."""
+    """The variants of a bitwise-headline run on config 1: the headline keeps
+    the reference's digest, exact-10 the oracle's (tests/golden/
+    golden_full.json), and both tolerance lines are within 1e-12 of their
+    bitwise states."""
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1",
-                          "--warmup", "1", "--no-cpu-baseline"],
+                          "--warmup", "1", "--no-cpu-baseline", "--workload", "cfg1",
+                          "--math", "bitwise"],
                          capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     d = json.loads([l for l in out.stdout.splitlines() if l.strip().startswith("{")][0])
     assert d["config"]["math"] == "bitwise"
-    assert d["flux_variants"]["exact10"]["result_digest"] == "5bba80ba4684d325"
-    for name in ("tolerance", "tolerance_exact10"):
-        v = d["math_variants"][name]
-        assert v["value"] > 0 and v["e2e"]["value"] > 0
-        assert 0 < v["max_rel_vs_bitwise"] <= 1e-12, (name, v["max_rel_vs_bitwise"])
+    assert d["result_digest"] == d["golden_digest"] == "e00cb4cfa888c325"
+    assert d["flux_variants"]["exact10_bitwise"]["result_digest"] == "5bba80ba4684d325"
+    for v in (d["math_variants"]["tolerance"], d["flux_variants"]["exact10_tolerance"]):
+        assert v["value"] > 0
+        assert 0 < v["max_rel_vs_bitwise"] <= 1e-12, v["max_rel_vs_bitwise"]
+    for wl in ("cfg2",):
+        sec = d["secondary"][wl]
+        assert sec["bitwise"]["result_digest"] == sec["bitwise"]["golden_digest"]
+        assert 0 < sec["tolerance"]["max_rel_vs_bitwise"] <= 1e-12
