@@ -276,6 +276,11 @@ int hydro_gpu_kernel_times(hydro_gpu_ctx* ctx, double* ms_x, double* ms_y,
                            double* ms_other, long long* n_x, long long* n_y,
                            long long* n_other);
 int hydro_gpu_reset_counters(hydro_gpu_ctx* ctx);
+/* Cell updates of the column / row sweeps since the last reset_counters that
+ * took the uniform-window identity (a cell whose 5-cell
+ * stencil window equals its predecessor's, whose update was the identity,
+ * gets the identical result without re-evaluating it). */
+int hydro_gpu_skipped(hydro_gpu_ctx* ctx, uint64_t* x, uint64_t* y);
 /* Launch-geometry override (0 = default): strip segment length along the
  * column and row sweeps; block must be 0 or 128. */
 int hydro_gpu_tune(hydro_gpu_ctx* ctx, int seg_x, int seg_y, int block);

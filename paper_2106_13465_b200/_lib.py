@@ -98,6 +98,7 @@ def lib() -> C.CDLL:
         "hydro_gpu_comm_unique_id": ([C.c_void_p], i),
         "hydro_gpu_comm_attach": ([_ctx, C.c_void_p, i, i], i),
         "hydro_gpu_comm_times": ([_ctx, _dp, P(C.c_longlong)], i),
+        "hydro_gpu_skipped": ([_ctx, P(u64), P(u64)], i),
         "hydro_gpu_math_selftest": ([i, _dp, _dp, _dp, _dp, P(i), sz], i),
         "hydro_grid_digest": ([_planes, sz, i, i], u64),
         "hydro_grid_state_hash": ([_planes, sz, i, i], u64),

@@ -86,7 +86,8 @@ namespace {
 constexpr int kSlotErr = 2;
 constexpr int kSlotDtErr = 3;
 constexpr int kSlotCounters = 4;
-constexpr int kSlots = 5;
+constexpr int kSlotSkipped = 5;  // [5], [6]: x / y cell updates taken by the uniform-window identity
+constexpr int kSlots = 7;
 
 const char* kFieldName[3] = {"rho", "pres", "internal energy"};
 
@@ -218,6 +219,7 @@ hb::SweepArgs sweep_args(hydro_gpu_ctx* c, int axis, int step) {
   a.dt_err = c->slots + kSlotDtErr;
   a.counter = reinterpret_cast<unsigned*>(c->slots + kSlotCounters) + axis;
   a.counter_next = reinterpret_cast<unsigned*>(c->slots + kSlotCounters) + (1 - axis);
+  a.skipped = c->slots + kSlotSkipped + axis;
   a.step = step;
   if (axis == 0) {
     a.src = c->A;
@@ -595,7 +597,7 @@ int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out) {
   cudaMemsetAsync(ctx->B, 0, bytes, ctx->stream);
   cudaMemsetAsync(ctx->inbox, 0, 4 * 8 * ctx->pitch * sizeof(double), ctx->stream);
   cudaMemsetAsync(ctx->slots, 0xff, 4 * sizeof(unsigned long long), ctx->stream);
-  cudaMemsetAsync(ctx->slots + kSlotCounters, 0, sizeof(unsigned long long), ctx->stream);
+  cudaMemsetAsync(ctx->slots + kSlotCounters, 0, 3 * sizeof(unsigned long long), ctx->stream);
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
     hydro_gpu_destroy(ctx);
     return HYDRO_GPU_ERR_CUDA;
@@ -1146,6 +1148,18 @@ int hydro_gpu_reset_counters(hydro_gpu_ctx* c) {
     c->ms[k] = 0;
     c->n[k] = 0;
   }
+  CUDA_TRY(c, cudaMemset(c->slots + kSlotSkipped, 0, 2 * sizeof(unsigned long long)));
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_skipped(hydro_gpu_ctx* c, uint64_t* x, uint64_t* y) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  unsigned long long v[2] = {0, 0};
+  CUDA_TRY(c, cudaMemcpy(v, c->slots + kSlotSkipped, sizeof v, cudaMemcpyDeviceToHost));
+  if (x) *x = v[0];
+  if (y) *y = v[1];
   return HYDRO_GPU_OK;
 }
 

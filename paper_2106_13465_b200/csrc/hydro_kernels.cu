@@ -177,9 +177,9 @@ __device__ __forceinline__ void step_cell(M& m, const Window& w, const Cons& uC,
   if (STAGE >= 2 && upd) {
     o.un = old();
     Recip rn;
-    double eint;
-    o.fU = update_cell(m, o.un, w.fluxPrev, o.F, dtdx, rn, eint);
-    if (WANT_DT) o.fD = dt_speed(m, o.un, rn, eint, g, o.spd);
+    UpdAux aux;
+    o.fU = update_cell(m, o.un, w.fluxPrev, o.F, dtdx, rn, aux);
+    if (WANT_DT) o.fD = dt_speed(m, o.un, rn, aux, g, o.spd);
   }
 }
 
@@ -206,6 +206,47 @@ __device__ __forceinline__ void keep_min(unsigned long long& k, unsigned long lo
 // iterations are peeled, so a segment costs its cells plus two primitive
 // conversions, two face reconstructions and one flux.  Returns false if a
 // FastMath operation left its proven range somewhere in the segment.
+__device__ __forceinline__ bool same_bits(const Cons& a, const Cons& b) {
+  return (__double_as_longlong(a.r) == __double_as_longlong(b.r)) &
+         (__double_as_longlong(a.ma) == __double_as_longlong(b.ma)) &
+         (__double_as_longlong(a.mb) == __double_as_longlong(b.mb)) &
+         (__double_as_longlong(a.e) == __double_as_longlong(b.e));
+}
+
+// The uniform-window identity (below) pays where the sweeps are compute-bound
+// on uniform flow -- the bitwise mode (config 3 column/row sweeps -11%/-22%,
+// config 1 -20%/-36%).  The tolerance-mode sweeps of config 3 are already at
+// the memory system's rate and the cell compares cost them registers (config
+// 2: +7%), so that TU leaves it out.
+#ifndef HB_SKIP
+#ifdef HB_TOLERANCE
+#define HB_SKIP 0
+#else
+#define HB_SKIP 1
+#endif
+#endif
+
+// Walks strip cells [ka, kb] (strip coordinates: cell k holds grid index
+// k-1) with math policy M.  src.load(k) returns cell k in sweep orientation
+// (called for k = ka-2 .. kb+2 in order), sink(k, out) receives updated
+// cells ka..kb, src.boundary(c) is called after every iteration (chunk
+// bookkeeping).  Positivity failures are folded into `ekey` (kg converts a
+// local strip cell to the global index used in error keys).  The two halo
+// iterations are peeled, so a segment costs its cells plus two primitive
+// conversions, two face reconstructions and one flux.  Returns false if a
+// FastMath operation left its proven range somewhere in the segment.
+//
+// Uniform-window identity: the update of cell c-1 is a pure function of the
+// five cells c-3..c+1 (loop 1-4 of sweep_strip, euler_kernel.cpp:111-223),
+// and so are the carried faces and flux.  When the six cells c-4..c+1 are
+// bitwise equal, cell c-1's window equals cell c-2's, so its update is cell
+// c-2's result bit for bit, and the carried window state is unchanged; if
+// that result was the identity (the updated cell equal to its input), cell
+// c-1 keeps its input and nothing needs evaluating -- the same bits as
+// evaluating it (uniform flow, e.g. the quiescent gas ahead of a blast).  A
+// warp takes the shortcut only when all its lanes can (no divergence), in
+// either math policy; errors are reported by the first cell of a uniform run,
+// which is evaluated (later ones would fail identically at higher indices).
 template <class M, bool WANT_DT, int FLUX, class Src, class Sink>
 __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink, const Gas& g,
                                            double dtdx, double spacing,
@@ -220,12 +261,27 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
   memo.valid = src.memo_valid;
   Window w;
   auto none = [] { return Cons{}; };
-  int f = to_prim(m, src.load(ka - 2), g, w.wA);
+  int same = 0;         // consecutive loaded cells bitwise equal to their predecessor
+  bool idprev = false;  // the last update was the identity
+  // A warp whose last item had no uniform window at all (dense flow) stops
+  // testing for kSkipCool items: the cell compares cost ~5% where they never
+  // pay off.
+  constexpr int kSkipCool = 8;
+  const bool probe = HB_SKIP && src.skip_cool == 0;
+  bool saw = false;
+  Cons u = src.load(ka - 2);
+  int f = to_prim(m, u, g, w.wA);
   if (f >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka - 2 + kg) << 2) | f);
-  f = to_prim(m, src.load(ka - 1), g, w.wB);
+  {
+    const Cons u1 = src.load(ka - 1);
+    if (probe) same = same_bits(u1, u) ? 1 : 0;
+    u = u1;
+  }
+  f = to_prim(m, u, g, w.wB);
   if (f >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka - 1 + kg) << 2) | f);
   {  // c = ka-1: faces of the first halo cell
     const Cons uC = src.load(ka);
+    if (probe) same = same_bits(uC, u) ? same + 1 : 0;
     StepOut o;
     step_cell<0, false, FLUX>(m, w, uC, half, dtdx, spacing, g, none, o, memo);
     if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka + kg) << 2) | o.fC);
@@ -240,6 +296,7 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
   constexpr bool kFold = FLUX == 1 ? HB_FOLD_EXACT : HB_FOLD_HLLC;
   if constexpr (!kFold) {  // c = ka: faces of cell ka and the flux through its left interface
     const Cons uC = src.load(ka + 1);
+    if (probe) same = same_bits(uC, src.prev()) ? same + 1 : 0;
     StepOut o;
     step_cell<1, false, FLUX>(m, w, uC, half, dtdx, spacing, g, none, o, memo);
     if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(ka + 1 + kg) << 2) | o.fC);
@@ -254,8 +311,25 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
 #pragma unroll 1
   for (int c = kFold ? ka : ka + 1; c <= kb + 1; ++c) {
     const Cons uC = src.load(c + 1);
-    StepOut o;
     const bool upd = !kFold || c > ka;
+    if (probe) {
+      same = same_bits(uC, src.prev()) ? same + 1 : 0;
+      saw |= same >= 5;
+      // cells c-4..c+1 equal and the previous update the identity: cell c-1
+      // keeps its input (see the comment above)
+      if (__all_sync(0xffffffffu, (upd && same >= 5 && idprev) || !src.active)) {
+        StepOut o;
+        o.un = uC;  // == cell c-1, bit for bit
+        o.fU = -1;
+        o.fD = -1;
+        o.spd = 0.0;  // cell c-2's equal speed is already in the maximum
+        sink(c - 1, o);
+        if (src.active) src.count_skip();
+        src.boundary(c);
+        continue;
+      }
+    }
+    StepOut o;
     step_cell<2, WANT_DT, FLUX>(m, w, uC, half, dtdx, spacing, g,
                                 [&] { return src.reload(c - 1); }, o, memo, upd);
     if (o.fC >= 0) keep_min(ekey, key_base | ((unsigned long long)(c + 1 + kg) << 2) | o.fC);
@@ -264,6 +338,13 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
     if (upd) {
       if (o.fU >= 0)
         keep_min(ekey, key_base | (2ull << 20) | ((unsigned long long)(c - 1 + kg) << 2) | o.fU);
+      if (probe) {
+        // only worth knowing where the next window can be uniform
+        idprev = false;
+        if (__any_sync(0xffffffffu, same >= 4))
+          idprev = same >= 4 && o.fU < 0 && (!WANT_DT || o.fD < 0) &&
+                   same_bits(o.un, src.reload(c - 1));
+      }
       sink(c - 1, o);
     }
     src.boundary(c);
@@ -271,6 +352,10 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
     w.wB = o.wC;
     w.frPrev = o.fr;
     w.fluxPrev = o.F;
+  }
+  if (HB_SKIP) {
+    if (!probe) --src.skip_cool;
+    else if (!__any_sync(0xffffffffu, saw && src.active)) src.skip_cool = kSkipCool;
   }
   // the memo carries over to this thread's next work item only if its
   // entries are exact: written by an exact pass, or by a fast pass that kept
@@ -293,6 +378,13 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 #if HB_PDL
   asm volatile("griddepcontrol.launch_dependents;" :::);
 #endif
+}
+
+// The warp's count of uniform-window cell updates -> the sweep's counter.
+__device__ __forceinline__ void add_skipped(const SweepArgs& a, unsigned n) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if ((threadIdx.x & 31) == 0 && n && a.skipped) atomicAdd(a.skipped, (unsigned long long)n);
 }
 
 __device__ __forceinline__ bool latched(const SweepArgs& a) {
@@ -341,7 +433,7 @@ __device__ __forceinline__ int claim(unsigned* counter) {
 #define HB_X_MINB 4
 #endif
 #ifndef HB_Y_MINB
-#define HB_Y_MINB 4
+#define HB_Y_MINB 3  // the 8-cell ring (64 KB per CTA) allows 3 CTAs per SM anyway
 #endif
 #ifndef HB_EX_MINB  // exact-10 sweeps (long log/exp chains, ~200 registers)
 #define HB_EX_MINB 3
@@ -461,6 +553,9 @@ struct Tiles {
   // walker visits cells in order, so they advance by one slot per cell
   // instead of recomputing chunk/buffer indices.
   uint32_t lo_addr, wr_addr;
+  uint32_t last_addr, prev_addr;  // slots of the last two loaded cells (uniform-window test)
+  unsigned nskip;       // cell updates taken by the uniform-window identity (this warp)
+  int skip_cool;        // items left before this warp probes for uniform windows again
   uint32_t sw;          // this lane's TMA swizzle term (row sweep)
   int lo_pos, lo_buf, wr_pos, wr_buf;
   unsigned lo_par;      // mbarrier phase parity of the load cursor's buffer
@@ -516,6 +611,8 @@ struct Tiles {
   __device__ __forceinline__ Cons load(int) {
     if (lo_pos == 0) mbar_wait((uint64_t*)(hb_smem + full) + lo_buf, lo_par);
     const Cons u = get(lo_addr);
+    prev_addr = last_addr;
+    last_addr = lo_addr;
     lo_addr += kPosBytes;
     if (++lo_pos == C) {
       lo_pos = 0;
@@ -531,6 +628,12 @@ struct Tiles {
 
   // The cell being updated, again (staged; its slot is overwritten only by put).
   __device__ __forceinline__ Cons reload(int) { return get(wr_addr); }
+
+  // The cell loaded before the last one (its slot is rewritten only by the
+  // update two iterations after its load, and its chunk is not flushed
+  // before that).
+  __device__ __forceinline__ Cons prev() const { return get(prev_addr); }
+  __device__ __forceinline__ void count_skip() { ++nskip; }
 
   // The cell being updated, of strip `ln` (default: this lane's), receives u.
   __device__ __forceinline__ void put(int, const Cons& u, int ln = -1) {
@@ -592,6 +695,7 @@ struct Tiles {
     lo_pos = C - 2;
     lo_par = (q0 / NBUF) & 1u;
     lo_addr = base + b0 * kChunkBytes + (C - 2) * kPosBytes + lane * kLaneBytes;
+    last_addr = prev_addr = lo_addr;
     wr_buf = b1;
     wr_pos = 0;
     wr_addr = base + b1 * kChunkBytes + lane * kLaneBytes;
@@ -625,6 +729,8 @@ __device__ __forceinline__ Tiles<AXIS, FLUX> make_tiles(const CUtensorMap* load_
   t.memo_valid = false;
   t.lane = lane;
   t.q0 = 0;
+  t.nskip = 0;
+  t.skip_cool = 0;
   // row sweep, lane = box row of 8C bytes: SWIZZLE_32B (C = 4) flips the
   // 16-byte half of a row with address bit 7 (bit 2 of the row); SWIZZLE_64B
   // (C = 8) XORs the 16-byte unit index (bits 4-5) with bits 7-8 (row bits 1-2)
@@ -730,6 +836,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : HB_EX_MINB)
     if (active && r.key != kNoError) record(a.err, r.key);
   }
   if (lane == 0) bulk_wait0();
+  add_skipped(a, t.nskip);
 }
 
 // PEER: also store the halo rows into the neighbours' inboxes (peer-memory
@@ -850,6 +957,7 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : HB_EX_MINB) sweep
     }
   }
   if (lane == 0) bulk_wait0();
+  add_skipped(a, t.nskip);
   // peer stores performed system-wide before this kernel completes (the
   // neighbour reads them after the dt allreduce that follows on the stream)
   if (PEER && wrote_peer) __threadfence_system();

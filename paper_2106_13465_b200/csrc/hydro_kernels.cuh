@@ -86,6 +86,7 @@ struct SweepArgs {
   unsigned* counter_next;     // the other sweep's counter, reset for its launch
   double* halo_up;            // row sweep: upper neighbour's inbox block for rows 1..2
   double* halo_dn;            // row sweep: lower neighbour's inbox block for rows nx-1..nx
+  unsigned long long* skipped;  // cell updates taken by the uniform-window identity (counter)
 };
 
 struct TmaMaps {

@@ -408,6 +408,13 @@ class GpuGrid:
         return {"ms_x": ms[0].value, "ms_y": ms[1].value, "ms_other": ms[2].value,
                 "n_x": n[0].value, "n_y": n[1].value, "n_other": n[2].value}
 
+    def skipped(self) -> tuple[int, int]:
+        """Cell updates of the (column, row) sweeps since reset_counters() taken
+        by the uniform-window identity (hydro_gpu_skipped)."""
+        x, y = C.c_uint64(), C.c_uint64()
+        self._check(self._lib.hydro_gpu_skipped(self._ctx, C.byref(x), C.byref(y)))
+        return x.value, y.value
+
     def reset_counters(self):
         self._check(self._lib.hydro_gpu_reset_counters(self._ctx))
 

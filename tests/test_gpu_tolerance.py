@@ -156,3 +156,36 @@ def test_tolerance_mode_redo_items_are_decomposition_invariant(gpu, scale, bc):
         assert np.array_equal(o, outs[0])
     if msg_ref is None:
         assert max_rel(outs[0][:, 2:74, 2:42], ref.u[:, 2:74, 2:42]) <= TOL
+
+
+@pytest.mark.parametrize("scale", [1e-310, 1e-200, 1e150])
+def test_tolerance_mode_extreme_densities_match_the_oracle(gpu, scale):
+    """The whole state scaled by `scale` (rho, momenta, E -- the same flow:
+    the Euler equations are invariant under rho, p -> a rho, a p at fixed
+    velocities): subnormal, tiny or huge densities and pressures, outside the
+    fast pass's envelope, so every item takes the redo pass, which must use
+    IEEE division and sqrt where the fast formulas cannot take the operands
+    (a flushed reciprocal seed of a subnormal density gave NaN velocities and
+    a false 'pres non-positive').  The reference accepts these states; the GPU
+    must too, within 1e-12 of the oracle and independent of the
+    segmentation."""
+    grid = P.make_case("random", 64, 48, MODEL, seed=23)
+    grid.planes *= scale
+    ref = O.Grid(grid.nx, grid.ny, grid.dx, grid.dy, grid.planes.copy())
+    dt_ref = O.run_sequential(ref, 3, "transmit")
+    outs, dts = [], []
+    for seg in ((0, 0), (8, 8), (64, 48)):
+        planes = grid.planes.copy()
+        with P.GpuGrid(64, 48, grid.dx, grid.dy, MODEL, "transmit", device=0, math="tolerance") as g:
+            g.tune(seg[0], seg[1], 0)
+            g.upload(planes)
+            dts.append(g.run(3))
+            g.download(planes)
+        outs.append(planes)
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    got, want = outs[0][:, 2:66, 2:50], ref.u[:, 2:66, 2:50]
+    assert np.isfinite(got).all()
+    # relative to the scale (the floored metric would pass tiny states trivially)
+    assert max_rel(got / scale, want / scale) <= 1e-10
+    assert abs(dts[0] - dt_ref) <= 1e-10 * dt_ref  # subnormal states carry ~44 bits
