@@ -447,6 +447,7 @@ class Measured:
         self.sync()
         kt = self.grid.kernel_times()
         kt["ms_comm"], kt["n_comm"] = self.grid.comm_times()
+        kt["skipped_x"], kt["skipped_y"] = self.grid.skipped()
         self.grid.set_timing(False)
         return kt
 
@@ -599,6 +600,12 @@ def measure_line(env, workload, flux, math, steps, warmup, *, e2e=True, clocks=N
     if m.halo:
         out["config"]["halo"] = m.halo
         out["config"]["driver"] = m.driver
+    local = m.geo.nx * m.ny
+    out["uniform_window_identity"] = {
+        "sweep_x": kt["skipped_x"] / max(1, local * kt["n_x"]),
+        "sweep_y": kt["skipped_y"] / max(1, local * kt["n_y"]),
+        "note": "share of cell updates the bitwise sweeps took by the uniform-window identity "
+                "(DESIGN.md 3.1: same bits as evaluating them); the tolerance sweeps evaluate every cell"}
     if kt.get("n_comm"):
         # device time of the per-step exchange (dt allreduce + inbox copy), max
         # over ranks: the communication the step exposes
@@ -846,6 +853,7 @@ def main():
             "gpu_launches": head["gpu_launches"],
             "kernel_ms": head["kernel_ms"],
             "comm_us_per_step": head.get("comm_us_per_step"),
+            "uniform_window_identity": head.get("uniform_window_identity"),
             "clocks": head["clocks"],
             "cpu_baseline": cpu,
             "result_digest": head["result_digest"],

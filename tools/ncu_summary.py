@@ -28,6 +28,7 @@ KEYS = {
     "sm_clock_hz": "smsp__cycles_elapsed.avg.per_second",
     "l1_hit_pct": "l1tex__t_sector_hit_rate.pct",
     "l2_hit_pct": "lts__t_sector_hit_rate.pct",
+    "l2_read_sectors_from_sm": "lts__t_sectors_srcunit_tex_op_read.sum",
 }
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1,
          "msecond": 1e3, "ns": 1e-3, "us": 1, "ms": 1e3, "s": 1e6,
@@ -67,6 +68,8 @@ def kernel_metrics(rep, cells):
         m["top_stalls"] = [(s, round(v, 3)) for v, s in sorted(stalls, reverse=True)[:6]]
         if "dram_read" in m and "dram_write" in m:
             m["dram_bytes"] = m["dram_read"] + m["dram_write"]
+        if "l2_read_sectors_from_sm" in m:
+            m["l2_read_bytes_from_sm"] = 32 * m["l2_read_sectors_from_sm"]
         if cells and "sweep" in m["kernel"]:
             m["alg_bytes"] = 64 * cells
             m["thread_inst_per_cell"] = m.get("inst_executed", 0) * 32 / cells
