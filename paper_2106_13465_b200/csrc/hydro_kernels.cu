@@ -176,10 +176,17 @@ __device__ __forceinline__ void step_cell(M& m, const Window& w, const Cons& uC,
   o.fr = face_prim(m, er, w.wB, g);
   if (STAGE >= 2 && upd) {
     o.un = old();
-    Recip rn;
-    UpdAux aux;
-    o.fU = update_cell(m, o.un, w.fluxPrev, o.F, dtdx, rn, aux);
-    if (WANT_DT) o.fD = dt_speed(m, o.un, rn, aux, g, o.spd);
+#ifdef HB_TOLERANCE
+    if constexpr (!WANT_DT) {
+      o.fU = update_cell_nodt(m, o.un, w.fluxPrev, o.F, dtdx);
+    } else
+#endif
+    {
+      Recip rn;
+      UpdAux aux;
+      o.fU = update_cell(m, o.un, w.fluxPrev, o.F, dtdx, rn, aux);
+      if (WANT_DT) o.fD = dt_speed(m, o.un, rn, aux, g, o.spd);
+    }
   }
 }
 
