@@ -214,3 +214,46 @@ def test_gather_of_cut_slabs_is_identity():
     for world in (1, 2, 5):
         parts = [S.slab_planes(full, NX, world, r) for r in range(world)]
         assert np.array_equal(S.gather_planes(parts, NX, NY), full)
+
+
+def _digest_worker(rank, world, port, case, bc, outdir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    full = O.make_case(case, NX, NY, seed=6)
+    geo = S.SlabGeometry(NX, NY, rank, world)
+    sl = OracleSlab(geo, S.slab_planes(full.u, NX, world, rank), full.dx, full.dy, bc)
+    comm = S.TorchComm()
+    # the C++ schedule needs NCCL: over gloo every rank stays on the Python one
+    assert comm.setup_native(sl) is False and not comm.native
+    S.run_slab(sl, comm, STEPS)
+
+    def send(h, to):
+        dist.send(torch.tensor([h - (1 << 64) if h >= (1 << 63) else h], dtype=torch.int64), to)
+
+    def recv(frm):
+        t = torch.zeros(1, dtype=torch.int64)
+        dist.recv(t, frm)
+        return int(t.item()) & ((1 << 64) - 1)
+
+    planes = np.ascontiguousarray(sl.g.u)
+    h = S.chained_digest(planes, geo.nx, NY, rank, world, send, recv)
+    if rank == world - 1:
+        with open(os.path.join(outdir, "digest"), "w") as f:
+            f.write(f"{h:016x}")
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,case,bc", [(2, "random", "transmit"), (3, "corner_blast", "reflect")])
+def test_chained_slab_digest_is_the_grid_digest(world, case, bc):
+    """The reference's byte-serial FNV-1a digest (audit.cpp:53-76) of a grid
+    held as row slabs, chained over the ranks plane by plane without gathering
+    the grid (bench.py gates multi-rank runs on it), equals the digest of the
+    single-domain run."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_digest_worker, args=(world, _free_port(), case, bc, d), nprocs=world, join=True)
+        got = open(os.path.join(d, "digest")).read()
+    ref = O.make_case(case, NX, NY, seed=6)
+    O.run_sequential(ref, STEPS, bc)
+    assert got == f"{O.digest(ref):016x}"
