@@ -21,7 +21,8 @@
 // (tests/test_exact_flux.py).  Divisions and square roots go through the
 // walker's math policy M: FastMath (bitwise the IEEE result in its proven
 // range, else the work item is redone) or ExactMath (the compiler's IEEE
-// operations).
+// operations); in the tolerance TU the loose TolFast / TolExact policies
+// (hydro_physics_tol.cuh), whose results are tolerance-checked, not bitwise.
 #pragma once
 
 #include <cstdint>

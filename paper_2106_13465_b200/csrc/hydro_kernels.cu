@@ -951,7 +951,10 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : HB_EX_MINB) sweep
     };
     OkKey r = pass(FastMath{});
     // a fast path left its proven range somewhere: the warp redoes the item
-    // with the compiler's IEEE division/sqrt (restaging and overwriting all)
+    // with the exact policy (restaging and overwriting all): the compiler's
+    // IEEE division/sqrt in the bitwise TU; in the tolerance TU the same
+    // formulas as the fast pass wherever their operands are in range and IEEE
+    // outside it, with the reference's branches and error reports
     if (!__all_sync(0xffffffffu, r.ok || !active)) {
       if (lane == 0) bulk_wait0();  // the fast pass's stores have landed
       __syncwarp();
