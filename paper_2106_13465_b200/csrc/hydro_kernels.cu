@@ -274,7 +274,9 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
   // testing for kSkipCool items: the cell compares cost ~5% where they never
   // pay off.
   constexpr int kSkipCool = 8;
-  const bool probe = HB_SKIP && src.skip_cool == 0;
+  // the exact-10 sweeps take it in both TUs (their uniform cells cost a memo hit each)
+  constexpr bool kSkip = HB_SKIP || FLUX == 1;
+  const bool probe = kSkip && src.skip_cool == 0;
   bool saw = false;
   Cons u = src.load(ka - 2);
   int f = to_prim(m, u, g, w.wA);
@@ -360,7 +362,7 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
     w.frPrev = o.fr;
     w.fluxPrev = o.F;
   }
-  if (HB_SKIP) {
+  if (kSkip) {
     if (!probe) --src.skip_cool;
     else if (!__any_sync(0xffffffffu, saw && src.active)) src.skip_cool = kSkipCool;
   }
