@@ -213,6 +213,17 @@ __device__ __forceinline__ void keep_min(unsigned long long& k, unsigned long lo
 // iterations are peeled, so a segment costs its cells plus two primitive
 // conversions, two face reconstructions and one flux.  Returns false if a
 // FastMath operation left its proven range somewhere in the segment.
+// Main-loop unroll: 2 for the tolerance row sweep (its 168-register budget
+// holds the renamed window: -2..6% on configs 1-2), 1 elsewhere (the column
+// sweeps spill at their 128-register cap, the bitwise row sweep runs slower).
+#ifndef HB_UNROLL
+#ifdef HB_TOLERANCE
+#define HB_UNROLL 2
+#else
+#define HB_UNROLL 1
+#endif
+#endif
+
 __device__ __forceinline__ bool same_bits(const Cons& a, const Cons& b) {
   return (__double_as_longlong(a.r) == __double_as_longlong(b.r)) &
          (__double_as_longlong(a.ma) == __double_as_longlong(b.ma)) &
@@ -317,7 +328,8 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
     w.frPrev = o.fr;
     w.fluxPrev = o.F;
   }
-#pragma unroll 1
+  constexpr int kUnroll = (WANT_DT && FLUX == 0) ? HB_UNROLL : 1;
+#pragma unroll kUnroll
   for (int c = kFold ? ka : ka + 1; c <= kb + 1; ++c) {
     const Cons uC = src.load(c + 1);
     const bool upd = !kFold || c > ka;
