@@ -1244,13 +1244,14 @@ __global__ void math_selftest_kernel(int op, const double* a, const double* b, d
 // Segment length for the persistent sweeps: about kItemsPerWarp work items
 // per resident warp (dynamic balance), 16..128 cells, whole row-sweep chunks.
 constexpr int kItemsPerWarp = 8;
-int pick_seg(int n, int strips, int warps, int chunk) {
+int pick_seg(int n, int strips, int warps, int chunk, int items_per_warp = kItemsPerWarp,
+             int max_seg = 128) {
   const long long groups = (strips + 31) / 32;
-  long long segs = (long long)warps * kItemsPerWarp / (groups > 0 ? groups : 1);
+  long long segs = (long long)warps * items_per_warp / (groups > 0 ? groups : 1);
   if (segs < 1) segs = 1;
   long long seg = (n + segs - 1) / segs;
   if (seg < 16) seg = 16;
-  if (seg > 128) seg = 128;
+  if (seg > max_seg) seg = max_seg;
   seg = (seg + chunk - 1) / chunk * chunk;
   // small grids: 16-cell segments leave warps without work, and a segment
   // is a sequential walk, so trade halo recomputation for parallelism --
@@ -1266,11 +1267,11 @@ int pick_seg(int n, int strips, int warps, int chunk) {
 // bands' worth of items per wave of resident warps (the resident warps then
 // touch ~2 x warps/nseg strip groups at a time), band > 0 is an override
 // (>= groups: segment-major over all strips).
-int pick_band(int band, int strips, int nseg, int warps) {
+int pick_band(int band, int strips, int nseg, int warps, int div = 2) {
   const int groups = (strips + 31) / 32;
   if (band > 0) return band < groups ? band : groups;
   long long b = ((long long)warps + nseg - 1) / nseg;
-  b = (b + 1) / 2;
+  b = (b + div - 1) / div;
   if (b < 1) b = 1;
   return (int)(b < groups ? b : groups);
 }
@@ -1391,10 +1392,14 @@ void HB_SWEEP(launch_sweep_y)(const SweepArgs& a0, const TmaMaps& maps, const Ge
   SweepArgs a = a0;
   const int ctas = geo.sms * (a.flux == 1 ? geo.ctas_y_exact : geo.ctas_y_per_sm);
   const int C = a.flux == 1 ? Staging<1, 1>::C : Staging<1>::C;
-  if (a.seg <= 0) a.seg = pick_seg(a.ny, a.nx, ctas * 4, C);
+  // row sweep (HLLC): segments of at most 64 cells in narrow bands of row
+  // groups -- the resident warps then read neighbouring 64-byte pieces of the
+  // same grid rows (config 3 -4%, config 2 -4%, config 4 +1..3%)
+  if (a.seg <= 0)
+    a.seg = a.flux == 1 ? pick_seg(a.ny, a.nx, ctas * 4, C) : pick_seg(a.ny, a.nx, ctas * 4, C, 16, 64);
   a.seg = (a.seg + C - 1) / C * C;  // chunks never straddle segments
   a.nseg = (a.ny + a.seg - 1) / a.seg;
-  a.band = pick_band(a.band, a.nx, a.nseg, ctas * 4);
+  a.band = pick_band(a.band, a.nx, a.nseg, ctas * 4, a.flux == 1 ? 2 : 3);
   const bool peer = a.halo_up || a.halo_dn;
   if (a.flux == 1) {
     if (peer) launch_sweep(sweep_y_kernel<1, true>, ctas, kExYSmemBytes, s, a, maps.ey_load, maps.ey_store);
