@@ -248,6 +248,7 @@ void enqueue_x(hydro_gpu_ctx* c, int step, int explicit_dt, double dt) {
   ev_begin(c, &e0);
   if (c->math == HYDRO_GPU_MATH_TOLERANCE) hb::launch_sweep_x_tol(a, c->maps, c->geo_tol, c->stream);
   else hb::launch_sweep_x(a, c->maps, c->geo, c->stream);
+  hb::launch_ghost_fix(c->B, c->pitch, c->cfg.nx, c->cfg.ny, c->cfg.bc, c->stream);
   ev_end(c, e0, 0);
 }
 
@@ -578,8 +579,10 @@ int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out) {
   // rows -1..nx+2 plus one padding row read by the column sweep's prefetch
   ctx->count = (size_t)(c.nx + 5) * 4 * ctx->pitch;
   const size_t bytes = ctx->count * sizeof(double);
+  // U_b is tiled in 32-row blocks (hb::tile_index)
+  const size_t bytes_b = (size_t)hb::tile_rows(c.nx) * (ctx->pitch / 8) * 8192;
   if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaMalloc(&ctx->A, bytes) != cudaSuccess || cudaMalloc(&ctx->B, bytes) != cudaSuccess ||
+      cudaMalloc(&ctx->A, bytes) != cudaSuccess || cudaMalloc(&ctx->B, bytes_b) != cudaSuccess ||
       cudaMalloc(&ctx->slots, kSlots * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMalloc(&ctx->inbox, 4 * 8 * ctx->pitch * sizeof(double)) != cudaSuccess) {
     hydro_gpu_destroy(ctx);
@@ -594,7 +597,7 @@ int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out) {
     return HYDRO_GPU_ERR_CUDA;
   }
   cudaMemsetAsync(ctx->A, 0, bytes, ctx->stream);
-  cudaMemsetAsync(ctx->B, 0, bytes, ctx->stream);
+  cudaMemsetAsync(ctx->B, 0, bytes_b, ctx->stream);
   cudaMemsetAsync(ctx->inbox, 0, 4 * 8 * ctx->pitch * sizeof(double), ctx->stream);
   cudaMemsetAsync(ctx->slots, 0xff, 4 * sizeof(unsigned long long), ctx->stream);
   cudaMemsetAsync(ctx->slots + kSlotCounters, 0, 3 * sizeof(unsigned long long), ctx->stream);

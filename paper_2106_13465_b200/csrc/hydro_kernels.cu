@@ -500,6 +500,23 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                          int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store5(const CUtensorMap* map, const void* src, int c0, int c1,
+                                           int c2, int c3, int c4) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::
+                   "l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
+}
+
 __device__ __forceinline__ void tma_store(const CUtensorMap* map, const void* src, int c0, int c1,
                                           int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::
@@ -549,12 +566,12 @@ struct Tiles {
   static constexpr int kVarBytes = 32 * C * 8;  // row sweep: one variable of a chunk
   static_assert(NBUF >= 2 && NBUF <= 4, "ring of 2-4 buffers");
   // smem bytes between consecutive cells of a strip / adjacent strips
-  // AXIS 0: one box {32 cols, 4 vars, C rows} per chunk, slot
-  //   [pos][var][lane]; AXIS 1: one box {C cols, 1 var, 32 rows} per
-  //   variable, slot [var][lane][pos].
-  static constexpr uint32_t kPosBytes = AXIS == 0 ? 4 * 32 * 8 : 8;
+  // AXIS 0: one box {32 cols, C rows, 4 vars} per chunk, slot
+  //   [var][pos][lane]; AXIS 1: one tiled block {C cols, 32 rows, 4 vars},
+  //   slot [var][lane][pos].
+  static constexpr uint32_t kPosBytes = 8 * (AXIS == 0 ? 32 : 1);
   static constexpr uint32_t kLaneBytes = AXIS == 0 ? 8 : C * 8;
-  static constexpr uint32_t kVarStride = AXIS == 0 ? 32 * 8 : kVarBytes;
+  static constexpr uint32_t kVarStride = AXIS == 0 ? C * 32 * 8 : kVarBytes;
 
   const CUtensorMap* load_map;
   const CUtensorMap* store_map;
@@ -600,17 +617,21 @@ struct Tiles {
     mbar_expect_tx(bar(q), kChunkBytes);
     const int k = ka - C + q * C;
     if constexpr (AXIS == 0) {
-      tma_load(buf(q), load_map, bar(q), c0(k), 0, c2(k));
+      // U_a: box {32 cols, 4 rows, 4 vars} at plane row k -> smem [var][row][col]
+      tma_load(buf(q), load_map, bar(q), c0(k), k, 0);
     } else {
-#pragma unroll
-      for (int v = 0; v < 4; ++v) tma_load(buf(q) + v * kVarBytes, load_map, bar(q), c0(k), v, c2(k));
+      // tiled U_b: the item's block row (s0 - 1) / 32, the chunk's column block
+      const int col = c0(k);
+      tma_load5(buf(q), load_map, bar(q), col & 7, col >> 3, 0, 0, (s0 + 31) >> 5);
     }
   }
 
   __device__ __forceinline__ void store(int t) {  // lane 0 only
     const int k = ka - C + t * C;
     if constexpr (AXIS == 0) {
-      tma_store(store_map, buf(t), c0(k), 0, c2(k));
+      // tiled U_b: 4 column blocks x grid rows k-1 .. k+2 (one block row)
+      const int r = k - 2;  // grid row - 1 of the chunk's first row (>= 0 for stored chunks)
+      tma_store5(store_map, buf(t), 0, c0(k) >> 3, r & 31, 0, (r >> 5) + 1);
     } else {
 #pragma unroll
       for (int v = 0; v < 4; ++v) tma_store(store_map, buf(t) + v * kVarBytes, c0(k), v, c2(k));
@@ -814,32 +835,38 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : HB_EX_MINB)
     auto pass = [&](auto math) {
       using M = decltype(math);
       t.begin();
-      auto put = [&](int i, int jj, const Cons& u, bool neg) {
-        double* q = dst + cell_index(pitch, 0, i, jj);
-        q[0] = u.r;
-        q[pitch] = u.ma;
-        q[2 * pitch] = neg ? -u.mb : u.mb;
-        q[3 * pitch] = u.e;
+      // ghost columns of U_b (tiled): inside this warp's store box (its 32
+      // columns) a ghost goes into the slot of the lane that holds that
+      // column -- an inactive lane, whose slot the TMA store writes -- else
+      // straight to memory (a block no store box covers)
+      auto put = [&](int k, int i, int jt, const Cons& u, bool neg) {
+        Cons gh = u;
+        if (neg) gh.mb = -gh.mb;
+        const int d = jt - j0;
+        if (d >= 0 && d < 32) {
+          t.put(k, gh, d);
+          return;
+        }
+        // a column inside another warp's store box (reflecting walls with
+        // ny % 32 == 1: ghost ny+2 mirrors column ny-1 of the previous group)
+        // is written after the sweep by ghost_fix_kernel
+        if (jt > ny && ((jt - 1) >> 5) < groups) return;
+        double* q = dst + tile_index(pitch, 0, i, jt);
+        q[0] = gh.r;
+        q[256] = gh.ma;
+        q[512] = gh.mb;
+        q[768] = gh.e;
       };
       auto sink = [&](int k, const StepOut& o) {
         if (active) t.put(k, o.un);
         if (edge && active) {  // y-wall ghosts of the column-sweep output (grid.cpp:44-59)
           const int i = k - 1;
           if (refl) {
-            if (j <= 2) put(i, 1 - j, o.un, true);
-            if (j >= ny - 1) put(i, 2 * ny + 1 - j, o.un, true);
+            if (j <= 2) put(k, i, 1 - j, o.un, true);
+            if (j >= ny - 1) put(k, i, 2 * ny + 1 - j, o.un, true);
           } else {
-            if (j == 1) { put(i, 0, o.un, false); put(i, -1, o.un, false); }
-            if (j == ny) { put(i, ny + 1, o.un, false); put(i, ny + 2, o.un, false); }
-          }
-          // For odd ny the store box's last 16-byte unit (TMA clips stores at
-          // that granularity along the inner dimension) also covers ghost
-          // column ny+1: its slot gets the same ghost value the direct store
-          // above writes, so both writes agree.
-          if ((ny & 1) && j == ny) {
-            Cons gh = o.un;
-            if (refl) gh.mb = -gh.mb;
-            t.put(k, gh, lane + 1);
+            if (j == 1) { put(k, i, 0, o.un, false); put(k, i, -1, o.un, false); }
+            if (j == ny) { put(k, i, ny + 1, o.un, false); put(k, i, ny + 2, o.un, false); }
           }
         }
       };
@@ -1090,6 +1117,19 @@ __global__ void __launch_bounds__(256) HB_SWEEP(prologue_kernel)(PrologueArgs a)
 }
 
 #ifndef HB_TOLERANCE
+// The one ghost column of the tiled U_b the column sweep cannot store: with
+// reflecting walls and ny % 32 == 1, ghost column ny+2 (the mirror of column
+// ny-1, grid.cpp:44-59) lies in the last column group's store box while its
+// source column belongs to the previous group.
+__global__ void ghost_fix_kernel(double* __restrict__ b, size_t pitch, int nx, int ny) {
+  const int i = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > nx) return;
+  for (int v = 0; v < 4; ++v) {
+    const double x = b[tile_index(pitch, v, i, ny - 1)];
+    b[tile_index(pitch, v, i, ny + 2)] = v == 2 ? -x : x;
+  }
+}
+
 // End-of-run ghosts: the reference's last apply_boundary ran on the column
 // sweep output, so every ghost band mirrors U_b (grid.cpp:23-60).
 __global__ void finish_kernel(FinishArgs a) {
@@ -1105,7 +1145,7 @@ __global__ void finish_kernel(FinishArgs a) {
       for (int s = 0; s < 2; ++s) {
         if (!on[s]) continue;
         for (int v = 0; v < 4; ++v) {
-          const double x = a.post_x[cell_index(pitch, v, srcs[s], j)];
+          const double x = a.post_x[tile_index(pitch, v, srcs[s], j)];
           a.u[cell_index(pitch, v, gh[s], j)] = (refl && v == 1) ? -x : x;
         }
       }
@@ -1115,7 +1155,7 @@ __global__ void finish_kernel(FinishArgs a) {
     const int cols[4] = {-1, 0, a.ny + 1, a.ny + 2};
     for (int c = 0; c < 4; ++c)
       for (int v = 0; v < 4; ++v)
-        a.u[cell_index(pitch, v, i, cols[c])] = a.post_x[cell_index(pitch, v, i, cols[c])];
+        a.u[cell_index(pitch, v, i, cols[c])] = a.post_x[tile_index(pitch, v, i, cols[c])];
   }
 }
 
@@ -1312,45 +1352,48 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
       return false;
     encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
   }
-  const cuuint64_t strides[2] = {pitch * 8, 4 * pitch * 8};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  // loads: the whole state buffer (ghost rows/columns included; boxes
-  // reaching past it are zero-filled)
-  const cuuint64_t dim_load[3] = {pitch, 4, (cuuint64_t)nx + 4};
-  // stores: interior only -- rows up to nx and column offsets up to j = ny,
-  // so tail items past the grid are clipped (ghosts are written separately)
-  const cuuint64_t dim_store[3] = {(cuuint64_t)ny + 1 + kColOff, 4, (cuuint64_t)nx + 2};
-  // column-sweep stores: the inner extent rounded up to whole 16-byte units,
-  // which is what TMA writes; the odd ghost column ny+1 this adds carries the
-  // ghost value (sweep_x_tma_kernel)
-  const cuuint64_t dim_xstore[3] = {((cuuint64_t)ny + 2 + kColOff) & ~(cuuint64_t)1, 4,
-                                    (cuuint64_t)nx + 2};
-  // L2 promotion per map (experiment knob HB_PROMO="x_load,x_store,y_load,y_store",
-  // 0 none, 1 64B, 2 128B, 3 256B; default 128B everywhere)
-  int promo[4] = {2, 2, 2, 2};
-  if (const char* e = getenv("HB_PROMO")) sscanf(e, "%d,%d,%d,%d", &promo[0], &promo[1], &promo[2], &promo[3]);
-  const CUtensorMapL2promotion pk[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
-                                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
-  auto enc = [&](CUtensorMap* m, double* base, const cuuint64_t* dim, const cuuint32_t* box,
-                 CUtensorMapSwizzle swz, int which) {
-    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dim, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                  pk[promo[which] & 3], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-           CUDA_SUCCESS;
+  auto enc = [&](CUtensorMap* m, int rank, double* base, const cuuint64_t* dim,
+                 const cuuint64_t* strides, const cuuint32_t* box, CUtensorMapSwizzle swz) {
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, base, dim, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
-  const cuuint32_t box_y[3] = {(cuuint32_t)Staging<1>::C, 1, 32};  // row sweep: C cols x 32 rows
-  const cuuint32_t box_ey[3] = {(cuuint32_t)Staging<1, 1>::C, 1, 32};
-  const cuuint32_t box_x[3] = {32, 4, (cuuint32_t)Staging<0>::C};  // column sweep: 32 cols x 4 vars x C rows
-  // row sweep: 32-byte box rows swizzled (halves the smem bank conflicts of
-  // lane-per-row accesses); column sweep: 256-byte rows are conflict-free
+  // U_a (row-interleaved planes), dims {column, var, plane row}: the row
+  // sweep's stores, interior only -- rows up to nx and column offsets up to
+  // j = ny, so tail items past the grid are clipped (ghosts are written
+  // separately)
+  const cuuint64_t a_str[2] = {pitch * 8, 4 * pitch * 8};
+  const cuuint64_t dim_store[3] = {(cuuint64_t)ny + 1 + kColOff, 4, (cuuint64_t)nx + 2};
+  // ... and the column sweep's loads, dims {column, plane row, var} (strides
+  // not increasing: the box lands as smem [var][row][column], the order of
+  // the tiled U_b blocks it is stored to); boxes reaching past the buffer
+  // are zero-filled
+  const cuuint64_t dim_xload[3] = {pitch, (cuuint64_t)nx + 4, 4};
+  const cuuint64_t xl_str[2] = {4 * pitch * 8, pitch * 8};
+  // tiled U_b (tile_index), dims {column in block, column block, row in
+  // block, var, block row}
+  const cuuint64_t ntj = pitch / 8;
+  const cuuint64_t dim_b[5] = {8, ntj, 32, 4, (cuuint64_t)tile_rows(nx)};
+  const cuuint64_t b_str[4] = {8192, 64, 2048, 8192 * ntj};
+  constexpr int CX = Staging<0>::C, CY = Staging<1>::C, CE = Staging<1, 1>::C;
+  const cuuint32_t box_xload[3] = {32, (cuuint32_t)CX, 4};
+  const cuuint32_t box_xstore[5] = {8, 4, (cuuint32_t)CX, 4, 1};  // 32 columns x CX rows x 4 vars
+  const cuuint32_t box_yload[5] = {(cuuint32_t)CY, 1, 32, 4, 1};  // one block (C = 8)
+  const cuuint32_t box_eyload[5] = {(cuuint32_t)CE, 1, 32, 4, 1};
+  const cuuint32_t box_y[3] = {(cuuint32_t)CY, 1, 32};           // row sweep stores: C cols x 32 rows
+  const cuuint32_t box_ey[3] = {(cuuint32_t)CE, 1, 32};
+  // row sweep: 64-byte (32-byte) box rows swizzled against the smem bank
+  // conflicts of lane-per-row accesses; column sweep: 256-byte rows are
+  // conflict-free
   auto swz = [](int c) { return c == 4 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B; };
-  const CUtensorMapSwizzle sy = swz(Staging<1>::C), sey = swz(Staging<1, 1>::C),
-                           sx = CU_TENSOR_MAP_SWIZZLE_NONE;
-  return enc(&maps->ey_load, B, dim_load, box_ey, sey, 2) &&
-         enc(&maps->ey_store, A, dim_store, box_ey, sey, 3) &&
-         enc(&maps->y_load, B, dim_load, box_y, sy, 2) &&
-         enc(&maps->y_store, A, dim_store, box_y, sy, 3) &&
-         enc(&maps->x_load, A, dim_load, box_x, sx, 0) && enc(&maps->x_store, B, dim_xstore, box_x, sx, 1);
+  const CUtensorMapSwizzle none = CU_TENSOR_MAP_SWIZZLE_NONE;
+  return enc(&maps->x_load, 3, A, dim_xload, xl_str, box_xload, none) &&
+         enc(&maps->x_store, 5, B, dim_b, b_str, box_xstore, none) &&
+         enc(&maps->y_load, 5, B, dim_b, b_str, box_yload, swz(CY)) &&
+         enc(&maps->y_store, 3, A, dim_store, a_str, box_y, swz(CY)) &&
+         enc(&maps->ey_load, 5, B, dim_b, b_str, box_eyload, swz(CE)) &&
+         enc(&maps->ey_store, 3, A, dim_store, a_str, box_ey, swz(CE));
 }
 
 #endif  // !HB_TOLERANCE
@@ -1418,6 +1461,11 @@ void HB_SWEEP(launch_prologue)(const PrologueArgs& a, cudaStream_t s) {
 }
 
 #ifndef HB_TOLERANCE
+
+void launch_ghost_fix(double* b, size_t pitch, int nx, int ny, int bc, cudaStream_t s) {
+  if (bc != 0 || (ny & 31) != 1 || ny < 33) return;
+  ghost_fix_kernel<<<(nx + 255) / 256, 256, 0, s>>>(b, pitch, nx, ny);
+}
 
 void launch_finish(const FinishArgs& a, cudaStream_t s) {
   const int n = a.nx + a.ny;

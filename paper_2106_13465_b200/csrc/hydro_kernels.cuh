@@ -54,6 +54,25 @@ __host__ __device__ __forceinline__ size_t cell_index(size_t pitch, int v, int i
   return ((size_t)(i + 1) * 4 + (size_t)v) * pitch + (size_t)(j + kColOff);
 }
 
+// The column-sweep output U_b (read only by the row sweep and the end-of-run
+// ghost pass) is stored TILED: blocks of 32 grid rows x 8 columns x 4
+// variables (8 KB), block (ti, tj) at ((ti + 1) * (pitch / 8) + tj) * 1024
+// doubles, element [v][ri][rj] inside, with ti = floor((i - 1) / 32),
+// ri = i - 1 - 32 ti, tj = (j + kColOff) / 8, rj = (j + kColOff) % 8.  A
+// row-sweep chunk (32 rows of one row group x 8 columns x 4 variables) is
+// then one contiguous 8 KB block, and a column-sweep chunk (4 rows x 32
+// columns) sixteen 256-byte pieces (tools/tma_pattern.cu: the row sweep's
+// 64-byte box rows streamed at 4.4 TB/s, the tiled blocks at 6.6 TB/s).
+__host__ __device__ __forceinline__ size_t tile_index(size_t pitch, int v, int i, int j) {
+  const int ti = (i + 31) / 32 - 1;  // floor((i - 1) / 32) for i >= -31
+  const int ri = i - 1 - 32 * ti;
+  const int c = j + kColOff;
+  return (((size_t)(ti + 1) * (pitch / 8) + (size_t)(c >> 3)) * 4 + (size_t)v) * 256 +
+         (size_t)ri * 8 + (size_t)(c & 7);
+}
+// Tile rows of U_b: grid rows -1 .. nx+2.
+__host__ __device__ __forceinline__ int tile_rows(int nx) { return (nx + 1) / 32 + 2; }
+
 inline size_t pitch_for(int ny) {
   const size_t need = (size_t)ny + 3 + kColOff;  // offsets 0..ny+2+kColOff
   return (need + 15) / 16 * 16;        // 128-byte rows
@@ -90,12 +109,12 @@ struct SweepArgs {
 };
 
 struct TmaMaps {
-  CUtensorMap y_load;         // U_b, box {Staging<1>::C cols, 1 var, 32 rows}
-  CUtensorMap y_store;        // U_a interior rows/cols only (clips ghosts)
-  CUtensorMap x_load;         // U_a, box {32 cols, 4 vars, 4 rows}
-  CUtensorMap x_store;        // U_b interior only
-  CUtensorMap ey_load;        // the exact-10 row sweep's maps: box {4 cols, 1 var, 32 rows}
-  CUtensorMap ey_store;
+  CUtensorMap y_load;         // U_b (tiled), one 8 KB block {8 cols, 32 rows, 4 vars}
+  CUtensorMap y_store;        // U_a interior rows/cols only (clips ghosts), box {8 cols, 1 var, 32 rows}
+  CUtensorMap x_load;         // U_a, box {32 cols, 4 rows, 4 vars} -> smem [var][row][col]
+  CUtensorMap x_store;        // U_b (tiled), box {8 cols, 4 blocks, 4 rows, 4 vars}
+  CUtensorMap ey_load;        // the exact-10 row sweep: U_b (tiled) {4 cols, 32 rows, 4 vars}
+  CUtensorMap ey_store;       // ... and U_a, box {4 cols, 1 var, 32 rows}
 };
 
 struct PrologueArgs {
@@ -147,6 +166,9 @@ void launch_sweep_y_tol(const SweepArgs& a, const TmaMaps& maps, const Geometry&
 void launch_prologue(const PrologueArgs& a, cudaStream_t s);
 void launch_prologue_tol(const PrologueArgs& a, cudaStream_t s);  // the tolerance mode's dt
 void launch_finish(const FinishArgs& a, cudaStream_t s);
+// The tiled U_b's ghost column ny+2 for reflecting walls with ny % 32 == 1
+// (no-op otherwise); after every column sweep.
+void launch_ghost_fix(double* b, size_t pitch, int nx, int ny, int bc, cudaStream_t s);
 void launch_init(const InitArgs& a, cudaStream_t s);
 void launch_row_audit(const double* u, size_t pitch, int nx, int ny, unsigned long long* hashes,
                       double* sums, cudaStream_t s);
