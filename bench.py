@@ -558,27 +558,13 @@ class Measured:
         self.grid.download_ptr([h[v].data_ptr() for v in range(4)], self.ny + 4)
         return self.digest_of(h)
 
-    def state_view(self):
-        """The interior of the device state as a (rows, 4, ny) torch view."""
-        ptr, pitch = self.grid.state()
-        off = self.grid.col_offset() + 1  # column j = 1
-        rows = self.geo.nx + 4
-        t = self.S.device_tensor(ptr, rows * 4 * pitch, device=self.env.torch.device("cuda", self.env.local))
-        return t.view(rows, 4, pitch)[2:self.geo.nx + 2, :, off:off + self.ny]
-
-    def max_rel_vs(self, other: "Measured", rows: int = 512) -> float:
+    def max_rel_vs(self, other: "Measured") -> float:
         """compare_tolerance max_rel (proj/src/audit.cpp:137-154) of this run's
-        final state against another's, on the device, max over ranks."""
-        torch = self.env.torch
+        final state against another's, on the device (hydro_gpu_compare), max
+        over ranks."""
         self.sync()
         other.sync()
-        a, b = self.state_view(), other.state_view()
-        out = 0.0
-        for i in range(0, a.shape[0], rows):
-            x, y = a[i:i + rows], b[i:i + rows]
-            den = torch.maximum(torch.maximum(x.abs(), y.abs()), torch.ones((), dtype=x.dtype, device=x.device))
-            out = max(out, float(((x - y).abs() / den).max().item()))
-        return self.env.allmax(out)
+        return self.env.allmax(self.grid.compare(other.grid))
 
 
 def measure_line(env, workload, flux, math, steps, warmup, *, e2e=True, clocks=None):

@@ -126,6 +126,14 @@ int hydro_gpu_last_error(const hydro_gpu_ctx* ctx, hydro_gpu_error* out);
 /* ---- state transfer (host <-> HBM) ------------------------------------- */
 int hydro_gpu_upload(hydro_gpu_ctx* ctx, const double* const planes[4],
                      size_t row_stride);
+/* Grid rows i_lo .. i_lo+nrows-1 (within -1 .. nx+2) of the 4 planes only;
+ * planes[v] points at grid row i_lo's column -1. */
+int hydro_gpu_download_rows(hydro_gpu_ctx* ctx, double* const planes[4], size_t row_stride,
+                            int i_lo, int nrows);
+/* compare_tolerance's max |a-b| / max(|a|,|b|,1) over the interior
+ * (proj/src/audit.cpp:137-154) of two contexts of one geometry on one
+ * device, computed on the device. */
+int hydro_gpu_compare(hydro_gpu_ctx* a, hydro_gpu_ctx* b, double* max_rel);
 int hydro_gpu_download(hydro_gpu_ctx* ctx, double* const planes[4],
                        size_t row_stride);
 /* The same transfers enqueued on the context's stream without waiting (see
@@ -182,6 +190,13 @@ int hydro_gpu_error_slot(hydro_gpu_ctx* ctx, uint64_t** dev_ptr);
  * variables x pitch), so a halo swap is one send/recv per neighbour. */
 int hydro_gpu_halo(hydro_gpu_ctx* ctx, double** send_lo, double** send_hi,
                    double** recv_lo, double** recv_hi, size_t* count);
+/* The collective halo transport: hydro_gpu_halo's four blocks (2 rows x 4
+ * variables, `count` doubles each, the inbox format) are a staging buffer of
+ * the tiled state: pack rows 1..2 / nx-1..nx into the send blocks before the
+ * sends, unpack the received blocks into ghost rows -1..0 / nx+1..nx+2
+ * after the receives (both on the context's stream). */
+int hydro_gpu_slab_halo_pack(hydro_gpu_ctx* ctx);
+int hydro_gpu_slab_halo_unpack(hydro_gpu_ctx* ctx);
 int hydro_gpu_slab_sweep_x(hydro_gpu_ctx* ctx, int step);
 int hydro_gpu_slab_sweep_y(hydro_gpu_ctx* ctx, int step);
 /* Peer-memory halo (row slabs on NVLink-connected GPUs; replaces the per-step
@@ -302,9 +317,11 @@ int hydro_gpu_set_math(hydro_gpu_ctx* ctx, int math);
  * in_range[k] = 1 where the fast path applied. */
 int hydro_gpu_math_selftest(int op, const double* a, const double* b, double* fast,
                             double* exact, int* in_range, size_t n);
-/* Device pointer to plane-interleaved storage and its pitch (doubles): cell
- * (i, j) of variable v, i and j in [-1, n+2], is element
- * ((i + 1) * 4 + v) * pitch + j + hydro_gpu_col_offset(). */
+/* Device pointer to the state and its pitch (doubles).  The state is tiled:
+ * blocks of 32 grid rows x 8 columns x 4 variables; cell (i, j) of variable
+ * v, i and j in [-1, n+2], with c = j + hydro_gpu_col_offset(),
+ * ti = floor((i - 1) / 32), ri = i - 1 - 32 ti, is element
+ * (((ti + 1) * (pitch / 8) + c / 8) * 4 + v) * 256 + ri * 8 + c % 8. */
 int hydro_gpu_state(hydro_gpu_ctx* ctx, double** dev_ptr, size_t* pitch);
 int hydro_gpu_col_offset(void);
 

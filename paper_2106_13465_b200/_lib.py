@@ -99,6 +99,10 @@ def lib() -> C.CDLL:
         "hydro_gpu_comm_attach": ([_ctx, C.c_void_p, i, i], i),
         "hydro_gpu_comm_times": ([_ctx, _dp, P(C.c_longlong)], i),
         "hydro_gpu_skipped": ([_ctx, P(u64), P(u64)], i),
+        "hydro_gpu_download_rows": ([_ctx, _planes, sz, i, i], i),
+        "hydro_gpu_compare": ([_ctx, _ctx, _dp], i),
+        "hydro_gpu_slab_halo_pack": ([_ctx], i),
+        "hydro_gpu_slab_halo_unpack": ([_ctx], i),
         "hydro_gpu_math_selftest": ([i, _dp, _dp, _dp, _dp, P(i), sz], i),
         "hydro_grid_digest": ([_planes, sz, i, i], u64),
         "hydro_grid_state_hash": ([_planes, sz, i, i], u64),

@@ -77,8 +77,10 @@ struct hydro_gpu_ctx {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   // pinned staging ring for pageable host planes (hydro_gpu_upload/download)
-  double* stage[2] = {nullptr, nullptr};
+  double* stage[2] = {nullptr, nullptr};     // pinned host
+  double* dstage[2] = {nullptr, nullptr};    // device (row format)
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  double* halo_buf = nullptr;                // send/recv blocks of the collective halo
 };
 
 namespace {
@@ -261,6 +263,7 @@ void enqueue_y(hydro_gpu_ctx* c, int step, int explicit_dt, double dt, int want_
   ev_begin(c, &e0);
   if (c->math == HYDRO_GPU_MATH_TOLERANCE) hb::launch_sweep_y_tol(a, c->maps, c->geo_tol, c->stream);
   else hb::launch_sweep_y(a, c->maps, c->geo, c->stream);
+  hb::launch_ghost_row_fix(c->A, c->pitch, c->cfg.nx, c->cfg.ny, c->cfg.bc, c->cfg.wall_hi, c->stream);
   ev_end(c, e0, 1);
 }
 
@@ -411,6 +414,16 @@ const NcclApi& nccl() {
       return set_err(c, HYDRO_GPU_ERR_CUDA, "NCCL: %s (%s)", nccl().error_string(r_), #expr); \
   } while (0)
 
+// Two grid rows of all four variables <-> a halo block (the inbox format:
+// element (r, v, j) at (4 r + v) pitch + j + kColOff; the row sweep's peer
+// stores write it): the state is tiled, so these are small kernels.
+void rows_to_block(hydro_gpu_ctx* c, int i0, double* blk) {
+  hb::launch_tiles_to_rows(c->A, c->pitch, blk, 0, -1, i0, 2, c->cfg.ny, c->stream);
+}
+void block_to_rows(hydro_gpu_ctx* c, const double* blk, int i0) {
+  hb::launch_rows_to_tiles(blk, 0, c->A, c->pitch, -1, i0, 2, c->cfg.ny, c->stream);
+}
+
 // The slab's per-step exchange (compute_dt_parallel's min, schedulers.cpp:47-65,
 // and the column sweep's InterfaceBuffer, decomposition.hpp:58-79): the step's
 // dt limit min-allreduced over the ranks (u64 min: positive doubles order like
@@ -422,15 +435,10 @@ int enqueue_exchange(hydro_gpu_ctx* c, int step) {
   ev_begin(c, &e0);
   unsigned long long* lim = c->slots + (step & 1);
   NCCL_TRY(c, nccl().all_reduce(lim, lim, 1, ncclUint64, ncclMin, c->comm, c->stream));
-  const size_t blk = 8 * c->pitch, rowblk = 4 * c->pitch, par = (size_t)(step & 1);
-  const size_t bytes = blk * sizeof(double);
-  if (!c->cfg.wall_lo)
-    CUDA_TRY(c, cudaMemcpyAsync(c->A, c->inbox + (par * 2 + 0) * blk, bytes,
-                                cudaMemcpyDeviceToDevice, c->stream));
-  if (!c->cfg.wall_hi)
-    CUDA_TRY(c, cudaMemcpyAsync(c->A + (size_t)(c->cfg.nx + 2) * rowblk,
-                                c->inbox + (par * 2 + 1) * blk, bytes, cudaMemcpyDeviceToDevice,
-                                c->stream));
+  const size_t blk = 8 * c->pitch, par = (size_t)(step & 1);
+  if (!c->cfg.wall_lo) block_to_rows(c, c->inbox + (par * 2 + 0) * blk, -1);
+  if (!c->cfg.wall_hi) block_to_rows(c, c->inbox + (par * 2 + 1) * blk, c->cfg.nx + 1);
+  CUDA_TRY(c, cudaGetLastError());
   ev_end(c, e0, 3);
   return HYDRO_GPU_OK;
 }
@@ -445,14 +453,10 @@ int enqueue_run(hydro_gpu_ctx* c, int steps) {
   const bool slab = c->comm != nullptr;
   enqueue_prologue(c, 1, 0, 0);
   if (slab && (c->peer_up || c->peer_dn)) {
-    const size_t blk = 8 * c->pitch, rowblk = 4 * c->pitch;
-    const size_t bytes = blk * sizeof(double);
-    if (c->peer_up)  // rows 1..2 -> the upper neighbour's inbox, parity 0
-      CUDA_TRY(c, cudaMemcpyAsync(c->peer_up + 1 * blk, c->A + 2 * rowblk, bytes,
-                                  cudaMemcpyDeviceToDevice, c->stream));
-    if (c->peer_dn)  // rows nx-1..nx -> the lower neighbour's inbox, parity 0
-      CUDA_TRY(c, cudaMemcpyAsync(c->peer_dn, c->A + (size_t)c->cfg.nx * rowblk, bytes,
-                                  cudaMemcpyDeviceToDevice, c->stream));
+    const size_t blk = 8 * c->pitch;
+    if (c->peer_up) rows_to_block(c, 1, c->peer_up + 1 * blk);  // rows 1..2, parity 0
+    if (c->peer_dn) rows_to_block(c, c->cfg.nx - 1, c->peer_dn);  // rows nx-1..nx
+    CUDA_TRY(c, cudaGetLastError());
   }
   for (int s = 0; s < steps; ++s) {
     if (slab) {
@@ -577,10 +581,9 @@ int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out) {
   cudaGetDevice(&ctx->device);
   ctx->pitch = hb::pitch_for(c.ny);
   // rows -1..nx+2 plus one padding row read by the column sweep's prefetch
-  ctx->count = (size_t)(c.nx + 5) * 4 * ctx->pitch;
+  ctx->count = hb::state_doubles(c.nx, ctx->pitch);  // tiled in 32-row blocks (hb::cell_index)
   const size_t bytes = ctx->count * sizeof(double);
-  // U_b is tiled in 32-row blocks (hb::tile_index)
-  const size_t bytes_b = (size_t)hb::tile_rows(c.nx) * (ctx->pitch / 8) * 8192;
+  const size_t bytes_b = bytes;
   if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&ctx->A, bytes) != cudaSuccess || cudaMalloc(&ctx->B, bytes_b) != cudaSuccess ||
       cudaMalloc(&ctx->slots, kSlots * sizeof(unsigned long long)) != cudaSuccess ||
@@ -622,7 +625,9 @@ int hydro_gpu_destroy(hydro_gpu_ctx* ctx) {
   if (ctx->slots) cudaFree(ctx->slots);
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
   if (ctx->inbox) cudaFree(ctx->inbox);
+  if (ctx->halo_buf) cudaFree(ctx->halo_buf);
   for (int b = 0; b < 2; ++b) {
+    if (ctx->dstage[b]) cudaFree(ctx->dstage[b]);
     if (ctx->stage[b]) cudaFreeHost(ctx->stage[b]);
     if (ctx->stage_ev[b]) cudaEventDestroy(ctx->stage_ev[b]);
   }
@@ -650,26 +655,18 @@ int hydro_gpu_set_stream(hydro_gpu_ctx* ctx, void* s) {
   return HYDRO_GPU_OK;
 }
 
-int hydro_gpu_upload_async(hydro_gpu_ctx* c, const double* const planes[4], size_t row_stride) {
-  if (!c || !planes) return HYDRO_GPU_ERR_CONFIG;
-  if (row_stride < (size_t)c->cfg.ny + 4)
-    return set_err(c, HYDRO_GPU_ERR_CONFIG, "row stride %zu below ny+4", row_stride);
-  DeviceGuard g(c->device);
-  for (int v = 0; v < 4; ++v) {
-    if (!planes[v]) return set_err(c, HYDRO_GPU_ERR_CONFIG, "null plane %d", v);
-    CUDA_TRY(c, cudaMemcpy2DAsync(c->A + cell_index(c->pitch, v, -1, -1), 4 * c->pitch * 8,
-                                  planes[v], row_stride * 8, (size_t)(c->cfg.ny + 4) * 8,
-                                  (size_t)(c->cfg.nx + 4), cudaMemcpyHostToDevice, c->stream));
-  }
-  return HYDRO_GPU_OK;
-}
+}  // extern "C"
 
 namespace {
 
-// Pageable host planes (a Grid2D's std::vectors, grid.hpp:63) go through a
-// pinned two-buffer ring: the host copies of one band of rows run on
-// several threads while the DMA of the previous band is in flight -- a
-// pageable cudaMemcpy is staged by the driver one buffer at a time.
+// Host transfers.  The device state is tiled (hb::cell_index), so every
+// transfer goes through the context's two device staging buffers in bands of
+// plane rows: H2D of a band in the Grid2D row format, then a scatter kernel
+// into the blocks (and the reverse for downloads), both on the context's
+// stream.  Pageable host planes (a Grid2D's std::vectors, grid.hpp:63) are
+// staged once more through a pinned two-buffer ring: the host copies of one
+// band run on several threads while the DMA of the previous band is in
+// flight -- a pageable cudaMemcpy is staged by the driver one buffer at a time.
 constexpr size_t kStageBytes = 64u << 20;
 
 bool pageable(const void* p) {
@@ -681,9 +678,10 @@ bool pageable(const void* p) {
   return at.type == cudaMemoryTypeUnregistered;
 }
 
-int ensure_stage(hydro_gpu_ctx* c) {
+int ensure_stage(hydro_gpu_ctx* c, bool pinned) {
   for (int b = 0; b < 2; ++b) {
-    if (!c->stage[b]) CUDA_TRY(c, cudaMallocHost(&c->stage[b], kStageBytes));
+    if (!c->dstage[b]) CUDA_TRY(c, cudaMalloc(&c->dstage[b], kStageBytes));
+    if (pinned && !c->stage[b]) CUDA_TRY(c, cudaMallocHost(&c->stage[b], kStageBytes));
     if (!c->stage_ev[b]) CUDA_TRY(c, cudaEventCreateWithFlags(&c->stage_ev[b], cudaEventDisableTiming));
   }
   return HYDRO_GPU_OK;
@@ -708,51 +706,73 @@ void par_copy_rows(char* dst, size_t dst_stride, const char* src, size_t src_str
   for (auto& th : team) th.join();
 }
 
-// Host plane v rows [-1, nx+2] <-> device; up = host to device.
-int staged_transfer(hydro_gpu_ctx* c, double* const hp[4], size_t row_stride, bool up) {
-  int rc = ensure_stage(c);
+// Grid rows [i_lo, i_lo + nrows) of the 4 host planes (hp[v] points at grid
+// row i_lo's column -1, rows `row_stride` doubles apart) <-> the tiled state.
+// host_sync: pageable planes (staged through pinned memory, synchronous);
+// otherwise the copies are only enqueued (pinned planes that stay alive).
+int transfer_rows(hydro_gpu_ctx* c, double* const hp[4], size_t row_stride, int i_lo, int nrows,
+                  bool up, bool host_sync) {
+  int rc = ensure_stage(c, host_sync);
   if (rc) return rc;
-  const size_t row_bytes = (size_t)(c->cfg.ny + 4) * 8;
-  const size_t rows_total = (size_t)c->cfg.nx + 4;
+  const int ny = c->cfg.ny;
+  const size_t row_bytes = (size_t)(ny + 4) * 8;
   const size_t band = kStageBytes / row_bytes;
   if (band == 0) return set_err(c, HYDRO_GPU_ERR_CONFIG, "rows too long to stage");
-  struct Chunk { int v; size_t r0, n; };
+  struct Chunk { int v, r0, n; };
   std::vector<Chunk> chunks;
   for (int v = 0; v < 4; ++v)
-    for (size_t r0 = 0; r0 < rows_total; r0 += band)
-      chunks.push_back({v, r0, std::min(band, rows_total - r0)});
-  auto dev = [&](const Chunk& k) { return c->A + cell_index(c->pitch, k.v, (int)k.r0 - 1, -1); };
-  auto host = [&](const Chunk& k) { return hp[k.v] + k.r0 * row_stride; };
-  const size_t dpitch = 4 * c->pitch * 8;
+    for (int r0 = 0; r0 < nrows; r0 += (int)band)
+      chunks.push_back({v, r0, (int)std::min<size_t>(band, (size_t)(nrows - r0))});
+  auto host = [&](const Chunk& k) { return hp[k.v] + (size_t)k.r0 * row_stride; };
   if (up) {
     for (size_t q = 0; q < chunks.size(); ++q) {
       const int b = (int)(q & 1);
       const Chunk& k = chunks[q];
-      CUDA_TRY(c, cudaEventSynchronize(c->stage_ev[b]));  // the buffer's previous DMA is done
-      par_copy_rows((char*)c->stage[b], row_bytes, (const char*)host(k), row_stride * 8, k.n, row_bytes);
-      CUDA_TRY(c, cudaMemcpy2DAsync(dev(k), dpitch, c->stage[b], row_bytes, row_bytes, k.n,
+      const double* src = host(k);
+      size_t spitch = row_stride * 8;
+      if (host_sync) {  // the pinned buffer's previous DMA is done
+        CUDA_TRY(c, cudaEventSynchronize(c->stage_ev[b]));
+        par_copy_rows((char*)c->stage[b], row_bytes, (const char*)src, spitch, k.n, row_bytes);
+        src = c->stage[b];
+        spitch = row_bytes;
+      }
+      CUDA_TRY(c, cudaMemcpy2DAsync(c->dstage[b], row_bytes, src, spitch, row_bytes, k.n,
                                     cudaMemcpyHostToDevice, c->stream));
+      hb::launch_rows_to_tiles(c->dstage[b], ny + 4, c->A, c->pitch, k.v, i_lo + k.r0, k.n, ny,
+                               c->stream);
       CUDA_TRY(c, cudaEventRecord(c->stage_ev[b], c->stream));
     }
   } else {
     auto issue = [&](size_t q) -> int {
       const int b = (int)(q & 1);
       const Chunk& k = chunks[q];
-      CUDA_TRY(c, cudaMemcpy2DAsync(c->stage[b], row_bytes, dev(k), dpitch, row_bytes, k.n,
-                                    cudaMemcpyDeviceToHost, c->stream));
+      hb::launch_tiles_to_rows(c->A, c->pitch, c->dstage[b], ny + 4, k.v, i_lo + k.r0, k.n, ny,
+                               c->stream);
+      if (host_sync)
+        CUDA_TRY(c, cudaMemcpy2DAsync(c->stage[b], row_bytes, c->dstage[b], row_bytes, row_bytes,
+                                      k.n, cudaMemcpyDeviceToHost, c->stream));
+      else
+        CUDA_TRY(c, cudaMemcpy2DAsync(host(k), row_stride * 8, c->dstage[b], row_bytes, row_bytes,
+                                      k.n, cudaMemcpyDeviceToHost, c->stream));
       CUDA_TRY(c, cudaEventRecord(c->stage_ev[b], c->stream));
       return HYDRO_GPU_OK;
     };
+    if (!host_sync) {
+      for (size_t q = 0; q < chunks.size(); ++q)
+        if ((rc = issue(q))) return rc;
+      return HYDRO_GPU_OK;
+    }
     if ((rc = issue(0))) return rc;
     for (size_t q = 0; q < chunks.size(); ++q) {
-      if (q + 1 < chunks.size() && (rc = issue(q + 1))) return rc;
       const int b = (int)(q & 1);
-      const Chunk& k = chunks[q];
+      // chunk q+1 may not overwrite the pinned buffer chunk q-1 is copied out of
+      if (q + 1 < chunks.size() && (rc = issue(q + 1))) return rc;
       CUDA_TRY(c, cudaEventSynchronize(c->stage_ev[b]));
+      const Chunk& k = chunks[q];
       par_copy_rows((char*)host(k), row_stride * 8, (const char*)c->stage[b], row_bytes, k.n, row_bytes);
     }
   }
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (host_sync) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return HYDRO_GPU_OK;
 }
 
@@ -762,49 +782,86 @@ bool any_pageable(const double* const planes[4]) {
   return false;
 }
 
+int check_planes(hydro_gpu_ctx* c, const double* const planes[4], size_t row_stride) {
+  if (row_stride < (size_t)c->cfg.ny + 4)
+    return set_err(c, HYDRO_GPU_ERR_CONFIG, "row stride %zu below ny+4", row_stride);
+  for (int v = 0; v < 4; ++v)
+    if (!planes[v]) return set_err(c, HYDRO_GPU_ERR_CONFIG, "null plane %d", v);
+  return HYDRO_GPU_OK;
+}
+
 }  // namespace
 
-int hydro_gpu_upload(hydro_gpu_ctx* c, const double* const planes[4], size_t row_stride) {
-  if (c && planes && row_stride >= (size_t)c->cfg.ny + 4 && planes[0] && planes[1] && planes[2] &&
-      planes[3] && (size_t)(c->cfg.nx + 4) * (c->cfg.ny + 4) * 32 >= (32u << 20)) {
-    DeviceGuard g(c->device);
-    if (any_pageable(planes)) return staged_transfer(c, const_cast<double* const*>(planes), row_stride, true);
-  }
-  const int rc = hydro_gpu_upload_async(c, planes, row_stride);
+extern "C" {
+
+int hydro_gpu_upload_async(hydro_gpu_ctx* c, const double* const planes[4], size_t row_stride) {
+  if (!c || !planes) return HYDRO_GPU_ERR_CONFIG;
+  int rc = check_planes(c, planes, row_stride);
   if (rc) return rc;
   DeviceGuard g(c->device);
+  return transfer_rows(c, const_cast<double* const*>(planes), row_stride, -1, c->cfg.nx + 4, true,
+                       false);
+}
+
+int hydro_gpu_upload(hydro_gpu_ctx* c, const double* const planes[4], size_t row_stride) {
+  if (!c || !planes) return HYDRO_GPU_ERR_CONFIG;
+  int rc = check_planes(c, planes, row_stride);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
+  rc = transfer_rows(c, const_cast<double* const*>(planes), row_stride, -1, c->cfg.nx + 4, true,
+                     any_pageable(planes));
+  if (rc) return rc;
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return HYDRO_GPU_OK;
 }
 
 int hydro_gpu_download_async(hydro_gpu_ctx* c, double* const planes[4], size_t row_stride) {
   if (!c || !planes) return HYDRO_GPU_ERR_CONFIG;
-  if (row_stride < (size_t)c->cfg.ny + 4)
-    return set_err(c, HYDRO_GPU_ERR_CONFIG, "row stride %zu below ny+4", row_stride);
+  int rc = check_planes(c, planes, row_stride);
+  if (rc) return rc;
   DeviceGuard g(c->device);
-  for (int v = 0; v < 4; ++v) {
-    if (!planes[v]) return set_err(c, HYDRO_GPU_ERR_CONFIG, "null plane %d", v);
-    CUDA_TRY(c, cudaMemcpy2DAsync(planes[v], row_stride * 8,
-                                  c->A + cell_index(c->pitch, v, -1, -1), 4 * c->pitch * 8,
-                                  (size_t)(c->cfg.ny + 4) * 8, (size_t)(c->cfg.nx + 4),
-                                  cudaMemcpyDeviceToHost, c->stream));
-  }
-  return HYDRO_GPU_OK;
+  return transfer_rows(c, planes, row_stride, -1, c->cfg.nx + 4, false, false);
 }
 
 int hydro_gpu_download(hydro_gpu_ctx* c, double* const planes[4], size_t row_stride) {
-  if (c && planes && row_stride >= (size_t)c->cfg.ny + 4 && planes[0] && planes[1] && planes[2] &&
-      planes[3] && (size_t)(c->cfg.nx + 4) * (c->cfg.ny + 4) * 32 >= (32u << 20)) {
-    DeviceGuard g(c->device);
-    if (any_pageable(planes)) {
-      CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // the state is final
-      return staged_transfer(c, planes, row_stride, false);
-    }
-  }
-  const int rc = hydro_gpu_download_async(c, planes, row_stride);
+  if (!c || !planes) return HYDRO_GPU_ERR_CONFIG;
+  int rc = check_planes(c, planes, row_stride);
   if (rc) return rc;
   DeviceGuard g(c->device);
+  rc = transfer_rows(c, planes, row_stride, -1, c->cfg.nx + 4, false, any_pageable(planes));
+  if (rc) return rc;
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_download_rows(hydro_gpu_ctx* c, double* const planes[4], size_t row_stride,
+                            int i_lo, int nrows) {
+  if (!c || !planes || nrows < 0 || i_lo < -1 || i_lo + nrows > c->cfg.nx + 3)
+    return HYDRO_GPU_ERR_CONFIG;
+  int rc = check_planes(c, planes, row_stride);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
+  rc = transfer_rows(c, planes, row_stride, i_lo, nrows, false, any_pageable(planes));
+  if (rc) return rc;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_compare(hydro_gpu_ctx* a, hydro_gpu_ctx* b, double* max_rel) {
+  if (!a || !b || !max_rel || a->cfg.nx != b->cfg.nx || a->cfg.ny != b->cfg.ny ||
+      a->pitch != b->pitch || a->device != b->device)
+    return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(a->device);
+  CUDA_TRY(a, cudaStreamSynchronize(b->stream));
+  unsigned long long* d = nullptr;
+  CUDA_TRY(a, cudaMallocAsync(&d, sizeof *d, a->stream));
+  CUDA_TRY(a, cudaMemsetAsync(d, 0, sizeof *d, a->stream));
+  hb::launch_compare(a->A, b->A, a->pitch, a->cfg.nx, a->cfg.ny, d, a->stream);
+  unsigned long long bits = 0;
+  CUDA_TRY(a, cudaMemcpyAsync(&bits, d, sizeof bits, cudaMemcpyDeviceToHost, a->stream));
+  CUDA_TRY(a, cudaFreeAsync(d, a->stream));
+  CUDA_TRY(a, cudaStreamSynchronize(a->stream));
+  *max_rel = as_double(bits);
   return HYDRO_GPU_OK;
 }
 
@@ -976,13 +1033,34 @@ int hydro_gpu_error_slot(hydro_gpu_ctx* c, uint64_t** p) {
 int hydro_gpu_halo(hydro_gpu_ctx* c, double** send_lo, double** send_hi, double** recv_lo,
                    double** recv_hi, size_t* count) {
   if (!c) return HYDRO_GPU_ERR_CONFIG;
-  const int nx = c->cfg.nx;
-  const size_t rowblk = 4 * c->pitch;
-  if (send_lo) *send_lo = c->A + (size_t)(1 + 1) * rowblk;       // rows 1..2
-  if (send_hi) *send_hi = c->A + (size_t)(nx - 1 + 1) * rowblk;  // rows nx-1..nx
-  if (recv_lo) *recv_lo = c->A + (size_t)(-1 + 1) * rowblk;      // rows -1..0
-  if (recv_hi) *recv_hi = c->A + (size_t)(nx + 1 + 1) * rowblk;  // rows nx+1..nx+2
-  if (count) *count = 2 * rowblk;
+  DeviceGuard g(c->device);
+  const size_t blk = 8 * c->pitch;
+  if (!c->halo_buf) CUDA_TRY(c, cudaMalloc(&c->halo_buf, 4 * blk * sizeof(double)));
+  if (send_lo) *send_lo = c->halo_buf;            // rows 1..2
+  if (send_hi) *send_hi = c->halo_buf + blk;      // rows nx-1..nx
+  if (recv_lo) *recv_lo = c->halo_buf + 2 * blk;  // rows -1..0
+  if (recv_hi) *recv_hi = c->halo_buf + 3 * blk;  // rows nx+1..nx+2
+  if (count) *count = blk;
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_slab_halo_pack(hydro_gpu_ctx* c) {
+  if (!c || !c->halo_buf) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  const size_t blk = 8 * c->pitch;
+  rows_to_block(c, 1, c->halo_buf);
+  rows_to_block(c, c->cfg.nx - 1, c->halo_buf + blk);
+  CUDA_TRY(c, cudaGetLastError());
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_slab_halo_unpack(hydro_gpu_ctx* c) {
+  if (!c || !c->halo_buf) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  const size_t blk = 8 * c->pitch;
+  if (!c->cfg.wall_lo) block_to_rows(c, c->halo_buf + 2 * blk, -1);
+  if (!c->cfg.wall_hi) block_to_rows(c, c->halo_buf + 3 * blk, c->cfg.nx + 1);
+  CUDA_TRY(c, cudaGetLastError());
   return HYDRO_GPU_OK;
 }
 
@@ -1056,30 +1134,20 @@ int hydro_gpu_comm_attach(hydro_gpu_ctx* c, const void* id128, int nranks, int r
 int hydro_gpu_slab_halo_out(hydro_gpu_ctx* c, int step) {
   if (!c) return HYDRO_GPU_ERR_CONFIG;
   DeviceGuard g(c->device);
-  const size_t blk = 8 * c->pitch, rowblk = 4 * c->pitch, par = (size_t)(step & 1);
-  const size_t bytes = blk * sizeof(double);
-  if (c->peer_up)
-    CUDA_TRY(c, cudaMemcpyAsync(c->peer_up + (par * 2 + 1) * blk, c->A + 2 * rowblk, bytes,
-                                cudaMemcpyDeviceToDevice, c->stream));
-  if (c->peer_dn)
-    CUDA_TRY(c, cudaMemcpyAsync(c->peer_dn + (par * 2 + 0) * blk,
-                                c->A + (size_t)c->cfg.nx * rowblk, bytes,
-                                cudaMemcpyDeviceToDevice, c->stream));
+  const size_t blk = 8 * c->pitch, par = (size_t)(step & 1);
+  if (c->peer_up) rows_to_block(c, 1, c->peer_up + (par * 2 + 1) * blk);
+  if (c->peer_dn) rows_to_block(c, c->cfg.nx - 1, c->peer_dn + (par * 2 + 0) * blk);
+  CUDA_TRY(c, cudaGetLastError());
   return HYDRO_GPU_OK;
 }
 
 int hydro_gpu_slab_inbox_in(hydro_gpu_ctx* c, int step) {
   if (!c) return HYDRO_GPU_ERR_CONFIG;
   DeviceGuard g(c->device);
-  const size_t blk = 8 * c->pitch, rowblk = 4 * c->pitch, par = (size_t)(step & 1);
-  const size_t bytes = blk * sizeof(double);
-  if (!c->cfg.wall_lo)  // ghost rows -1..0
-    CUDA_TRY(c, cudaMemcpyAsync(c->A, c->inbox + (par * 2 + 0) * blk, bytes,
-                                cudaMemcpyDeviceToDevice, c->stream));
-  if (!c->cfg.wall_hi)  // ghost rows nx+1..nx+2
-    CUDA_TRY(c, cudaMemcpyAsync(c->A + (size_t)(c->cfg.nx + 2) * rowblk,
-                                c->inbox + (par * 2 + 1) * blk, bytes, cudaMemcpyDeviceToDevice,
-                                c->stream));
+  const size_t blk = 8 * c->pitch, par = (size_t)(step & 1);
+  if (!c->cfg.wall_lo) block_to_rows(c, c->inbox + (par * 2 + 0) * blk, -1);  // ghost rows -1..0
+  if (!c->cfg.wall_hi) block_to_rows(c, c->inbox + (par * 2 + 1) * blk, c->cfg.nx + 1);
+  CUDA_TRY(c, cudaGetLastError());
   return HYDRO_GPU_OK;
 }
 

@@ -390,22 +390,15 @@ int hydro_gpu_group_download(hydro_gpu_group* g, double* const planes[4], size_t
   if (!g || !planes) return HYDRO_GPU_ERR_CONFIG;
   if (row_stride < (size_t)g->cfg.ny + 4) return fail(g, HYDRO_GPU_ERR_CONFIG, "row stride below ny+4");
   for (int k = 0; k < g->n; ++k) {
-    double* a = nullptr;
-    size_t pitch = 0;
-    hydro_gpu_state(g->ctx[k], &a, &pitch);
     const int lo = k == 0 ? 0 : 2, hi = k == g->n - 1 ? g->rows[k] + 4 : g->rows[k] + 2;
-    Guard d(g->device[k]);
+    double* p[4];
     for (int v = 0; v < 4; ++v) {
       if (!planes[v]) return fail(g, HYDRO_GPU_ERR_CONFIG, "null plane");
-      GROUP_CUDA(g, cudaMemcpy2DAsync(planes[v] + (size_t)(g->row0[k] + lo) * row_stride,
-                                      row_stride * 8, a + hb::cell_index(pitch, v, lo - 1, -1),
-                                      4 * pitch * 8, (size_t)(g->cfg.ny + 4) * 8,
-                                      (size_t)(hi - lo), cudaMemcpyDeviceToHost, g->stream[k]));
+      p[v] = planes[v] + (size_t)(g->row0[k] + lo) * row_stride;
     }
-  }
-  for (int k = 0; k < g->n; ++k) {
-    Guard d(g->device[k]);
-    GROUP_CUDA(g, cudaStreamSynchronize(g->stream[k]));
+    // plane rows lo .. hi-1 of the slab = grid rows lo-1 .. hi-2
+    const int rc = hydro_gpu_download_rows(g->ctx[k], p, row_stride, lo - 1, hi - lo);
+    if (rc) return slab_rc(g, k, rc);
   }
   return HYDRO_GPU_OK;
 }

@@ -491,15 +491,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   } while (!done);
 }
 
-__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
-                                         int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-
 __device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
                                           int c1, int c2, int c3, int c4) {
   asm volatile(
@@ -514,14 +505,6 @@ __device__ __forceinline__ void tma_store5(const CUtensorMap* map, const void* s
   asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::
                    "l"(map),
                "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
-               : "memory");
-}
-
-__device__ __forceinline__ void tma_store(const CUtensorMap* map, const void* src, int c0, int c1,
-                                          int c2) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::
-                   "l"(map),
-               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
                : "memory");
 }
 
@@ -617,8 +600,10 @@ struct Tiles {
     mbar_expect_tx(bar(q), kChunkBytes);
     const int k = ka - C + q * C;
     if constexpr (AXIS == 0) {
-      // U_a: box {32 cols, 4 rows, 4 vars} at plane row k -> smem [var][row][col]
-      tma_load(buf(q), load_map, bar(q), c0(k), k, 0);
+      // U_a: 4 column blocks x grid rows k-1 .. k+2 (one block row; r + 1 =
+      // grid row - 1 of the first row, >= -4) -> smem [var][row][col]
+      const int r = k - 2;
+      tma_load5(buf(q), load_map, bar(q), 0, c0(k) >> 3, r & 31, 0, (r >> 5) + 1);
     } else {
       // tiled U_b: the item's block row (s0 - 1) / 32, the chunk's column block
       const int col = c0(k);
@@ -633,8 +618,9 @@ struct Tiles {
       const int r = k - 2;  // grid row - 1 of the chunk's first row (>= 0 for stored chunks)
       tma_store5(store_map, buf(t), 0, c0(k) >> 3, r & 31, 0, (r >> 5) + 1);
     } else {
-#pragma unroll
-      for (int v = 0; v < 4; ++v) tma_store(store_map, buf(t) + v * kVarBytes, c0(k), v, c2(k));
+      // U_a: one block (the item's block row, the chunk's column block)
+      const int col = c0(k);
+      tma_store5(store_map, buf(t), col & 7, col >> 3, 0, 0, (s0 + 31) >> 5);
     }
     bulk_commit();
   }
@@ -677,10 +663,20 @@ struct Tiles {
   __device__ __forceinline__ Cons prev() const { return get(prev_addr); }
   __device__ __forceinline__ void count_skip() { ++nskip; }
 
+  // The TMA swizzle term of strip (lane) l's slots: row sweep SWIZZLE_32B
+  // (C = 4) flips the 16-byte half of a 32-byte row with address bit 7 (bit
+  // 2 of the row); SWIZZLE_64B (C = 8) XORs the 16-byte unit index (bits 4-5)
+  // with bits 7-8 (row bits 1-2); the column sweep is not swizzled.
+  __device__ __forceinline__ static uint32_t swz(int l) {
+    if constexpr (AXIS == 0) return 0u;
+    return C == 4 ? (uint32_t)((l >> 2) & 1) << 4 : (uint32_t)((l >> 1) & 3) << 4;
+  }
+
   // The cell being updated, of strip `ln` (default: this lane's), receives u.
   __device__ __forceinline__ void put(int, const Cons& u, int ln = -1) {
     constexpr int va = AXIS == 0 ? 1 : 2, vb = AXIS == 0 ? 2 : 1;
-    uint8_t* b = hb_smem + ((wr_addr + (ln < 0 ? 0 : (ln - lane) * (int)kLaneBytes)) ^ sw);
+    uint8_t* b = hb_smem + (ln < 0 ? (wr_addr ^ sw)
+                                   : ((wr_addr + (ln - lane) * (int)kLaneBytes) ^ swz(ln)));
     *(double*)(b) = u.r;
     *(double*)(b + va * kVarStride) = u.ma;
     *(double*)(b + vb * kVarStride) = u.mb;
@@ -773,14 +769,7 @@ __device__ __forceinline__ Tiles<AXIS, FLUX> make_tiles(const CUtensorMap* load_
   t.q0 = 0;
   t.nskip = 0;
   t.skip_cool = 0;
-  // row sweep, lane = box row of 8C bytes: SWIZZLE_32B (C = 4) flips the
-  // 16-byte half of a row with address bit 7 (bit 2 of the row); SWIZZLE_64B
-  // (C = 8) XORs the 16-byte unit index (bits 4-5) with bits 7-8 (row bits 1-2)
-  if constexpr (AXIS == 1) {
-    t.sw = Tl::C == 4 ? (uint32_t)((lane >> 2) & 1) << 4 : (uint32_t)((lane >> 1) & 3) << 4;
-  } else {
-    t.sw = 0u;
-  }
+  t.sw = Tl::swz(lane);
   if (lane == 0) {
     for (int q = 0; q < Tl::NBUF; ++q) mbar_init((uint64_t*)(hb_smem + t.full) + q, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -851,11 +840,11 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_X_MINB : HB_EX_MINB)
         // ny % 32 == 1: ghost ny+2 mirrors column ny-1 of the previous group)
         // is written after the sweep by ghost_fix_kernel
         if (jt > ny && ((jt - 1) >> 5) < groups) return;
-        double* q = dst + tile_index(pitch, 0, i, jt);
+        double* q = dst + cell_index(pitch, 0, i, jt);
         q[0] = gh.r;
-        q[256] = gh.ma;
-        q[512] = gh.mb;
-        q[768] = gh.e;
+        q[kVarStep] = gh.ma;
+        q[2 * kVarStep] = gh.mb;
+        q[3 * kVarStep] = gh.e;
       };
       auto sink = [&](int k, const StepOut& o) {
         if (active) t.put(k, o.un);
@@ -937,12 +926,27 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : HB_EX_MINB) sweep
                                   ((mirror_hi || send_dn) && i >= nx - 1));
     const int gi = a.row0 + i;
     const unsigned long long base = error_key(a.step, 2, gi, 0, 0, 0);
-    auto put_row = [&](int ii, int j, const Cons& u, bool neg) {
+    // x-wall ghost rows of U_a: inside this warp's store blocks (its 32 rows)
+    // a ghost row goes into the slot of the lane that holds that row -- an
+    // inactive lane, whose slot the TMA store writes -- else straight to
+    // memory (block row -1 and rows no store block covers); a row inside
+    // another warp's blocks (reflecting walls with nx % 32 == 1: ghost nx+2
+    // mirrors row nx-1 of the previous group) is written after the sweep by
+    // ghost_fix_kernel
+    auto put_row = [&](int k, int ii, int j, const Cons& u, bool neg) {
+      Cons gh = u;
+      if (neg) gh.mb = -gh.mb;  // sweep orientation: mom_b is mom_x
+      const int d = ii - i0;
+      if (d >= 0 && d < 32) {
+        t.put(k, gh, d);
+        return;
+      }
+      if (ii > nx && ((ii - 1) >> 5) < groups) return;
       double* q = dst + cell_index(pitch, 0, ii, j);
-      q[0] = u.r;
-      q[2 * pitch] = u.ma;
-      q[pitch] = neg ? -u.mb : u.mb;
-      q[3 * pitch] = u.e;
+      q[0] = gh.r;
+      q[kVarStep] = gh.mb;
+      q[2 * kVarStep] = gh.ma;
+      q[3 * kVarStep] = gh.e;
     };
     auto put_peer = [&](double* q, const Cons& u) {  // NVLink store into a peer's inbox
       q[0] = u.r;
@@ -963,12 +967,12 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : HB_EX_MINB) sweep
         const int j = k - 1;
         if (extra) {
         if (mirror_lo && active && i <= 2) {  // x-wall ghosts for the next column sweep (grid.cpp:26-42)
-          if (refl) put_row(1 - i, j, o.un, true);
-          else if (i == 1) { put_row(0, j, o.un, false); put_row(-1, j, o.un, false); }
+          if (refl) put_row(k, 1 - i, j, o.un, true);
+          else if (i == 1) { put_row(k, 0, j, o.un, false); put_row(k, -1, j, o.un, false); }
         }
         if (mirror_hi && active && i >= nx - 1) {
-          if (refl) put_row(2 * nx + 1 - i, j, o.un, true);
-          else if (i == nx) { put_row(nx + 1, j, o.un, false); put_row(nx + 2, j, o.un, false); }
+          if (refl) put_row(k, 2 * nx + 1 - i, j, o.un, true);
+          else if (i == nx) { put_row(k, nx + 1, j, o.un, false); put_row(k, nx + 2, j, o.un, false); }
         }
         if constexpr (PEER) {
           if (send_up && active && i <= 2)  // -> upper neighbour's ghost rows nx'+1..nx'+2
@@ -1125,9 +1129,67 @@ __global__ void ghost_fix_kernel(double* __restrict__ b, size_t pitch, int nx, i
   const int i = 1 + blockIdx.x * blockDim.x + threadIdx.x;
   if (i > nx) return;
   for (int v = 0; v < 4; ++v) {
-    const double x = b[tile_index(pitch, v, i, ny - 1)];
-    b[tile_index(pitch, v, i, ny + 2)] = v == 2 ? -x : x;
+    const double x = b[cell_index(pitch, v, i, ny - 1)];
+    b[cell_index(pitch, v, i, ny + 2)] = v == 2 ? -x : x;
   }
+}
+
+// The same for U_a after a row sweep: with a reflecting lower wall and
+// nx % 32 == 1, ghost row nx+2 (the mirror of row nx-1, grid.cpp:26-42) lies
+// in the last row group's store blocks.
+__global__ void ghost_row_fix_kernel(double* __restrict__ a, size_t pitch, int nx, int ny) {
+  const int j = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > ny) return;
+  for (int v = 0; v < 4; ++v) {
+    const double x = a[cell_index(pitch, v, nx - 1, j)];
+    a[cell_index(pitch, v, nx + 2, j)] = v == 1 ? -x : x;
+  }
+}
+
+// Row-layout rows <-> the tiled state.  rows[r * row_stride + (j + 1)] is
+// cell (i0 + r, j), j = -1 .. ny+2, of variable v (the host Grid2D plane
+// format, through the transfers' device staging); v = -1: all four
+// variables of 2 rows in the halo-block format (element (r, v, j) at
+// (4 r + v) pitch + j + kColOff, the inbox layout the row sweep's peer stores
+// use).
+__global__ void rows_tiles_kernel(double* rows, size_t row_stride, double* u, size_t pitch, int v,
+                                  int i0, int n, int ny, int to_tiles) {
+  const int j = -1 + (int)(blockIdx.x * blockDim.x + threadIdx.x);
+  if (j > ny + 2) return;
+  for (int r = blockIdx.y; r < n; r += gridDim.y) {
+    for (int w = (v < 0 ? 0 : v); w <= (v < 0 ? 3 : v); ++w) {
+      double* h = v < 0 ? rows + ((size_t)4 * r + w) * pitch + (j + kColOff)
+                        : rows + (size_t)r * row_stride + (j + 1);
+      double* d = u + cell_index(pitch, w, i0 + r, j);
+      if (to_tiles) *d = *h;
+      else *h = *d;
+    }
+  }
+}
+
+// compare_tolerance's max |a - b| / max(|a|, |b|, 1) over the interior
+// (proj/src/audit.cpp:137-154) of two states of one geometry, as the bits of
+// a non-negative double (atomicMax).
+__global__ void compare_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                               size_t pitch, int nx, int ny, unsigned long long* out) {
+  double m = 0.0;
+  const size_t cells = (size_t)nx * ny;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < 4 * cells;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const int v = (int)(t / cells);
+    const size_t c = t % cells;
+    const int i = 1 + (int)(c / ny), j = 1 + (int)(c % ny);
+    const size_t k = cell_index(pitch, v, i, j);
+    const double x = a[k], y = b[k];
+    const double r = fabs(x - y) / fmax(fmax(fabs(x), fabs(y)), 1.0);
+    m = (r > m || r != r) ? r : m;  // a NaN difference propagates
+  }
+  unsigned long long bits = (unsigned long long)__double_as_longlong(m);
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, bits, o);
+    bits = w > bits ? w : bits;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, bits);
 }
 
 // End-of-run ghosts: the reference's last apply_boundary ran on the column
@@ -1145,7 +1207,7 @@ __global__ void finish_kernel(FinishArgs a) {
       for (int s = 0; s < 2; ++s) {
         if (!on[s]) continue;
         for (int v = 0; v < 4; ++v) {
-          const double x = a.post_x[tile_index(pitch, v, srcs[s], j)];
+          const double x = a.post_x[cell_index(pitch, v, srcs[s], j)];
           a.u[cell_index(pitch, v, gh[s], j)] = (refl && v == 1) ? -x : x;
         }
       }
@@ -1155,7 +1217,7 @@ __global__ void finish_kernel(FinishArgs a) {
     const int cols[4] = {-1, 0, a.ny + 1, a.ny + 2};
     for (int c = 0; c < 4; ++c)
       for (int v = 0; v < 4; ++v)
-        a.u[cell_index(pitch, v, i, cols[c])] = a.post_x[tile_index(pitch, v, i, cols[c])];
+        a.u[cell_index(pitch, v, i, cols[c])] = a.post_x[cell_index(pitch, v, i, cols[c])];
   }
 }
 
@@ -1234,11 +1296,10 @@ __global__ void row_audit_kernel(const double* __restrict__ u, size_t pitch, int
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= 4 * nx) return;
   const int v = t / nx, i = t % nx + 1;
-  const double* row = u + cell_index(pitch, v, i, 1);
   unsigned long long h = 14695981039346656037ull;
   double sum = 0.0;
   for (int j = 0; j < ny; ++j) {
-    const double x = __ldg(row + j);
+    const double x = __ldg(u + cell_index(pitch, v, i, j + 1));
     const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
@@ -1342,6 +1403,7 @@ int HB_SWEEP(query_geometry)(Geometry* g) {
 
 #ifndef HB_TOLERANCE
 bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, int ny) {
+  (void)ny;
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -1352,48 +1414,30 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
       return false;
     encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
   }
-  auto enc = [&](CUtensorMap* m, int rank, double* base, const cuuint64_t* dim,
-                 const cuuint64_t* strides, const cuuint32_t* box, CUtensorMapSwizzle swz) {
+  // a tiled state buffer (cell_index) as dims {column in block, column
+  // block, row in block, var, block row}: strides not increasing, so a box
+  // lands in smem as [var][row][block][column]
+  const cuuint64_t ntj = pitch / 8;
+  const cuuint64_t dim[5] = {8, ntj, 32, 4, (cuuint64_t)tile_rows(nx)};
+  const cuuint64_t str[4] = {8192, 64, 2048, 8192 * ntj};
+  auto enc = [&](CUtensorMap* m, double* base, const cuuint32_t* box, CUtensorMapSwizzle swz) {
     const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, base, dim, strides, box, estr,
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, dim, str, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
-  // U_a (row-interleaved planes), dims {column, var, plane row}: the row
-  // sweep's stores, interior only -- rows up to nx and column offsets up to
-  // j = ny, so tail items past the grid are clipped (ghosts are written
-  // separately)
-  const cuuint64_t a_str[2] = {pitch * 8, 4 * pitch * 8};
-  const cuuint64_t dim_store[3] = {(cuuint64_t)ny + 1 + kColOff, 4, (cuuint64_t)nx + 2};
-  // ... and the column sweep's loads, dims {column, plane row, var} (strides
-  // not increasing: the box lands as smem [var][row][column], the order of
-  // the tiled U_b blocks it is stored to); boxes reaching past the buffer
-  // are zero-filled
-  const cuuint64_t dim_xload[3] = {pitch, (cuuint64_t)nx + 4, 4};
-  const cuuint64_t xl_str[2] = {4 * pitch * 8, pitch * 8};
-  // tiled U_b (tile_index), dims {column in block, column block, row in
-  // block, var, block row}
-  const cuuint64_t ntj = pitch / 8;
-  const cuuint64_t dim_b[5] = {8, ntj, 32, 4, (cuuint64_t)tile_rows(nx)};
-  const cuuint64_t b_str[4] = {8192, 64, 2048, 8192 * ntj};
   constexpr int CX = Staging<0>::C, CY = Staging<1>::C, CE = Staging<1, 1>::C;
-  const cuuint32_t box_xload[3] = {32, (cuuint32_t)CX, 4};
-  const cuuint32_t box_xstore[5] = {8, 4, (cuuint32_t)CX, 4, 1};  // 32 columns x CX rows x 4 vars
-  const cuuint32_t box_yload[5] = {(cuuint32_t)CY, 1, 32, 4, 1};  // one block (C = 8)
-  const cuuint32_t box_eyload[5] = {(cuuint32_t)CE, 1, 32, 4, 1};
-  const cuuint32_t box_y[3] = {(cuuint32_t)CY, 1, 32};           // row sweep stores: C cols x 32 rows
-  const cuuint32_t box_ey[3] = {(cuuint32_t)CE, 1, 32};
+  const cuuint32_t box_x[5] = {8, 4, (cuuint32_t)CX, 4, 1};  // 32 columns x CX rows x 4 vars
+  const cuuint32_t box_y[5] = {(cuuint32_t)CY, 1, 32, 4, 1};  // C columns x 32 rows x 4 vars
+  const cuuint32_t box_ey[5] = {(cuuint32_t)CE, 1, 32, 4, 1};
   // row sweep: 64-byte (32-byte) box rows swizzled against the smem bank
-  // conflicts of lane-per-row accesses; column sweep: 256-byte rows are
-  // conflict-free
+  // conflicts of lane-per-row accesses; column sweep: lanes read consecutive
+  // words
   auto swz = [](int c) { return c == 4 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B; };
   const CUtensorMapSwizzle none = CU_TENSOR_MAP_SWIZZLE_NONE;
-  return enc(&maps->x_load, 3, A, dim_xload, xl_str, box_xload, none) &&
-         enc(&maps->x_store, 5, B, dim_b, b_str, box_xstore, none) &&
-         enc(&maps->y_load, 5, B, dim_b, b_str, box_yload, swz(CY)) &&
-         enc(&maps->y_store, 3, A, dim_store, a_str, box_y, swz(CY)) &&
-         enc(&maps->ey_load, 5, B, dim_b, b_str, box_eyload, swz(CE)) &&
-         enc(&maps->ey_store, 3, A, dim_store, a_str, box_ey, swz(CE));
+  return enc(&maps->x_load, A, box_x, none) && enc(&maps->x_store, B, box_x, none) &&
+         enc(&maps->y_load, B, box_y, swz(CY)) && enc(&maps->y_store, A, box_y, swz(CY)) &&
+         enc(&maps->ey_load, B, box_ey, swz(CE)) && enc(&maps->ey_store, A, box_ey, swz(CE));
 }
 
 #endif  // !HB_TOLERANCE
@@ -1465,6 +1509,31 @@ void HB_SWEEP(launch_prologue)(const PrologueArgs& a, cudaStream_t s) {
 void launch_ghost_fix(double* b, size_t pitch, int nx, int ny, int bc, cudaStream_t s) {
   if (bc != 0 || (ny & 31) != 1 || ny < 33) return;
   ghost_fix_kernel<<<(nx + 255) / 256, 256, 0, s>>>(b, pitch, nx, ny);
+}
+
+void launch_ghost_row_fix(double* a, size_t pitch, int nx, int ny, int bc, int wall_hi,
+                          cudaStream_t s) {
+  if (bc != 0 || !wall_hi || (nx & 31) != 1 || nx < 33) return;
+  ghost_row_fix_kernel<<<(ny + 255) / 256, 256, 0, s>>>(a, pitch, nx, ny);
+}
+
+void launch_rows_to_tiles(const double* rows, size_t row_stride, double* u, size_t pitch, int v,
+                          int i0, int n, int ny, cudaStream_t s) {
+  dim3 grid((ny + 4 + 255) / 256, n < 1024 ? n : 1024);
+  rows_tiles_kernel<<<grid, 256, 0, s>>>(const_cast<double*>(rows), row_stride, u, pitch, v, i0, n,
+                                         ny, 1);
+}
+
+void launch_tiles_to_rows(const double* u, size_t pitch, double* rows, size_t row_stride, int v,
+                          int i0, int n, int ny, cudaStream_t s) {
+  dim3 grid((ny + 4 + 255) / 256, n < 1024 ? n : 1024);
+  rows_tiles_kernel<<<grid, 256, 0, s>>>(rows, row_stride, const_cast<double*>(u), pitch, v, i0, n,
+                                         ny, 0);
+}
+
+void launch_compare(const double* a, const double* b, size_t pitch, int nx, int ny,
+                    unsigned long long* out, cudaStream_t s) {
+  compare_kernel<<<1184, 256, 0, s>>>(a, b, pitch, nx, ny, out);
 }
 
 void launch_finish(const FinishArgs& a, cudaStream_t s) {

@@ -50,28 +50,30 @@ constexpr int kMemoBytes = 13 * 128 * 8;
 constexpr int kExXSmemBytes = Staging<0, 1>::kSmem + kMemoBytes;
 constexpr int kExYSmemBytes = Staging<1, 1>::kSmem + kMemoBytes;
 
+// Both state buffers are stored TILED (r2): blocks of 32 grid rows x 8
+// columns x 4 variables (8 KB), block (ti, tj) at ((ti + 1) * (pitch / 8) + tj)
+// * 1024 doubles, element [v][ri][rj] inside, with ti = floor((i - 1) / 32),
+// ri = i - 1 - 32 ti, tj = (j + kColOff) / 8, rj = (j + kColOff) % 8 (grid
+// rows -1 .. nx+2, i.e. block rows -1 .. tile_rows - 2; `pitch` = 8 x the
+// block columns).  A row-sweep chunk (32 rows of one row group x 8 columns x
+// 4 variables) is then one contiguous 8 KB block, and a column-sweep chunk
+// (4 rows x 32 columns) sixteen 256-byte pieces: tools/tma_pattern.cu
+// streams the row sweep's pattern at 6.6 TB/s on this layout against 4.4 TB/s
+// with 64-byte pieces of row-interleaved planes.
 __host__ __device__ __forceinline__ size_t cell_index(size_t pitch, int v, int i, int j) {
-  return ((size_t)(i + 1) * 4 + (size_t)v) * pitch + (size_t)(j + kColOff);
-}
-
-// The column-sweep output U_b (read only by the row sweep and the end-of-run
-// ghost pass) is stored TILED: blocks of 32 grid rows x 8 columns x 4
-// variables (8 KB), block (ti, tj) at ((ti + 1) * (pitch / 8) + tj) * 1024
-// doubles, element [v][ri][rj] inside, with ti = floor((i - 1) / 32),
-// ri = i - 1 - 32 ti, tj = (j + kColOff) / 8, rj = (j + kColOff) % 8.  A
-// row-sweep chunk (32 rows of one row group x 8 columns x 4 variables) is
-// then one contiguous 8 KB block, and a column-sweep chunk (4 rows x 32
-// columns) sixteen 256-byte pieces (tools/tma_pattern.cu: the row sweep's
-// 64-byte box rows streamed at 4.4 TB/s, the tiled blocks at 6.6 TB/s).
-__host__ __device__ __forceinline__ size_t tile_index(size_t pitch, int v, int i, int j) {
   const int ti = (i + 31) / 32 - 1;  // floor((i - 1) / 32) for i >= -31
   const int ri = i - 1 - 32 * ti;
   const int c = j + kColOff;
   return (((size_t)(ti + 1) * (pitch / 8) + (size_t)(c >> 3)) * 4 + (size_t)v) * 256 +
          (size_t)ri * 8 + (size_t)(c & 7);
 }
-// Tile rows of U_b: grid rows -1 .. nx+2.
+// distance between the variables of one cell
+constexpr size_t kVarStep = 256;
+// Block rows of a state buffer: grid rows -1 .. nx+2.
 __host__ __device__ __forceinline__ int tile_rows(int nx) { return (nx + 1) / 32 + 2; }
+__host__ __device__ __forceinline__ size_t state_doubles(int nx, size_t pitch) {
+  return (size_t)tile_rows(nx) * (pitch / 8) * 1024;
+}
 
 inline size_t pitch_for(int ny) {
   const size_t need = (size_t)ny + 3 + kColOff;  // offsets 0..ny+2+kColOff
@@ -108,13 +110,15 @@ struct SweepArgs {
   unsigned long long* skipped;  // cell updates taken by the uniform-window identity (counter)
 };
 
+// All maps view a tiled buffer as dims {column in block, column block, row in
+// block, var, block row} (strides not increasing).
 struct TmaMaps {
-  CUtensorMap y_load;         // U_b (tiled), one 8 KB block {8 cols, 32 rows, 4 vars}
-  CUtensorMap y_store;        // U_a interior rows/cols only (clips ghosts), box {8 cols, 1 var, 32 rows}
-  CUtensorMap x_load;         // U_a, box {32 cols, 4 rows, 4 vars} -> smem [var][row][col]
-  CUtensorMap x_store;        // U_b (tiled), box {8 cols, 4 blocks, 4 rows, 4 vars}
-  CUtensorMap ey_load;        // the exact-10 row sweep: U_b (tiled) {4 cols, 32 rows, 4 vars}
-  CUtensorMap ey_store;       // ... and U_a, box {4 cols, 1 var, 32 rows}
+  CUtensorMap y_load;         // U_b: one block {8 cols, 32 rows, 4 vars}
+  CUtensorMap y_store;        // U_a: the same
+  CUtensorMap x_load;         // U_a: {8 cols, 4 blocks, 4 rows, 4 vars} -> smem [var][row][col]
+  CUtensorMap x_store;        // U_b: the same
+  CUtensorMap ey_load;        // the exact-10 row sweep: {4 cols, 32 rows, 4 vars} of U_b
+  CUtensorMap ey_store;       // ... and of U_a
 };
 
 struct PrologueArgs {
@@ -169,6 +173,18 @@ void launch_finish(const FinishArgs& a, cudaStream_t s);
 // The tiled U_b's ghost column ny+2 for reflecting walls with ny % 32 == 1
 // (no-op otherwise); after every column sweep.
 void launch_ghost_fix(double* b, size_t pitch, int nx, int ny, int bc, cudaStream_t s);
+// ... and U_a's ghost row nx+2 (lower wall, nx % 32 == 1); after every row sweep.
+void launch_ghost_row_fix(double* a, size_t pitch, int nx, int ny, int bc, int wall_hi,
+                          cudaStream_t s);
+// Row-layout <-> tiled transfers of plane rows (host transfer staging, the
+// slab halo): rows[r][j + kColOff'] <-> cell (row0 + r, j) of variable v
+// (or of all 4 variables, row-interleaved, for the halo blocks).
+void launch_rows_to_tiles(const double* rows, size_t row_stride, double* u, size_t pitch, int v,
+                          int i0, int n, int ny, cudaStream_t s);
+void launch_tiles_to_rows(const double* u, size_t pitch, double* rows, size_t row_stride, int v,
+                          int i0, int n, int ny, cudaStream_t s);
+void launch_compare(const double* a, const double* b, size_t pitch, int nx, int ny,
+                    unsigned long long* out, cudaStream_t s);
 void launch_init(const InitArgs& a, cudaStream_t s);
 void launch_row_audit(const double* u, size_t pitch, int nx, int ny, unsigned long long* hashes,
                       double* sums, cudaStream_t s);

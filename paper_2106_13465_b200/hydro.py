@@ -357,6 +357,19 @@ class GpuGrid:
     def set_halo_peers(self, upper: int | None, lower: int | None):
         self._check(self._lib.hydro_gpu_set_halo_peers(self._ctx, upper or None, lower or None))
 
+    def slab_halo_pack(self):
+        self._check(self._lib.hydro_gpu_slab_halo_pack(self._ctx))
+
+    def slab_halo_unpack(self):
+        self._check(self._lib.hydro_gpu_slab_halo_unpack(self._ctx))
+
+    def compare(self, other: "GpuGrid") -> float:
+        """compare_tolerance max_rel against another context of the same
+        geometry (hydro_gpu_compare, on the device)."""
+        out = C.c_double()
+        self._check(self._lib.hydro_gpu_compare(self._ctx, other._ctx, C.byref(out)))
+        return out.value
+
     def slab_halo_out(self, step: int):
         self._check(self._lib.hydro_gpu_slab_halo_out(self._ctx, step))
 
@@ -445,8 +458,8 @@ class GpuGrid:
         return ms.value, n.value
 
     def col_offset(self) -> int:
-        """Column offset of the device layout (state()): cell (i, j) of variable
-        v is element ((i + 1) * 4 + v) * pitch + j + col_offset()."""
+        """Column offset of the device layout (state(); tiled in blocks of 32
+        rows x 8 columns x 4 variables, include/hydro_gpu.h hydro_gpu_state)."""
         return int(self._lib.hydro_gpu_col_offset())
 
     def state(self) -> tuple[int, int]:

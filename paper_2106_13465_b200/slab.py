@@ -149,13 +149,14 @@ class GpuSlab:
         return self._limits[step & 1]
 
     def halo_send(self) -> tuple[torch.Tensor, torch.Tensor]:
+        self.grid.slab_halo_pack()  # rows 1..2 / n-1..n of the tiled state -> the send blocks
         return self._halo["send_lo"], self._halo["send_hi"]
 
     def halo_recv(self) -> tuple[torch.Tensor, torch.Tensor]:
         return self._halo["recv_lo"], self._halo["recv_hi"]
 
     def halo_done(self):
-        pass  # received straight into the ghost rows
+        self.grid.slab_halo_unpack()  # the received blocks -> ghost rows
 
     def error_key(self) -> torch.Tensor:
         return self._err
