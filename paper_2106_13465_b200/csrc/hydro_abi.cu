@@ -78,7 +78,8 @@ struct hydro_gpu_ctx {
   int nranks = 1, rank = 0;
   // pinned staging ring for pageable host planes (hydro_gpu_upload/download)
   double* stage[2] = {nullptr, nullptr};     // pinned host
-  double* dstage[2] = {nullptr, nullptr};    // device (row format)
+  double* dstage[2] = {nullptr, nullptr};    // device (row format), bands
+  double* rowstage = nullptr;                // device (row format), the whole grid
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   double* halo_buf = nullptr;                // send/recv blocks of the collective halo
 };
@@ -626,6 +627,7 @@ int hydro_gpu_destroy(hydro_gpu_ctx* ctx) {
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
   if (ctx->inbox) cudaFree(ctx->inbox);
   if (ctx->halo_buf) cudaFree(ctx->halo_buf);
+  if (ctx->rowstage) cudaFree(ctx->rowstage);
   for (int b = 0; b < 2; ++b) {
     if (ctx->dstage[b]) cudaFree(ctx->dstage[b]);
     if (ctx->stage[b]) cudaFreeHost(ctx->stage[b]);
@@ -712,9 +714,37 @@ void par_copy_rows(char* dst, size_t dst_stride, const char* src, size_t src_str
 // otherwise the copies are only enqueued (pinned planes that stay alive).
 int transfer_rows(hydro_gpu_ctx* c, double* const hp[4], size_t row_stride, int i_lo, int nrows,
                   bool up, bool host_sync) {
+  const int ny = c->cfg.ny;
+  if (!host_sync && i_lo == -1 && nrows == c->cfg.nx + 4) {
+    // pinned planes, the whole grid: all DMA through a grid-sized row-format
+    // staging buffer, then one conversion kernel per plane -- the copies need
+    // no SM, so they overlap other work on the device (e.g. another
+    // context's run)
+    const size_t plane = (size_t)nrows * (ny + 4);
+    if (!c->rowstage) CUDA_TRY(c, cudaMalloc(&c->rowstage, 4 * plane * sizeof(double)));
+    // all four planes' copies back to back, the conversions on one side of
+    // them: the stream's DMA run is not broken by kernels waiting for SMs
+    const size_t rb = (size_t)(ny + 4) * 8;
+    if (up) {
+      for (int v = 0; v < 4; ++v)
+        CUDA_TRY(c, cudaMemcpy2DAsync(c->rowstage + v * plane, rb, hp[v], row_stride * 8, rb,
+                                      nrows, cudaMemcpyHostToDevice, c->stream));
+      for (int v = 0; v < 4; ++v)
+        hb::launch_rows_to_tiles(c->rowstage + v * plane, ny + 4, c->A, c->pitch, v, -1, nrows,
+                                 ny, c->stream);
+    } else {
+      for (int v = 0; v < 4; ++v)
+        hb::launch_tiles_to_rows(c->A, c->pitch, c->rowstage + v * plane, ny + 4, v, -1, nrows,
+                                 ny, c->stream);
+      for (int v = 0; v < 4; ++v)
+        CUDA_TRY(c, cudaMemcpy2DAsync(hp[v], row_stride * 8, c->rowstage + v * plane, rb, rb,
+                                      nrows, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CUDA_TRY(c, cudaGetLastError());
+    return HYDRO_GPU_OK;
+  }
   int rc = ensure_stage(c, host_sync);
   if (rc) return rc;
-  const int ny = c->cfg.ny;
   const size_t row_bytes = (size_t)(ny + 4) * 8;
   const size_t band = kStageBytes / row_bytes;
   if (band == 0) return set_err(c, HYDRO_GPU_ERR_CONFIG, "rows too long to stage");
