@@ -454,7 +454,11 @@ __device__ __forceinline__ int claim(unsigned* counter) {
 #define HB_X_MINB 4
 #endif
 #ifndef HB_Y_MINB
+#ifdef HB_TOLERANCE
+#define HB_Y_MINB 4  // 4-cell ring, 48 KB per CTA
+#else
 #define HB_Y_MINB 3  // the 8-cell ring (64 KB per CTA) allows 3 CTAs per SM anyway
+#endif
 #endif
 #ifndef HB_EX_MINB  // exact-10 sweeps (long log/exp chains, ~200 registers)
 #define HB_EX_MINB 3
@@ -1435,6 +1439,8 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
   // words
   auto swz = [](int c) { return c == 4 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B; };
   const CUtensorMapSwizzle none = CU_TENSOR_MAP_SWIZZLE_NONE;
+  maps->y_cols = CY;
+  maps->ey_cols = CE;
   return enc(&maps->x_load, A, box_x, none) && enc(&maps->x_store, B, box_x, none) &&
          enc(&maps->y_load, B, box_y, swz(CY)) && enc(&maps->y_store, A, box_y, swz(CY)) &&
          enc(&maps->ey_load, B, box_ey, swz(CE)) && enc(&maps->ey_store, A, box_ey, swz(CE));
@@ -1492,8 +1498,17 @@ void HB_SWEEP(launch_sweep_y)(const SweepArgs& a0, const TmaMaps& maps, const Ge
     if (peer) launch_sweep(sweep_y_kernel<1, true>, ctas, kExYSmemBytes, s, a, maps.ey_load, maps.ey_store);
     else launch_sweep(sweep_y_kernel<1, false>, ctas, kExYSmemBytes, s, a, maps.ey_load, maps.ey_store);
   } else {
-    if (peer) launch_sweep(sweep_y_kernel<0, true>, ctas, kYSmemBytes, s, a, maps.y_load, maps.y_store);
-    else launch_sweep(sweep_y_kernel<0, false>, ctas, kYSmemBytes, s, a, maps.y_load, maps.y_store);
+    // the maps whose box is this TU's chunk (the tolerance TU's 4-cell
+    // chunks share the exact-10 sweep's maps)
+    const bool wide = Staging<1>::C == maps.y_cols;
+    if (!wide && Staging<1>::C != maps.ey_cols) {
+      std::fprintf(stderr, "hydro_b200: no tensor map for %d-cell row chunks\n", Staging<1>::C);
+      std::abort();
+    }
+    const CUtensorMap& ld = wide ? maps.y_load : maps.ey_load;
+    const CUtensorMap& st = wide ? maps.y_store : maps.ey_store;
+    if (peer) launch_sweep(sweep_y_kernel<0, true>, ctas, kYSmemBytes, s, a, ld, st);
+    else launch_sweep(sweep_y_kernel<0, false>, ctas, kYSmemBytes, s, a, ld, st);
   }
 }
 

@@ -27,11 +27,23 @@ constexpr int kColOff = 7;
 #ifndef HB_NBUF
 #define HB_NBUF 3
 #endif
+// The HLLC row sweep: 8-cell chunks in two buffers (64 KB per CTA, 3 CTAs
+// per SM) for the bitwise TU; the tolerance TU's lighter walker fits 128
+// registers, and 4-cell chunks in three buffers give it 4 CTAs per SM
+// (gpurun_out r2fi: config 3 -4%, config 2 -3%, config 4 -8% per row sweep).
 #ifndef HB_YCHUNK
+#ifdef HB_TOLERANCE
+#define HB_YCHUNK 4
+#else
 #define HB_YCHUNK 8
 #endif
+#endif
 #ifndef HB_YNBUF
+#ifdef HB_TOLERANCE
+#define HB_YNBUF 3
+#else
 #define HB_YNBUF 2
+#endif
 #endif
 // The exact-10 row sweep keeps 4-cell chunks in three buffers: with its
 // interface memo an 8-cell ring would cost it a resident CTA per SM.
@@ -119,6 +131,7 @@ struct TmaMaps {
   CUtensorMap x_store;        // U_b: the same
   CUtensorMap ey_load;        // the exact-10 row sweep: {4 cols, 32 rows, 4 vars} of U_b
   CUtensorMap ey_store;       // ... and of U_a
+  int y_cols, ey_cols;        // box widths (columns) of the y / ey maps
 };
 
 struct PrologueArgs {
