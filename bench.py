@@ -590,8 +590,8 @@ def measure_line(env, workload, flux, math, steps, warmup, *, e2e=True, clocks=N
     out["uniform_window_identity"] = {
         "sweep_x": kt["skipped_x"] / max(1, local * kt["n_x"]),
         "sweep_y": kt["skipped_y"] / max(1, local * kt["n_y"]),
-        "note": "share of cell updates the bitwise sweeps took by the uniform-window identity "
-                "(DESIGN.md 3.1: same bits as evaluating them); the tolerance sweeps evaluate every cell"}
+        "note": "share of cell updates the sweeps took by the uniform-window identity "
+                "(DESIGN.md 3.1: the same bits as evaluating them, in either arithmetic)"}
     if kt.get("n_comm"):
         # device time of the per-step exchange (dt allreduce + inbox copy), max
         # over ranks: the communication the step exposes

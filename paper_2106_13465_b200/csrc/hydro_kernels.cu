@@ -232,16 +232,11 @@ __device__ __forceinline__ bool same_bits(const Cons& a, const Cons& b) {
 }
 
 // The uniform-window identity (below) pays where the sweeps are compute-bound
-// on uniform flow -- the bitwise mode (config 3 column/row sweeps -11%/-22%,
-// config 1 -20%/-36%).  The tolerance-mode sweeps of config 3 are already at
-// the memory system's rate and the cell compares cost them registers (config
-// 2: +7%), so that TU leaves it out.
+// on uniform flow: bitwise config 3 column/row sweeps -11%/-22%, config 1
+// -20%/-36%; tolerance config 3 -11%/-10%, config 1 -10%/-13%.  Dense flow
+// runs a walker without it (walk_strip).
 #ifndef HB_SKIP
-#ifdef HB_TOLERANCE
-#define HB_SKIP 0
-#else
 #define HB_SKIP 1
-#endif
 #endif
 
 // Walks strip cells [ka, kb] (strip coordinates: cell k holds grid index
@@ -265,11 +260,11 @@ __device__ __forceinline__ bool same_bits(const Cons& a, const Cons& b) {
 // warp takes the shortcut only when all its lanes can (no divergence), in
 // either math policy; errors are reported by the first cell of a uniform run,
 // which is evaluated (later ones would fail identically at higher indices).
-template <class M, bool WANT_DT, int FLUX, class Src, class Sink>
-__device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink, const Gas& g,
-                                           double dtdx, double spacing,
-                                           unsigned long long key_base, int kg,
-                                           unsigned long long& ekey) {
+template <class M, bool WANT_DT, int FLUX, bool SKIP, class Src, class Sink>
+__device__ __forceinline__ bool walk_strip_impl(int ka, int kb, Src& src, Sink& sink, const Gas& g,
+                                                double dtdx, double spacing,
+                                                unsigned long long key_base, int kg,
+                                                unsigned long long& ekey) {
   M m;
   if constexpr (M::kFast) m.ok = g.fast;  // divb's bounds need gamma - 1 in [2^-6, 2^6]
   const double half = 0.5 * dtdx;
@@ -285,8 +280,7 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
   // testing for kSkipCool items: the cell compares cost ~5% where they never
   // pay off.
   constexpr int kSkipCool = 8;
-  // the exact-10 sweeps take it in both TUs (their uniform cells cost a memo hit each)
-  constexpr bool kSkip = HB_SKIP || FLUX == 1;
+  constexpr bool kSkip = SKIP;
   const bool probe = kSkip && src.skip_cool == 0;
   bool saw = false;
   Cons u = src.load(ka - 2);
@@ -383,6 +377,34 @@ __device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink,
   // every range (this lane's own flag -- masked lanes included)
   src.memo_valid = memo.valid && (!M::kFast || m.ok);
   return m.ok;
+}
+
+// The walker a work item runs.  HLLC: the fast pass of a warp that is probing
+// for uniform windows runs the instantiation with the identity, every other
+// pass (a cooling-down warp on dense flow, the redo pass) one without it --
+// the compares and the shortcut's registers cost dense flow 5-8% otherwise.
+// Exact-10: one instantiation with a run-time probe (its solver is ~5k
+// instructions per copy; a second copy would not fit the instruction cache),
+// and its uniform cells are memo hits anyway.
+template <class M, bool WANT_DT, int FLUX, class Src, class Sink>
+__device__ __forceinline__ bool walk_strip(int ka, int kb, Src& src, Sink& sink, const Gas& g,
+                                           double dtdx, double spacing,
+                                           unsigned long long key_base, int kg,
+                                           unsigned long long& ekey) {
+  if constexpr (FLUX == 1) {
+    return walk_strip_impl<M, WANT_DT, FLUX, true>(ka, kb, src, sink, g, dtdx, spacing, key_base,
+                                                   kg, ekey);
+  } else if constexpr (!HB_SKIP || !M::kFast) {
+    return walk_strip_impl<M, WANT_DT, FLUX, false>(ka, kb, src, sink, g, dtdx, spacing, key_base,
+                                                    kg, ekey);
+  } else {
+    if (src.skip_cool == 0)
+      return walk_strip_impl<M, WANT_DT, FLUX, true>(ka, kb, src, sink, g, dtdx, spacing, key_base,
+                                                     kg, ekey);
+    --src.skip_cool;
+    return walk_strip_impl<M, WANT_DT, FLUX, false>(ka, kb, src, sink, g, dtdx, spacing, key_base,
+                                                    kg, ekey);
+  }
 }
 
 // Programmatic dependent launch (the sweeps are launched with
