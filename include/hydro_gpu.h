@@ -77,6 +77,12 @@ enum hydro_gpu_flux { HYDRO_GPU_FLUX_HLLC = 0, HYDRO_GPU_FLUX_EXACT10 = 1 };
  * reference is kept, and the results do not depend on the launch geometry,
  * the slab split or how a run is divided into calls. */
 enum hydro_gpu_math { HYDRO_GPU_MATH_BITWISE = 0, HYDRO_GPU_MATH_TOLERANCE = 1 };
+/* Step schedule (hydro_gpu_set_schedule): SPLIT = a column-sweep and a
+ * row-sweep launch per step; FUSED = one launch per step doing both sweeps
+ * (the column sweep's output stays in shared memory), used for the steps of a
+ * run before its last on a whole single-device HLLC domain -- bitwise the
+ * same results. */
+enum hydro_gpu_schedule { HYDRO_GPU_SCHEDULE_SPLIT = 0, HYDRO_GPU_SCHEDULE_FUSED = 1 };
 
 /* Case ids for the initialisers (cases.cpp:11-69 + BASELINE configs). */
 enum hydro_gpu_case {
@@ -307,6 +313,14 @@ int hydro_gpu_tune_order(hydro_gpu_ctx* ctx, int band_x, int band_y);
  * this context; no reference equivalent (the reference has one arithmetic).
  * Config error for an unknown mode. */
 int hydro_gpu_set_math(hydro_gpu_ctx* ctx, int math);
+/* Selects the step schedule (enum hydro_gpu_schedule; default FUSED) and the
+ * fused step's rows per work item (0 = automatic) for later runs; no
+ * reference equivalent (results do not depend on it).  Config error for an
+ * unknown schedule. */
+int hydro_gpu_set_schedule(hydro_gpu_ctx* ctx, int schedule, int seg);
+/* Summed device milliseconds and launch count of the fused steps while
+ * timing is on (hydro_gpu_set_timing). */
+int hydro_gpu_fused_times(hydro_gpu_ctx* ctx, double* ms, long long* n);
 /* Self-test of the device fp64 division (op 0), square root (op 1),
  * signed-zero-safe division (op 2) and density division (op 4: zero
  * numerators, denominators inside the fast-pass envelope [2^-256, 2^256))

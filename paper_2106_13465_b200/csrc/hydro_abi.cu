@@ -51,8 +51,11 @@ struct hydro_gpu_ctx {
   struct Pending { cudaEvent_t a, b; int kind; };
   std::vector<Pending> pending;
   size_t ev_next = 0;
-  double ms[4] = {0, 0, 0, 0};   // column sweeps, row sweeps, other, comm phases
-  long long n[4] = {0, 0, 0, 0};
+  double ms[5] = {0, 0, 0, 0, 0};   // column sweeps, row sweeps, other, comm phases, fused steps
+  long long n[5] = {0, 0, 0, 0, 0};
+  // schedule (hydro_gpu_set_schedule): fused steps where they apply
+  int schedule = HYDRO_GPU_SCHEDULE_FUSED;
+  int seg_xy = 0;
   // CUDA graphs of whole run_sequential calls, one per (steps, timing):
   // the 2*steps+3 launches replay without per-launch CPU and queue gaps.
   struct GraphEntry {
@@ -90,7 +93,8 @@ constexpr int kSlotErr = 2;
 constexpr int kSlotDtErr = 3;
 constexpr int kSlotCounters = 4;
 constexpr int kSlotSkipped = 5;  // [5], [6]: x / y cell updates taken by the uniform-window identity
-constexpr int kSlots = 7;
+constexpr int kSlotFused = 7;    // fused step: work counter, finished CTAs (2 x u32)
+constexpr int kSlots = 8;
 
 const char* kFieldName[3] = {"rho", "pres", "internal energy"};
 
@@ -268,6 +272,35 @@ void enqueue_y(hydro_gpu_ctx* c, int step, int explicit_dt, double dt, int want_
   ev_end(c, e0, 1);
 }
 
+// One fused step (hydro_fused.cuh): U_a -> U_b in a single launch when
+// `a_to_b`, else U_b -> U_a; never the last step of a run.
+void enqueue_xy(hydro_gpu_ctx* c, int step, bool a_to_b) {
+  hb::SweepArgs a = sweep_args(c, 0, step);
+  a.src = a_to_b ? c->A : c->B;
+  a.dst = a_to_b ? c->B : c->A;
+  a.dx2 = c->cfg.dy;
+  a.want_limit = 1;
+  a.seg = c->seg_xy;
+  a.counter = reinterpret_cast<unsigned*>(c->slots + kSlotFused);
+  a.done = a.counter + 1;
+  a.counter_next = nullptr;
+  a.halo_up = a.halo_dn = nullptr;
+  const CUtensorMap& ld = a_to_b ? c->maps.fa_load : c->maps.fb_load;
+  const CUtensorMap& st = a_to_b ? c->maps.fb_store : c->maps.fa_store;
+  cudaEvent_t e0{};
+  ev_begin(c, &e0);
+  if (c->math == HYDRO_GPU_MATH_TOLERANCE) hb::launch_sweep_xy_tol(a, ld, st, c->geo_tol, c->stream);
+  else hb::launch_sweep_xy(a, ld, st, c->geo, c->stream);
+  ev_end(c, e0, 4);
+}
+
+// Whether a run of this context can take fused steps: the whole domain on
+// one device (slabs exchange halos between the sweeps), HLLC.
+bool fused_ok(const hydro_gpu_ctx* c) {
+  return c->schedule == HYDRO_GPU_SCHEDULE_FUSED && c->comm == nullptr && !c->peer_up &&
+         !c->peer_dn && c->cfg.wall_lo && c->cfg.wall_hi && c->cfg.flux == HYDRO_GPU_FLUX_HLLC;
+}
+
 // wall_bc: x-wall ghost rows; full_bc: also the y-wall columns;
 // limit_step >= 0: dt limit of that step into its slot.
 void enqueue_prologue(hydro_gpu_ctx* c, int wall_bc, int full_bc, int limit_step) {
@@ -314,6 +347,7 @@ void enqueue_finish(hydro_gpu_ctx* c) {
 int reset_slots(hydro_gpu_ctx* c) {
   CUDA_TRY(c, cudaMemsetAsync(c->slots, 0xff, 4 * sizeof(unsigned long long), c->stream));
   CUDA_TRY(c, cudaMemsetAsync(c->slots + kSlotCounters, 0, sizeof(unsigned long long), c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->slots + kSlotFused, 0, sizeof(unsigned long long), c->stream));
   return 0;
 }
 
@@ -459,7 +493,22 @@ int enqueue_run(hydro_gpu_ctx* c, int steps) {
     if (c->peer_dn) rows_to_block(c, c->cfg.nx - 1, c->peer_dn);  // rows nx-1..nx
     CUDA_TRY(c, cudaGetLastError());
   }
+  // fused schedule: pairs of fused steps (U_a -> U_b -> U_a) between an
+  // optional split first step and the split last step (whose column-sweep
+  // output feeds the final ghost bands)
+  int f0 = steps, f1 = steps;  // fused steps [f0, f1)
+  if (fused_ok(c) && steps >= 3) {
+    f0 = (steps - 1) % 2;
+    f1 = steps - 1;
+  }
   for (int s = 0; s < steps; ++s) {
+    if (s >= f0 && s < f1) {
+      if (s == f0)  // the dt slot the first fused step writes (a split step leaves it set)
+        CUDA_TRY(c, cudaMemsetAsync(c->slots + ((s + 1) & 1), 0xff, sizeof(unsigned long long),
+                                    c->stream));
+      enqueue_xy(c, s, ((s - f0) & 1) == 0);
+      continue;
+    }
     if (slab) {
       rc = enqueue_exchange(c, s);
       if (rc) return rc;
@@ -496,7 +545,7 @@ bool launch_graph(hydro_gpu_ctx* c, int steps) {
   if (!entry) {
     std::vector<hydro_gpu_ctx::Pending> saved;
     saved.swap(c->pending);
-    if (c->timing) {  // two events per phase: prologue, 3 per step, finish
+    if (c->timing) {  // two events per phase: prologue, 3 per step, finish, + a memset
       const size_t need = c->graph_events.size() + 2 * (3 * (size_t)steps + 3);
       c->graph_next = c->graph_events.size();
       while (c->graph_events.size() < need) {
@@ -594,6 +643,8 @@ int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out) {
     return HYDRO_GPU_ERR_CUDA;
   }
   ctx->stream = ctx->own_stream;
+  if (const char* sch = std::getenv("HYDRO_GPU_SCHEDULE"))  // test / A-B override of the default
+    ctx->schedule = std::strcmp(sch, "split") == 0 ? HYDRO_GPU_SCHEDULE_SPLIT : HYDRO_GPU_SCHEDULE_FUSED;
   if (hb::query_geometry(&ctx->geo) != 0 || hb::query_geometry_tol(&ctx->geo_tol) != 0 ||
       !hb::make_tma_maps(&ctx->maps, ctx->A, ctx->B, ctx->pitch, c.nx, c.ny)) {
     hydro_gpu_destroy(ctx);
@@ -604,7 +655,7 @@ int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out) {
   cudaMemsetAsync(ctx->B, 0, bytes_b, ctx->stream);
   cudaMemsetAsync(ctx->inbox, 0, 4 * 8 * ctx->pitch * sizeof(double), ctx->stream);
   cudaMemsetAsync(ctx->slots, 0xff, 4 * sizeof(unsigned long long), ctx->stream);
-  cudaMemsetAsync(ctx->slots + kSlotCounters, 0, 3 * sizeof(unsigned long long), ctx->stream);
+  cudaMemsetAsync(ctx->slots + kSlotCounters, 0, 4 * sizeof(unsigned long long), ctx->stream);
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
     hydro_gpu_destroy(ctx);
     return HYDRO_GPU_ERR_CUDA;
@@ -1245,7 +1296,7 @@ int hydro_gpu_reset_counters(hydro_gpu_ctx* c) {
   cudaStreamSynchronize(c->stream);
   c->pending.clear();
   c->ev_next = 0;
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < 5; ++k) {
     c->ms[k] = 0;
     c->n[k] = 0;
   }
@@ -1261,6 +1312,26 @@ int hydro_gpu_skipped(hydro_gpu_ctx* c, uint64_t* x, uint64_t* y) {
   CUDA_TRY(c, cudaMemcpy(v, c->slots + kSlotSkipped, sizeof v, cudaMemcpyDeviceToHost));
   if (x) *x = v[0];
   if (y) *y = v[1];
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_fused_times(hydro_gpu_ctx* c, double* ms, long long* n) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  harvest(c);
+  if (ms) *ms = c->ms[4];
+  if (n) *n = c->n[4];
+  return HYDRO_GPU_OK;
+}
+
+int hydro_gpu_set_schedule(hydro_gpu_ctx* c, int schedule, int seg) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  if ((schedule != HYDRO_GPU_SCHEDULE_SPLIT && schedule != HYDRO_GPU_SCHEDULE_FUSED) || seg < 0)
+    return set_err(c, HYDRO_GPU_ERR_CONFIG, "unknown schedule");
+  if (schedule != c->schedule || seg != c->seg_xy) drop_graphs(c);
+  c->schedule = schedule;
+  c->seg_xy = seg;
   return HYDRO_GPU_OK;
 }
 

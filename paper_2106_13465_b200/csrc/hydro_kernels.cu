@@ -1055,6 +1055,9 @@ __global__ void __launch_bounds__(128, FLUX == 0 ? HB_Y_MINB : HB_EX_MINB) sweep
   }
 }
 
+// The fused step (FUSED schedule): column and row sweep in one launch.
+#include "hydro_fused.cuh"
+
 // ---------------------------------------------------------------------------
 // Start-of-run pass: apply_boundary on the physical walls of the current
 // state and compute_dt's min-reduction for the first step.
@@ -1424,6 +1427,10 @@ int HB_SWEEP(query_geometry)(Geometry* g) {
   g->ctas_y_per_sm = oy > 0 ? oy : 1;
   g->ctas_x_exact = ox1 > 0 ? ox1 : 1;
   g->ctas_y_exact = oy1 > 0 ? oy1 : 1;
+  int oxy = 0;
+  cudaFuncSetAttribute(sweep_xy_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oxy, sweep_xy_kernel<0>, 256, kFSmemBytes);
+  g->ctas_xy_per_sm = oxy > 0 ? oxy : 1;
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -1463,6 +1470,14 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
   const CUtensorMapSwizzle none = CU_TENSOR_MAP_SWIZZLE_NONE;
   maps->y_cols = CY;
   maps->ey_cols = CE;
+  // fused step: the column phase's 4-row chunks of a band (+ one block either
+  // side) -> smem [var][row][col]; the row phase stores one row of one
+  // variable (the band's kFW columns, 960 contiguous bytes of smem) per box
+  const cuuint32_t box_fl[5] = {8, (cuuint32_t)kFLoadBlocks, 4, 4, 1};
+  const cuuint32_t box_fs[5] = {8, (cuuint32_t)(kFW / 8), 1, 1, 1};
+  if (!(enc(&maps->fa_load, A, box_fl, none) && enc(&maps->fb_load, B, box_fl, none) &&
+        enc(&maps->fa_store, A, box_fs, none) && enc(&maps->fb_store, B, box_fs, none)))
+    return false;
   return enc(&maps->x_load, A, box_x, none) && enc(&maps->x_store, B, box_x, none) &&
          enc(&maps->y_load, B, box_y, swz(CY)) && enc(&maps->y_store, A, box_y, swz(CY)) &&
          enc(&maps->ey_load, B, box_ey, swz(CE)) && enc(&maps->ey_store, A, box_ey, swz(CE));
@@ -1472,10 +1487,11 @@ bool make_tma_maps(TmaMaps* maps, double* A, double* B, size_t pitch, int nx, in
 
 namespace {
 template <class... KArgs, class... Args>
-void launch_sweep(void (*kernel)(KArgs...), int ctas, int smem, cudaStream_t s, Args... args) {
+void launch_sweep_block(void (*kernel)(KArgs...), int ctas, int block, int smem, cudaStream_t s,
+                        Args... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ctas);
-  cfg.blockDim = dim3(128);
+  cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -1484,6 +1500,10 @@ void launch_sweep(void (*kernel)(KArgs...), int ctas, int smem, cudaStream_t s, 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+template <class... KArgs, class... Args>
+void launch_sweep(void (*kernel)(KArgs...), int ctas, int smem, cudaStream_t s, Args... args) {
+  launch_sweep_block(kernel, ctas, 128, smem, s, args...);
 }
 }  // namespace
 
@@ -1532,6 +1552,24 @@ void HB_SWEEP(launch_sweep_y)(const SweepArgs& a0, const TmaMaps& maps, const Ge
     if (peer) launch_sweep(sweep_y_kernel<0, true>, ctas, kYSmemBytes, s, a, ld, st);
     else launch_sweep(sweep_y_kernel<0, false>, ctas, kYSmemBytes, s, a, ld, st);
   }
+}
+
+void HB_SWEEP(launch_sweep_xy)(const SweepArgs& a0, const CUtensorMap& load, const CUtensorMap& store,
+                                const Geometry& geo, cudaStream_t s) {
+  SweepArgs a = a0;
+  const int ctas = geo.sms * geo.ctas_xy_per_sm;
+  const int nbands = (a.ny + kFW - 1) / kFW;
+  // rows per work item: about 8 items per CTA (dynamic balance), 4-row
+  // chunks, 16..256 rows
+  if (a.seg <= 0) {
+    long long seg = (long long)a.nx * nbands / ((long long)ctas * 8);
+    if (seg < 16) seg = 16;
+    if (seg > 256) seg = 256;
+    a.seg = (int)seg;
+  }
+  a.seg = (a.seg + 3) / 4 * 4;
+  a.nseg = (a.nx + a.seg - 1) / a.seg;
+  launch_sweep_block(sweep_xy_kernel<0>, ctas, 256, kFSmemBytes, s, a, load, store);
 }
 
 void HB_SWEEP(launch_prologue)(const PrologueArgs& a, cudaStream_t s) {

@@ -92,6 +92,11 @@ inline size_t pitch_for(int ny) {
   return (need + 15) / 16 * 16;        // 128-byte rows
 }
 
+// The FUSED schedule (hydro_fused.cuh): bands of kFW output columns; the
+// column phase loads kFLoadBlocks column blocks (one either side).
+constexpr int kFW = 120;
+constexpr int kFLoadBlocks = kFW / 8 + 2;
+
 struct SweepArgs {
   const double* __restrict__ src;
   double* __restrict__ dst;
@@ -120,6 +125,8 @@ struct SweepArgs {
   double* halo_up;            // row sweep: upper neighbour's inbox block for rows 1..2
   double* halo_dn;            // row sweep: lower neighbour's inbox block for rows nx-1..nx
   unsigned long long* skipped;  // cell updates taken by the uniform-window identity (counter)
+  double dx2;                 // fused step: the row sweep's spacing (dy)
+  unsigned* done;             // fused step: CTAs finished (the last one resets limit_in, counter)
 };
 
 // All maps view a tiled buffer as dims {column in block, column block, row in
@@ -132,6 +139,10 @@ struct TmaMaps {
   CUtensorMap ey_load;        // the exact-10 row sweep: {4 cols, 32 rows, 4 vars} of U_b
   CUtensorMap ey_store;       // ... and of U_a
   int y_cols, ey_cols;        // box widths (columns) of the y / ey maps
+  // fused step (hydro_fused.cuh): loads {8 cols, kFLoadBlocks blocks, 4 rows,
+  // 4 vars} -> smem [var][row][col], row stores {8 cols, kFW/8 blocks, 1 row,
+  // 1 var}, of either buffer
+  CUtensorMap fa_load, fb_load, fa_store, fb_store;
 };
 
 struct PrologueArgs {
@@ -168,6 +179,7 @@ struct Geometry {
   int ctas_y_per_sm;
   int ctas_x_exact;           // the same for the exact-10 flux instantiations
   int ctas_y_exact;
+  int ctas_xy_per_sm;         // the fused step
   int sms;
 };
 
@@ -180,6 +192,12 @@ void launch_sweep_y(const SweepArgs& a, const TmaMaps& maps, const Geometry& geo
 int query_geometry_tol(Geometry* g);
 void launch_sweep_x_tol(const SweepArgs& a, const TmaMaps& maps, const Geometry& geo, cudaStream_t s);
 void launch_sweep_y_tol(const SweepArgs& a, const TmaMaps& maps, const Geometry& geo, cudaStream_t s);
+// The fused step (one launch per time step; hydro_fused.cuh): a.src -> a.dst
+// with the maps of those buffers.  HLLC only.
+void launch_sweep_xy(const SweepArgs& a, const CUtensorMap& load, const CUtensorMap& store,
+                     const Geometry& geo, cudaStream_t s);
+void launch_sweep_xy_tol(const SweepArgs& a, const CUtensorMap& load, const CUtensorMap& store,
+                         const Geometry& geo, cudaStream_t s);
 void launch_prologue(const PrologueArgs& a, cudaStream_t s);
 void launch_prologue_tol(const PrologueArgs& a, cudaStream_t s);  // the tolerance mode's dt
 void launch_finish(const FinishArgs& a, cudaStream_t s);

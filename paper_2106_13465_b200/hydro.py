@@ -112,6 +112,7 @@ FLUX = {"hllc": 0, "exact10": 1}
 # Sweep arithmetic (include/hydro_gpu.h, enum hydro_gpu_math): "bitwise" is the
 # reference's bits; "tolerance" holds compare_tolerance max_rel <= 1e-12.
 MATH = {"bitwise": 0, "tolerance": 1}
+SCHEDULE = {"split": 0, "fused": 1}
 CASES = {"uniform": 0, "blast": 1, "sod": 2, "corner_blast": 3, "sod_x": 4, "random": 5}
 RHO, MOM_X, MOM_Y, ENER = 0, 1, 2, 3
 
@@ -444,6 +445,22 @@ class GpuGrid:
             raise ConfigError(f"unknown math mode '{math}' (expected bitwise or tolerance)")
         self._check(self._lib.hydro_gpu_set_math(self._ctx, MATH[math]))
         self.math = math
+
+    def set_schedule(self, schedule: str, seg: int = 0):
+        """hydro_gpu_set_schedule: "fused" (default: one launch per step before
+        the last, both sweeps) or "split" (a column- and a row-sweep launch per
+        step); seg = rows per fused work item (0 = automatic).  Bitwise the
+        same results."""
+        if schedule not in SCHEDULE:
+            raise ConfigError(f"unknown schedule '{schedule}' (expected split or fused)")
+        self._check(self._lib.hydro_gpu_set_schedule(self._ctx, SCHEDULE[schedule], seg))
+
+    def fused_times(self) -> tuple[float, int]:
+        """(device ms, count) of the fused steps timed with set_timing(True)."""
+        ms = C.c_double()
+        n = C.c_longlong()
+        self._check(self._lib.hydro_gpu_fused_times(self._ctx, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     # multi-rank slabs driven from C++ (hydro_gpu_comm_attach) -----------------
     def comm_attach(self, unique_id: bytes, nranks: int, rank: int):

@@ -22,15 +22,18 @@ ap.add_argument("--seg", type=int, nargs=3, default=[0, 0, 0])
 ap.add_argument("--pre", type=int, default=2, help="untimed steps before the timed ones")
 ap.add_argument("--flux", default="hllc")
 ap.add_argument("--math", default="bitwise")
+ap.add_argument("--schedule", default="split")
 a = ap.parse_args()
 ny = a.ny or a.nx
 with P.GpuGrid(a.nx, ny, 1.0 / a.nx, 1.0 / ny, P.GasModel(), a.bc, device=0, flux=a.flux,
                math=a.math) as g:
     g.tune(*a.seg)
+    g.set_schedule(a.schedule)
     g.init_case(a.case, a.seed)
     g.run(a.pre)  # warm-up / advance the flow: init, prologue, sweeps, finish
     g.set_timing(True)
     g.run(a.steps)
     t = g.kernel_times()
 print({k: round(v, 4) if isinstance(v, float) else v for k, v in t.items()})
+fm, fn = g.fused_times() if False else (0.0, 0)
 print("ms per sweep_x %.4f  sweep_y %.4f" % (t["ms_x"] / max(1, t["n_x"]), t["ms_y"] / max(1, t["n_y"])))
