@@ -45,7 +45,7 @@
 // ---- layout -------------------------------------------------------------------
 constexpr int kFStrips = kFW + 4;                 // column-phase strips j0-2 .. j0+121
 constexpr int kFLoadCols = 8 * kFLoadBlocks;      // 136: loaded columns j0-8 .. j0+127
-constexpr int kFNBA = 6;                          // U_a ring buffers
+constexpr int kFNBA = 8;                          // U_a ring buffers (a power of two)
 constexpr uint32_t kFRowBytesA = kFLoadCols * 8;  // 1088
 constexpr uint32_t kFVarBytesA = 4 * kFRowBytesA; // 4352: [var][row][col]
 constexpr uint32_t kFChunkBytes = 4 * kFVarBytesA;  // 17408
@@ -331,51 +331,91 @@ struct FusedHdr {
 };
 
 // Column-phase source for walk_strip: the U_a ring (4-row chunks, kFNBA
-// buffers, one full barrier each) and the hand-over at every completed 4-row
-// output chunk (Chunk callback).
+// buffers, one full barrier each) read through a cursor, the U_b slot rows
+// written through another, and the hand-over (Chunk callback) at every
+// completed 4-row output chunk.  kTight: walk_strip runs steady uniform runs
+// through peek/preload (the cells are consumed in order either way).
 template <class Chunk>
 struct FusedCol {
+  static constexpr bool kTight = true;
   Chunk& chunk;
   uint32_t ring;      // hb_smem offset of ring buffer 0 + this lane's column
   uint32_t bars;      // hb_smem offset of the kFNBA full barriers
-  int ka, kb;         // output strip cells (grid rows + 1)
-  unsigned q0;        // running number of the item's input chunk 0
+  int ka;             // first output strip cell
   bool active;
-  uint32_t last_addr, prev_addr;
+  // load cursor: next cell's address, cells left in its chunk, its chunk number
+  uint32_t lo_at;
+  int lo_left;
+  unsigned lo_q;
+  uint32_t at1, at2, at3;  // addresses of the last three cells taken (at3: the cell updated next)
+  Cons last, before;       // the last two cells taken (the uniform-window test)
+  Cons pre;                // a cell peeked by the tight loop, not yet taken
+  bool have;
+  // output cursor: the slot row address of the next updated cell (this
+  // lane's column), outputs left in the chunk / after it
+  uint32_t out_at, lane_off;
+  int out_left, out_rest, q;
   unsigned nskip;
   int skip_cool;
   uint32_t memo_at;
   bool memo_valid;
 
-  __device__ __forceinline__ uint32_t addr(int t) const {
-    return ring + ((q0 + (unsigned)(t >> 2)) % kFNBA) * kFChunkBytes + (t & 3) * kFRowBytesA;
-  }
   // column orientation: mom_a = mom_x (var 1), mom_b = mom_y (var 2)
   __device__ __forceinline__ static Cons get(uint32_t at) {
     const uint8_t* b = hb_smem + at;
     return {*(const double*)b, *(const double*)(b + kFVarBytesA),
             *(const double*)(b + 2 * kFVarBytesA), *(const double*)(b + 3 * kFVarBytesA)};
   }
-  __device__ __forceinline__ Cons load(int k) {
-    const int t = k - ka + 4;  // input row offset from the item's first input chunk
-    if ((t & 3) == 0 || t == 2) {
-      const unsigned q = q0 + (unsigned)(t >> 2);
-      mbar_wait((uint64_t*)(hb_smem + bars) + (q % kFNBA), (q / kFNBA) & 1u);
-    }
-    const uint32_t at = addr(t);
-    prev_addr = last_addr;
-    last_addr = at;
-    return get(at);
+  __device__ __forceinline__ void wait_chunk() const {
+    mbar_wait((uint64_t*)(hb_smem + bars) + (lo_q & (kFNBA - 1)), (lo_q / kFNBA) & 1u);
   }
-  __device__ __forceinline__ Cons reload(int k) const { return get(addr(k - ka + 4)); }
-  __device__ __forceinline__ Cons prev() const { return get(prev_addr); }
+  // item start: the first cell taken is input row i_a - 2 (row 2 of chunk 0)
+  __device__ __forceinline__ void begin(unsigned q0) {
+    lo_q = q0;
+    lo_at = ring + (q0 & (kFNBA - 1)) * kFChunkBytes + 2 * kFRowBytesA;
+    lo_left = 2;
+    have = false;
+    wait_chunk();
+  }
+  __device__ __forceinline__ Cons peek(int) {
+    if (lo_left == 0) {
+      ++lo_q;
+      lo_at = ring + (lo_q & (kFNBA - 1)) * kFChunkBytes;
+      lo_left = 4;
+      wait_chunk();
+    }
+    at3 = at2;
+    at2 = at1;
+    at1 = lo_at;
+    lo_at += kFRowBytesA;
+    --lo_left;
+    return get(at1);
+  }
+  __device__ __forceinline__ void preload(const Cons& u) {
+    pre = u;
+    have = true;
+  }
+  __device__ __forceinline__ Cons load(int k) {
+    const Cons u = have ? pre : peek(k);
+    have = false;
+    before = last;
+    last = u;
+    return u;
+  }
+  __device__ __forceinline__ Cons reload(int) const { return get(at3); }
+  __device__ __forceinline__ Cons prev() const { return before; }
   __device__ __forceinline__ void count_skip() { ++nskip; }
   // after iteration c: cell c-1 was updated (c > ka); a completed 4-row
   // output chunk (or the item's last) is handed over
   __device__ __forceinline__ void boundary(int c) {
     if (c > ka) {
-      const int o = c - 1 - ka;
-      if ((o & 3) == 3 || c - 1 == kb) chunk(o >> 2, c - 1 == kb);
+      out_at += kFRowBytesS;
+      if (--out_left == 0) {
+        const bool last_chunk = out_rest == 0;
+        out_at = chunk(q++, last_chunk) + lane_off;
+        out_left = out_rest < 4 ? out_rest : 4;
+        out_rest -= out_left;
+      }
     }
   }
 };
@@ -456,7 +496,8 @@ __global__ void __launch_bounds__(256, 1)
         if (tid == 0)
           for (int q = 0; q < kFNBA && q < nq; ++q) issue(q);
         acquire(m);
-        auto chunk = [&](int q, bool last) {
+        // publishes chunk q (slot m % kFNS); returns the slot row base of the next
+        auto chunk = [&](int q, bool last) -> uint32_t {
           const unsigned sl = m % kFNS;
           if (tid == 0) {
             FusedHdr& h = hdrs[sl];
@@ -476,15 +517,19 @@ __global__ void __launch_bounds__(256, 1)
             issue(q + kFNBA);
           }
           if (!last) acquire(m);
+          return slots0 + (m % kFNS) * kFSlotBytes;
         };
         FusedCol<decltype(chunk)> col{chunk};
         col.ring = ring0 + (uint32_t)(s + 6) * 8;
         col.bars = bars;
         col.ka = ka;
-        col.kb = kb;
-        col.q0 = q0;
         col.active = active;
-        col.last_addr = col.prev_addr = 0;
+        col.begin(q0);
+        col.lane_off = (uint32_t)(s + 14) * 8;
+        col.out_at = slots0 + (m % kFNS) * kFSlotBytes + col.lane_off;
+        col.out_left = min(4, kb - ka + 1);
+        col.out_rest = kb - ka + 1 - col.out_left;
+        col.q = 0;
         col.nskip = 0;
         col.skip_cool = skip_cool;
         col.memo_at = 0;
@@ -496,12 +541,10 @@ __global__ void __launch_bounds__(256, 1)
           q[2 * kFPos] = u.mb;
           q[3 * kFPos] = u.e;
         };
-        auto sink = [&](int k, const StepOut& o) {
-          const int ob = k - ka;
-          const unsigned sl = m % kFNS;  // the chunk being produced is published as m
-          const uint32_t row = slots0 + sl * kFSlotBytes + (ob & 3) * kFRowBytesS;
-          if (active) put_slot(row + (uint32_t)(s + 14) * 8, o.un);
+        auto sink = [&](int, const StepOut& o) {
+          if (active) put_slot(col.out_at, o.un);
           if (edge) {  // y-wall ghosts of the column-sweep output (grid.cpp:44-59)
+            const uint32_t row = col.out_at - col.lane_off;
             auto ghost = [&](int jt, bool neg) {
               Cons gh = o.un;
               if (neg) gh.mb = -gh.mb;

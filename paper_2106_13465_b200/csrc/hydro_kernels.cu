@@ -325,7 +325,7 @@ __device__ __forceinline__ bool walk_strip_impl(int ka, int kb, Src& src, Sink& 
   constexpr int kUnroll = (WANT_DT && FLUX == 0) ? HB_UNROLL : 1;
 #pragma unroll kUnroll
   for (int c = kFold ? ka : ka + 1; c <= kb + 1; ++c) {
-    const Cons uC = src.load(c + 1);
+    const Cons uC = src.load(c + 1);  // (a tight source hands over a preloaded cell)
     const bool upd = !kFold || c > ka;
     if (probe) {
       same = same_bits(uC, src.prev()) ? same + 1 : 0;
@@ -341,6 +341,25 @@ __device__ __forceinline__ bool walk_strip_impl(int ka, int kb, Src& src, Sink& 
         sink(c - 1, o);
         if (src.active) src.count_skip();
         src.boundary(c);
+        if constexpr (Src::kTight) {
+          // steady uniform run: the next cell repeats this one in every lane
+          // -> the same shortcut, without the window bookkeeping (the
+          // fused step's column phase); the first cell that differs goes
+          // back to the general iteration, preloaded
+          while (c <= kb) {
+            const Cons un = src.peek(c + 2);
+            if (!__all_sync(0xffffffffu, same_bits(un, uC) || !src.active)) {
+              src.preload(un);
+              break;
+            }
+            ++c;
+            ++same;
+            o.un = un;
+            sink(c - 1, o);
+            if (src.active) src.count_skip();
+            src.boundary(c);
+          }
+        }
         continue;
       }
     }
@@ -569,6 +588,7 @@ __device__ __forceinline__ void fence_async_smem() {
 
 template <int AXIS, int FLUX>
 struct Tiles {
+  static constexpr bool kTight = false;  // no tight uniform-run loop (walk_strip_impl)
   static constexpr int C = Staging<AXIS, FLUX>::C;
   static constexpr int NBUF = Staging<AXIS, FLUX>::NBUF;
   static constexpr int kChunkBytes = Staging<AXIS, FLUX>::kChunkBytes;
