@@ -446,21 +446,35 @@ class Measured:
             self.one_step()
         self.sync()
         kt = self.grid.kernel_times()
+        kt["ms_xy"], kt["n_xy"] = self.grid.fused_times()
         kt["ms_comm"], kt["n_comm"] = self.grid.comm_times()
         kt["skipped_x"], kt["skipped_y"] = self.grid.skipped()
         self.grid.set_timing(False)
         return kt
 
     def roofline(self, kt, clock_info):
-        """The dominant sweep kernel against the HBM roofline (algorithmic
-        64 B per cell per sweep over its mean event-timed launch), and the
-        whole step against both the HBM and the measured FP64 peaks."""
+        """The dominant kernel against the HBM roofline, and the whole time step
+        against the HBM and the measured FP64 peaks.
+
+        Algorithmic bytes of one launch: a split sweep reads and writes the
+        state once (64 B per cell: two such sweeps = 128 B per
+        cell-step); the fused step kernel (both sweeps in one pass, the
+        column sweep's output kept in shared memory) also reads and writes the
+        state once per launch -- 64 B per cell -- but completes a whole
+        cell-step with it.  `frac` is the kernel against the bytes IT must
+        move; `step.frac_survey_128B` is the step against the survey's
+        two-sweep traffic model, which a fused step may exceed."""
         peak, peak_src = peaks()
-        which = "x" if kt["ms_x"] >= kt["ms_y"] else "y"
-        n_launch = max(1, kt[f"n_{which}"])
-        avg_ms = kt[f"ms_{which}"] / n_launch
         local_cells = self.geo.nx * self.ny
         alg_bytes = local_cells * ALG_BYTES_PER_CELL_SWEEP
+        fused = kt.get("n_xy", 0) > 0 and kt["ms_xy"] >= max(kt["ms_x"], kt["ms_y"])
+        if fused:
+            which, label = "xy", "sweep_xy (fused step: column + row sweep in one launch)"
+        else:
+            which = "x" if kt["ms_x"] >= kt["ms_y"] else "y"
+            label = f"sweep_{which}"
+        n_launch = max(1, kt[f"n_{which}"])
+        avg_ms = kt[f"ms_{which}"] / n_launch
         achieved = alg_bytes / (avg_ms / 1e3) / 1e9
         traffic = None
         prof = os.path.join(ROOT, "profiles", "traffic.json")
@@ -469,17 +483,29 @@ class Measured:
             per_cell = json.load(open(prof)).get(tkey)
             if per_cell:
                 traffic = per_cell * local_cells
-        # whole step: both sweeps' device time per time step (kernel share)
-        n_steps = max(1, min(kt["n_x"], kt["n_y"]))
-        step_ms = (kt["ms_x"] + kt["ms_y"]) / n_steps
-        step_bytes = local_cells * 2 * ALG_BYTES_PER_CELL_SWEEP
-        out = {"bound": "hbm", "kernel": f"sweep_{which}", "achieved": achieved,
+        # whole time step: device time of all sweep kernels per time step
+        n_steps = max(1, kt.get("n_xy", 0) + min(kt["n_x"], kt["n_y"]))
+        step_ms = (kt["ms_x"] + kt["ms_y"] + kt.get("ms_xy", 0.0)) / n_steps
+        moved = (local_cells * ALG_BYTES_PER_CELL_SWEEP *
+                 (kt.get("n_xy", 0) + kt["n_x"] + kt["n_y"]) / n_steps)  # bytes the schedule must move
+        survey = local_cells * 2 * ALG_BYTES_PER_CELL_SWEEP
+        out = {"bound": "hbm", "kernel": label, "achieved": achieved,
                "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                "frac": achieved / peak, "traffic": traffic,
                "traffic_source": f"profiles/traffic.json {tkey}" if traffic else None,
                "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms,
-               "step": {"achieved": step_bytes / (step_ms / 1e3) / 1e9, "frac":
-                        step_bytes / (step_ms / 1e3) / 1e9 / peak, "sweeps_ms_per_time_step": step_ms}}
+               "alg_bytes_note": "64 B per cell per launch: one read + one write of the 4 fp64 "
+                                 "fields (a fused launch completes a whole cell-step with them)",
+               "step": {"sweeps_ms_per_time_step": step_ms,
+                        "achieved": moved / (step_ms / 1e3) / 1e9,
+                        "frac": moved / (step_ms / 1e3) / 1e9 / peak,
+                        "achieved_survey_128B": survey / (step_ms / 1e3) / 1e9,
+                        "frac_survey_128B": survey / (step_ms / 1e3) / 1e9 / peak,
+                        "note": "frac: bytes this schedule must move per time step (fused steps 64 "
+                                "B/cell, split steps 128 B/cell) over the sweeps' device time; "
+                                "frac_survey_128B: SURVEY 8d's two-sweep model (128 B per "
+                                "cell-step), which the fused schedule undercuts by keeping U_b "
+                                "on chip"}}
         fp = fp64_peak()
         if fp and fp.get("dfma_tflops"):
             flops = local_cells * FP64_FLOPS_PER_CELL_STEP / (step_ms / 1e3) / 1e12
@@ -579,17 +605,23 @@ def measure_line(env, workload, flux, math, steps, warmup, *, e2e=True, clocks=N
            "ms_per_step": ms / steps,
            "config": workload_config(workload, m.global_nx, flux, math, env.world),
            "roofline": m.roofline(kt, clock_info),
-           "kernel_ms": {"sweep_x": kt["ms_x"], "sweep_y": kt["ms_y"], "other": kt["ms_other"],
+           "kernel_ms": {"sweep_xy": kt["ms_xy"], "sweep_x": kt["ms_x"], "sweep_y": kt["ms_y"],
+                         "other": kt["ms_other"],
+                         "launches": {"sweep_xy": kt["n_xy"], "sweep_x": kt["n_x"],
+                                      "sweep_y": kt["n_y"], "other": kt["n_other"]},
                          "note": "event-instrumented pass of the same K bench steps"},
-           "gpu_launches": kt["n_x"] + kt["n_y"] + kt["n_other"] + steps,  # + init kernels
+           "schedule": ("fused: one sweep_xy launch per time step between a split first (odd "
+                        "step counts) and last step" if kt["n_xy"] else "split: sweep_x + sweep_y "
+                        "per time step"),
+           "gpu_launches": kt["n_xy"] + kt["n_x"] + kt["n_y"] + kt["n_other"] + steps,  # + init kernels
            "clocks": clock_info}
     if m.halo:
         out["config"]["halo"] = m.halo
         out["config"]["driver"] = m.driver
     local = m.geo.nx * m.ny
     out["uniform_window_identity"] = {
-        "sweep_x": kt["skipped_x"] / max(1, local * kt["n_x"]),
-        "sweep_y": kt["skipped_y"] / max(1, local * kt["n_y"]),
+        "sweep_x": kt["skipped_x"] / max(1, local * (kt["n_x"] + kt["n_xy"])),
+        "sweep_y": kt["skipped_y"] / max(1, local * (kt["n_y"] + kt["n_xy"])),
         "note": "share of cell updates the sweeps took by the uniform-window identity "
                 "(DESIGN.md 3.1: the same bits as evaluating them, in either arithmetic)"}
     if kt.get("n_comm"):
@@ -838,6 +870,7 @@ def main():
             "e2e_dropin": dropin,
             "gpu_launches": head["gpu_launches"],
             "kernel_ms": head["kernel_ms"],
+            "schedule": head["schedule"],
             "comm_us_per_step": head.get("comm_us_per_step"),
             "uniform_window_identity": head.get("uniform_window_identity"),
             "clocks": head["clocks"],

@@ -1,0 +1,112 @@
+"""The fused schedule (one sweep_xy launch per time step, csrc/hydro_fused.cuh)
+against the oracle and against the split schedule (sweep_x + sweep_y).
+
+Bar: bitwise.  Every cell update is a pure function of its 5-cell window
+(sweep_strip, proj/src/euler_kernel.cpp:111-223), so keeping the column
+sweep's output in shared memory must not change a bit: every plane including
+ghosts, the last dt, and the first error in the reference's order
+(schedulers.cpp:23-26,80-91) are compared exactly, in both arithmetics.
+"""
+import numpy as np
+import pytest
+
+import paper_2106_13465_b200 as P
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+MODEL = P.GasModel()
+
+
+def gpu_run(case, nx, ny, steps, bc, seed, schedule, math="bitwise", seg=0, splits=None):
+    grid = P.make_case(case, nx, ny, MODEL, seed=seed)
+    with P.GpuGrid(nx, ny, grid.dx, grid.dy, MODEL, bc, device=0, math=math) as g:
+        g.set_schedule(schedule, seg)
+        g.upload(grid.planes)
+        dts = [g.run(k) for k in (splits or [steps])]
+        g.download(grid.planes)
+        fused_launches = None
+        if schedule == "fused":
+            g.set_timing(True)
+            g.reset_counters()
+            g.run(4)
+            fused_launches = g.fused_times()[1]
+    return grid.planes, dts, fused_launches
+
+
+# band width is 120 output columns: one band, band edges, a ragged last band,
+# short and ragged row segments, both boundary conditions
+SHAPES = [
+    ("corner_blast", 64, 64, 10, "reflect", 0),
+    ("random", 96, 119, 7, "transmit", 5),
+    ("random", 40, 120, 6, "reflect", 6),
+    ("random", 40, 121, 6, "transmit", 7),
+    ("random", 130, 250, 7, "reflect", 8),
+    ("sod_x", 33, 241, 12, "transmit", 0),
+    ("corner_blast", 257, 121, 6, "reflect", 0),
+    ("random", 4, 40, 5, "transmit", 9),
+    ("random", 7, 5, 5, "reflect", 10),
+]
+
+
+@pytest.mark.parametrize("case,nx,ny,steps,bc,seed", SHAPES)
+@pytest.mark.parametrize("seg", [0, 16])
+def test_fused_schedule_matches_the_oracle_bitwise(gpu, case, nx, ny, steps, bc, seed, seg):
+    planes, dts, launches = gpu_run(case, nx, ny, steps, bc, seed, "fused", seg=seg)
+    assert launches == 2, "the fused kernel did not run (4 steps = 1 split + 2 fused + 1 split)"
+    ref = O.make_case(case, nx, ny, seed=seed)
+    dt_ref = O.run_sequential(ref, steps, bc)
+    if not np.array_equal(planes, ref.u):
+        bad = np.argwhere(planes != ref.u)
+        pytest.fail(f"{len(bad)} values differ from the oracle, first {bad[:4].tolist()}")
+    assert dts[-1] == dt_ref
+
+
+@pytest.mark.parametrize("math", ["bitwise", "tolerance"])
+@pytest.mark.parametrize("case,nx,ny,steps,bc,seed", [
+    ("random", 300, 97, 5, "transmit", 11),
+    ("corner_blast", 512, 512, 20, "reflect", 0),
+    ("random", 200, 363, 8, "reflect", 12),
+])
+def test_fused_equals_split_in_both_arithmetics(gpu, math, case, nx, ny, steps, bc, seed):
+    ps, ds, _ = gpu_run(case, nx, ny, steps, bc, seed, "split", math)
+    pf, df, _ = gpu_run(case, nx, ny, steps, bc, seed, "fused", math)
+    assert np.array_equal(ps.view(np.uint64), pf.view(np.uint64))
+    assert ds == df
+
+
+@pytest.mark.parametrize("math", ["bitwise", "tolerance"])
+def test_fused_run_splits_compose(gpu, math):
+    """run(3) + run(4) == run(7): a run's first and last steps are split
+    launches, so the fused/split pattern differs between the two."""
+    p1, d1, _ = gpu_run("random", 200, 180, 7, "reflect", 3, "fused", math)
+    p2, d2, _ = gpu_run("random", 200, 180, 7, "reflect", 3, "fused", math, splits=[3, 4])
+    assert np.array_equal(p1.view(np.uint64), p2.view(np.uint64))
+    assert d1[-1] == d2[-1]
+
+
+@pytest.mark.parametrize("schedule", ["fused", "split"])
+@pytest.mark.parametrize("cfl,case,bc", [(25.0, "corner_blast", "reflect"), (3.0, "random", "transmit"),
+                                         (12.0, "random", "reflect")])
+def test_fused_reports_the_reference_error(gpu, schedule, cfl, case, bc):
+    """CFL fault injection (test_schedulers.cpp:115-128): the same message as
+    the oracle (the reference's first throw), whichever schedule hits it."""
+    nx, ny = 96, 130
+    model = P.GasModel(cfl=cfl)
+    ref = O.make_case(case, nx, ny, seed=1)
+    ref_msg = gpu_msg = None
+    try:
+        O.run_sequential(ref, 14, bc, cfl=cfl)
+    except O.CheckerError as e:
+        ref_msg = str(e)
+    grid = P.make_case(case, nx, ny, model, seed=1)
+    with P.GpuGrid(nx, ny, grid.dx, grid.dy, model, bc, device=0) as g:
+        g.set_schedule(schedule)
+        g.upload(grid.planes)
+        try:
+            g.run(14)
+        except P.PositivityError as e:
+            gpu_msg = str(e)
+        g.download(grid.planes)
+    assert gpu_msg == ref_msg
+    if ref_msg is None:
+        assert np.array_equal(grid.planes, ref.u)

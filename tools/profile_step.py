@@ -34,6 +34,8 @@ with P.GpuGrid(a.nx, ny, 1.0 / a.nx, 1.0 / ny, P.GasModel(), a.bc, device=0, flu
     g.set_timing(True)
     g.run(a.steps)
     t = g.kernel_times()
+    fm, fn = g.fused_times()
 print({k: round(v, 4) if isinstance(v, float) else v for k, v in t.items()})
-fm, fn = g.fused_times() if False else (0.0, 0)
+if fn:
+    print("ms per fused step %.4f (%d launches)" % (fm / fn, fn))
 print("ms per sweep_x %.4f  sweep_y %.4f" % (t["ms_x"] / max(1, t["n_x"]), t["ms_y"] / max(1, t["n_y"])))
