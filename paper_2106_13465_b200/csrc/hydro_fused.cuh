@@ -53,12 +53,26 @@ constexpr int kFPos = 144;                        // slot positions: column j at
 constexpr uint32_t kFVarBytesS = kFPos * 8;       // 1152 (9 x 128)
 constexpr uint32_t kFRowBytesS = 4 * kFVarBytesS; // 4608: [row][var][pos]
 constexpr uint32_t kFSlotBytes = 4 * kFRowBytesS; // 18432
-constexpr int kFNS = 3;                           // slots (chunks in hand-over)
+#ifndef HB_FNS
+#define HB_FNS 4
+#endif
+#ifndef HB_FLAG
+#define HB_FLAG 2
+#endif
+constexpr int kFNS = HB_FNS;                      // slots (chunks in hand-over)
+// The row warps release the slot of chunk n - kFLag when they take chunk n:
+// with kFLag = 2 the stores a row warp issued for chunk n - 1 need not have
+// read their slot yet (cp.async.bulk.wait_group.read 1), so a warp never
+// waits for the stores it has just issued.
+constexpr int kFLag = HB_FLAG;
+static_assert(kFLag >= 1 && kFLag <= 2 && kFLag < kFNS, "slot release lag");
 constexpr uint32_t kFSlotOff = kFNBA * kFChunkBytes;
 constexpr uint32_t kFBarOff = kFSlotOff + kFNS * kFSlotBytes;
 constexpr uint32_t kFHdrOff = kFBarOff + kFNBA * 8;
 constexpr uint32_t kFFlagOff = kFHdrOff + kFNS * 32;
-constexpr int kFSmemBytes = (int)kFFlagOff + 16 + 128;  // + flags, alignment
+constexpr uint32_t kFUniOff = kFFlagOff + 16;       // per slot: FusedUni
+constexpr uint32_t kFUniBytes = 160;
+constexpr int kFSmemBytes = (int)(kFUniOff + kFNS * kFUniBytes) + 128;  // + alignment
 
 // ---- warp shuffles of the row phase ------------------------------------------
 __device__ __forceinline__ double shfl_up_d(double v) {
@@ -309,15 +323,17 @@ __device__ __forceinline__ void fused_row(uint32_t at, int lane, const RowGeo& r
 }
 
 // Named barriers of the column -> row hand-over (bar 0 is __syncthreads):
-// FULL(s) = 1 + s (column warps arrive, row warps sync), EMPTY(s) = 4 + s
-// (row warps arrive, column warps sync), 7 = the column warps alone.
+// FULL(s) = 1 + s (column warps arrive, row warps sync), EMPTY(s) = 1 + kFNS
+// + s (row warps arrive, column warps sync), 1 + 2 kFNS = the column warps
+// alone.
 __device__ __forceinline__ void bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-constexpr int kFBarFull = 1, kFBarEmpty = 4, kFBarCol = 7;
+constexpr int kFBarFull = 1, kFBarEmpty = 1 + kFNS, kFBarCol = 1 + 2 * kFNS;
+static_assert(kFBarCol < 16, "named barriers");
 
 // A published chunk's header (one per slot): which rows, of which pass.
 struct FusedHdr {
@@ -329,6 +345,26 @@ struct FusedHdr {
   int end;    // no more chunks
   int pad[2];
 };
+
+// What the column warps know about a published chunk (one record per slot):
+// uni[w] != 0 -- column warp w took the chunk as part of a steady uniform run
+// (every cell of its 32 strips x 4 rows bitwise equal to st[w], updated by the
+// identity), in a band without wall or inactive strips.  When all four agree
+// on one state the chunk's rows are uniform rows of that state, and the row
+// warps need not read them to know it.
+struct FusedUni {
+  int uni[4];
+  int pad[4];
+  double st[4][4];  // r, mom_x, mom_y, E (column orientation)
+};
+static_assert(sizeof(FusedUni) == kFUniBytes, "FusedUni layout");
+
+__device__ __forceinline__ unsigned long long diff_bits(const Cons& a, const Cons& b) {
+  return ((unsigned long long)__double_as_longlong(a.r) ^ (unsigned long long)__double_as_longlong(b.r)) |
+         ((unsigned long long)__double_as_longlong(a.ma) ^ (unsigned long long)__double_as_longlong(b.ma)) |
+         ((unsigned long long)__double_as_longlong(a.mb) ^ (unsigned long long)__double_as_longlong(b.mb)) |
+         ((unsigned long long)__double_as_longlong(a.e) ^ (unsigned long long)__double_as_longlong(b.e));
+}
 
 // Column-phase source for walk_strip: the U_a ring (4-row chunks, kFNBA
 // buffers, one full barrier each) read through a cursor, the U_b slot rows
@@ -359,6 +395,7 @@ struct FusedCol {
   int skip_cool;
   uint32_t memo_at;
   bool memo_valid;
+  bool cross;  // steady uniform run: every active lane of the warp holds the same state
 
   // column orientation: mom_a = mom_x (var 1), mom_b = mom_y (var 2)
   __device__ __forceinline__ static Cons get(uint32_t at) {
@@ -402,6 +439,44 @@ struct FusedCol {
     last = u;
     return u;
   }
+  // ---- whole chunks of a steady uniform run (walk_strip's tight loop) ----------
+  __device__ __forceinline__ void enter_tight(const Cons& u) {
+    cross = __all_sync(0xffffffffu, same_bits(u, shfl(u, 0)) || !active);
+  }
+  // the cursors sit on a chunk boundary: four outputs open a slot, their four
+  // incoming cells are rows 2-3 of this input chunk and rows 0-1 of the next
+  __device__ __forceinline__ bool chunk_aligned() const {
+    return out_left == 4 && lo_left == 2 && !have;
+  }
+  __device__ __forceinline__ bool chunk_equal(const Cons& u) const {
+    const unsigned nq = lo_q + 1;
+    const uint32_t nx_at = ring + (nq & (kFNBA - 1)) * kFChunkBytes;
+    mbar_wait((uint64_t*)(hb_smem + bars) + (nq & (kFNBA - 1)), (nq / kFNBA) & 1u);
+    const unsigned long long d = diff_bits(get(lo_at), u) | diff_bits(get(lo_at + kFRowBytesA), u) |
+                                 diff_bits(get(nx_at), u) | diff_bits(get(nx_at + kFRowBytesA), u);
+    return d == 0ull;
+  }
+  // takes those four cells (all equal to o.un) and hands the chunk over
+  template <class Sink>
+  __device__ __forceinline__ void take_chunk(Sink& sink, int c, const StepOut& o) {
+    ++lo_q;
+    const uint32_t nx_at = ring + (lo_q & (kFNBA - 1)) * kFChunkBytes;
+    at3 = lo_at + kFRowBytesA;
+    at2 = nx_at;
+    at1 = nx_at + kFRowBytesA;
+    lo_at = nx_at + 2 * kFRowBytesA;
+    // lo_left stays 2; last/before already hold this state
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      sink(c + k, o);
+      out_at += kFRowBytesS;
+    }
+    if (active) nskip += 4;
+    const bool last_chunk = out_rest == 0;
+    out_at = chunk(q++, last_chunk, cross, o.un) + lane_off;
+    out_left = out_rest < 4 ? out_rest : 4;
+    out_rest -= out_left;
+  }
   __device__ __forceinline__ Cons reload(int) const { return get(at3); }
   __device__ __forceinline__ Cons prev() const { return before; }
   __device__ __forceinline__ void count_skip() { ++nskip; }
@@ -412,7 +487,7 @@ struct FusedCol {
       out_at += kFRowBytesS;
       if (--out_left == 0) {
         const bool last_chunk = out_rest == 0;
-        out_at = chunk(q++, last_chunk) + lane_off;
+        out_at = chunk(q++, last_chunk, false, Cons{}) + lane_off;
         out_left = out_rest < 4 ? out_rest : 4;
         out_rest -= out_left;
       }
@@ -429,6 +504,7 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t ring0 = pad, slots0 = pad + kFSlotOff, bars = pad + kFBarOff;
   FusedHdr* const hdrs = (FusedHdr*)(hb_smem + pad + kFHdrOff);
   int* const flags = (int*)(hb_smem + pad + kFFlagOff);  // [0] claimed item, [1] redo vote
+  FusedUni* const unis = (FusedUni*)(hb_smem + pad + kFUniOff);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     for (int q = 0; q < kFNBA; ++q) mbar_init((uint64_t*)(hb_smem + bars) + q, 1);
@@ -480,6 +556,9 @@ __global__ void __launch_bounds__(256, 1)
       const int j = j0 - 2 + s;
       const bool active = s < kFStrips && j >= 1 && j <= ny;
       const bool edge = active && (j <= 2 || j >= ny - 1);
+      // a band whose 124 strips are all interior columns (no wall ghosts, no
+      // inactive strips): its uniform chunks are uniform rows
+      const bool plain = j0 - 2 > 2 && j0 + kFW + 1 < ny - 1;
       const unsigned long long base_x = error_key(a.step, 1, j, 0, 0, 0);
       auto issue = [&](int q) {  // tid 0: input chunk q of this item
         const int rr = i_a - 4 + 4 * q - 1;  // grid row - 1 of its first row
@@ -497,8 +576,18 @@ __global__ void __launch_bounds__(256, 1)
           for (int q = 0; q < kFNBA && q < nq; ++q) issue(q);
         acquire(m);
         // publishes chunk q (slot m % kFNS); returns the slot row base of the next
-        auto chunk = [&](int q, bool last) -> uint32_t {
+        auto chunk = [&](int q, bool last, bool uni, const Cons& st) -> uint32_t {
           const unsigned sl = m % kFNS;
+          if (lane == 0) {
+            FusedUni& fu = unis[sl];
+            fu.uni[warp] = uni && plain;
+            if (uni) {
+              fu.st[warp][0] = st.r;
+              fu.st[warp][1] = st.ma;
+              fu.st[warp][2] = st.mb;
+              fu.st[warp][3] = st.e;
+            }
+          }
           if (tid == 0) {
             FusedHdr& h = hdrs[sl];
             h.tag = 2 * seq + pass_no;
@@ -578,8 +667,7 @@ __global__ void __launch_bounds__(256, 1)
       hdrs[m % kFNS].first = 0;
     }
     bar_arrive(kFBarFull + (int)(m % kFNS), 256);
-    acquire(m + 1);
-    acquire(m + 2);
+    for (int k = 1; k < kFNS; ++k) acquire(m + k);
   } else {
     // ---- row phase (warps 4-7: row w-4 of each chunk, lane-parallel) ----------
     const double dtdx = dt / a.dx2;
@@ -596,13 +684,22 @@ __global__ void __launch_bounds__(256, 1)
     for (unsigned n = 0;; ++n) {
       const unsigned sl = n % kFNS;
       bar_sync(kFBarFull + (int)sl, 256);
-      if (n >= 1) {  // the previous chunk's stores have read their slot: release it
-        if (lane == 0) bulk_wait_read0();
+      if (n >= (unsigned)kFLag) {  // the stores of chunk n - kFLag have read their slot: release it
+        if (lane == 0) {
+          if constexpr (kFLag == 1) bulk_wait_read0();
+          else bulk_wait_read1();
+        }
         __syncwarp();
-        bar_arrive(kFBarEmpty + (int)((n - 1) % kFNS), 256);
+        bar_arrive(kFBarEmpty + (int)((n - kFLag) % kFNS), 256);
       }
       const FusedHdr h = hdrs[sl];
-      if (h.end) break;
+      if (h.end) {  // the slots still held
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+        for (unsigned r = n >= (unsigned)kFLag ? n - kFLag + 1 : 0; r < n; ++r)
+          bar_arrive(kFBarEmpty + (int)(r % kFNS), 256);
+        break;
+      }
       if (h.first) {
         // a redo pass of the same item supersedes the fast pass's
         // contributions; otherwise the previous pass is final
@@ -611,10 +708,36 @@ __global__ void __launch_bounds__(256, 1)
         acc.clear();
         cur = h.tag;
       }
-      if (wr >= h.nrows) continue;
+      if (wr >= h.nrows) {  // no row for this warp: an empty group keeps one group per chunk
+        if (lane == 0) bulk_commit();
+        continue;
+      }
       const int i = h.i0 + wr;
       const int gi = a.row0 + i;
       const uint32_t at = slots0 + sl * kFSlotBytes + wr * kFRowBytesS;
+      const bool lo = a.wall_lo && i <= 2, hi = a.wall_hi && i >= nx - 1;
+      // a chunk every column warp published as uniform, all in one state this
+      // warp has already evaluated to the identity in this launch: the row
+      // keeps its input (fused_row would find exactly this by reading it)
+      bool quick = false;
+      if (memo.valid && !(lo || hi)) {
+        const FusedUni& fu = unis[sl];
+        const int4 uf = *(const int4*)fu.uni;
+        if (uf.x & uf.y & uf.z & uf.w) {
+          // row orientation: mom_a = mom_y (st[2]), mom_b = mom_x (st[1])
+          unsigned long long d = 0ull;
+#pragma unroll
+          for (int w2 = 0; w2 < 4; ++w2) {
+            const double2 ab = *(const double2*)&fu.st[w2][0], cd = *(const double2*)&fu.st[w2][2];
+            d |= diff_bits(Cons{ab.x, cd.x, ab.y, cd.y}, memo.u);
+          }
+          quick = d == 0ull;
+        }
+      }
+      if (quick) {
+        if (lane >= 1 && lane <= 30) acc.nskip += 4;
+        acc.spd = smax(acc.spd, memo.spd);
+      } else {
       RowGeo rg;
       rg.j0 = h.j0;
       rg.jb = h.j0 - 4 + 4 * lane;
@@ -627,7 +750,6 @@ __global__ void __launch_bounds__(256, 1)
       bool outk[4];
       fused_row(at, lane, rg, ny, g, dtdx, memo, acc, out, outk);
       // x-wall ghost rows of the next step (grid.cpp:26-42)
-      const bool lo = a.wall_lo && i <= 2, hi = a.wall_hi && i >= nx - 1;
       if (lo || hi) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -653,6 +775,7 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
       }
+      }  // !quick
       fence_async_smem();
       __syncwarp();
       if (lane == 0) {

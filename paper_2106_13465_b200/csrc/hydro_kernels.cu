@@ -346,7 +346,18 @@ __device__ __forceinline__ bool walk_strip_impl(int ka, int kb, Src& src, Sink& 
           // -> the same shortcut, without the window bookkeeping (the
           // fused step's column phase); the first cell that differs goes
           // back to the general iteration, preloaded
+          src.enter_tight(uC);
           while (c <= kb) {
+            // a whole output chunk at once where the cursors sit on a chunk
+            // boundary: its four incoming cells compared with one vote
+            if (c + 3 <= kb && src.chunk_aligned() &&
+                __all_sync(0xffffffffu, src.chunk_equal(uC) || !src.active)) {
+              o.un = uC;  // the same bits
+              src.take_chunk(sink, c, o);
+              c += 4;
+              same += 4;
+              continue;
+            }
             const Cons un = src.peek(c + 2);
             if (!__all_sync(0xffffffffu, same_bits(un, uC) || !src.active)) {
               src.preload(un);
@@ -556,6 +567,9 @@ __device__ __forceinline__ void tma_store5(const CUtensorMap* map, const void* s
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() {

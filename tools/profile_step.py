@@ -23,12 +23,13 @@ ap.add_argument("--pre", type=int, default=2, help="untimed steps before the tim
 ap.add_argument("--flux", default="hllc")
 ap.add_argument("--math", default="bitwise")
 ap.add_argument("--schedule", default="split")
+ap.add_argument("--fseg", type=int, default=0, help="rows per fused work item (0 = automatic)")
 a = ap.parse_args()
 ny = a.ny or a.nx
 with P.GpuGrid(a.nx, ny, 1.0 / a.nx, 1.0 / ny, P.GasModel(), a.bc, device=0, flux=a.flux,
                math=a.math) as g:
     g.tune(*a.seg)
-    g.set_schedule(a.schedule)
+    g.set_schedule(a.schedule, a.fseg)
     g.init_case(a.case, a.seed)
     g.run(a.pre)  # warm-up / advance the flow: init, prologue, sweeps, finish
     g.set_timing(True)
