@@ -449,6 +449,7 @@ class Measured:
         kt["ms_xy"], kt["n_xy"] = self.grid.fused_times()
         kt["ms_comm"], kt["n_comm"] = self.grid.comm_times()
         kt["skipped_x"], kt["skipped_y"] = self.grid.skipped()
+        kt["auto_fused"], kt["auto_share"] = self.grid.schedule_choice()
         self.grid.set_timing(False)
         return kt
 
@@ -610,9 +611,13 @@ def measure_line(env, workload, flux, math, steps, warmup, *, e2e=True, clocks=N
                          "launches": {"sweep_xy": kt["n_xy"], "sweep_x": kt["n_x"],
                                       "sweep_y": kt["n_y"], "other": kt["n_other"]},
                          "note": "event-instrumented pass of the same K bench steps"},
-           "schedule": ("fused: one sweep_xy launch per time step between a split first (odd "
-                        "step counts) and last step" if kt["n_xy"] else "split: sweep_x + sweep_y "
-                        "per time step"),
+           "schedule": {"ran": ("fused: one sweep_xy launch per time step between a split first "
+                                "(odd step counts) and last step" if kt["n_xy"] else
+                                "split: sweep_x + sweep_y per time step"),
+                        "how": "auto (hydro_gpu_set_schedule default): fused where the share of "
+                               "uniform-window updates of the context's last completed runs is >= "
+                               "0.6, else split; bitwise the same results",
+                        "uniform_share_behind_choice": kt["auto_share"]},
            "gpu_launches": kt["n_xy"] + kt["n_x"] + kt["n_y"] + kt["n_other"] + steps,  # + init kernels
            "clocks": clock_info}
     if m.halo:

@@ -81,8 +81,15 @@ enum hydro_gpu_math { HYDRO_GPU_MATH_BITWISE = 0, HYDRO_GPU_MATH_TOLERANCE = 1 }
  * row-sweep launch per step; FUSED = one launch per step doing both sweeps
  * (the column sweep's output stays in shared memory), used for the steps of a
  * run before its last on a whole single-device HLLC domain -- bitwise the
- * same results. */
-enum hydro_gpu_schedule { HYDRO_GPU_SCHEDULE_SPLIT = 0, HYDRO_GPU_SCHEDULE_FUSED = 1 };
+ * same results.  AUTO (the default) picks between them per run from the
+ * share of cell updates the context's last completed runs took by the
+ * uniform-window identity (fused above 0.6: memory-bound flow; split below:
+ * dense flow); a context's first run is fused. */
+enum hydro_gpu_schedule {
+  HYDRO_GPU_SCHEDULE_SPLIT = 0,
+  HYDRO_GPU_SCHEDULE_FUSED = 1,
+  HYDRO_GPU_SCHEDULE_AUTO = 2
+};
 
 /* Case ids for the initialisers (cases.cpp:11-69 + BASELINE configs). */
 enum hydro_gpu_case {
@@ -313,11 +320,15 @@ int hydro_gpu_tune_order(hydro_gpu_ctx* ctx, int band_x, int band_y);
  * this context; no reference equivalent (the reference has one arithmetic).
  * Config error for an unknown mode. */
 int hydro_gpu_set_math(hydro_gpu_ctx* ctx, int math);
-/* Selects the step schedule (enum hydro_gpu_schedule; default FUSED) and the
+/* Selects the step schedule (enum hydro_gpu_schedule; default AUTO) and the
  * fused step's rows per work item (0 = automatic) for later runs; no
  * reference equivalent (results do not depend on it).  Config error for an
  * unknown schedule. */
 int hydro_gpu_set_schedule(hydro_gpu_ctx* ctx, int schedule, int seg);
+/* What the next run of this context would do: *fused = 1 if it takes fused
+ * steps; *share = the uniform-window share behind an AUTO choice (-1 before
+ * the first completed run). */
+int hydro_gpu_schedule_choice(hydro_gpu_ctx* ctx, int* fused, double* share);
 /* Summed device milliseconds and launch count of the fused steps while
  * timing is on (hydro_gpu_set_timing). */
 int hydro_gpu_fused_times(hydro_gpu_ctx* ctx, double* ms, long long* n);

@@ -95,6 +95,7 @@ def lib() -> C.CDLL:
         "hydro_gpu_set_math": ([_ctx, i], i),
         "hydro_gpu_set_schedule": ([_ctx, i, i], i),
         "hydro_gpu_fused_times": ([_ctx, _dp, P(C.c_longlong)], i),
+        "hydro_gpu_schedule_choice": ([_ctx, P(C.c_int), _dp], i),
         "hydro_gpu_state": ([_ctx, P(_dp), P(sz)], i),
         "hydro_gpu_col_offset": ([], i),
         "hydro_gpu_comm_unique_id": ([C.c_void_p], i),

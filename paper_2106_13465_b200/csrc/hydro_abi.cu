@@ -54,13 +54,22 @@ struct hydro_gpu_ctx {
   double ms[5] = {0, 0, 0, 0, 0};   // column sweeps, row sweeps, other, comm phases, fused steps
   long long n[5] = {0, 0, 0, 0, 0};
   // schedule (hydro_gpu_set_schedule): fused steps where they apply
-  int schedule = HYDRO_GPU_SCHEDULE_FUSED;
+  int schedule = HYDRO_GPU_SCHEDULE_AUTO;
   int seg_xy = 0;
+  // AUTO: the current choice, and what it is decided from -- the share of
+  // cell updates the last completed runs took by the uniform-window identity
+  // (the sweeps' counters, copied into pinned memory at the end of every run)
+  bool auto_fused = true;
+  unsigned long long* stat_host = nullptr;     // pinned: cumulative counters after the last run
+  unsigned long long stat_seen = 0;            // their sum when the choice was last made
+  double stat_sweeps = 0;                      // cell-sweeps enqueued since then
+  double stat_share = -1.0;                    // the share behind the current choice
   // CUDA graphs of whole run_sequential calls, one per (steps, timing):
   // the 2*steps+3 launches replay without per-launch CPU and queue gaps.
   struct GraphEntry {
     int steps;
     bool timing;
+    bool fused;
     cudaGraphExec_t exec;
     std::vector<Pending> events;  // event pairs recorded inside the graph
   };
@@ -294,10 +303,33 @@ void enqueue_xy(hydro_gpu_ctx* c, int step, bool a_to_b) {
   ev_end(c, e0, 4);
 }
 
+// The AUTO schedule's choice, remade whenever the stream is idle and a run has
+// completed since the last one: fused steps stream the state once per step
+// but run 8 warps per SM, split sweeps stream it twice with 16 -- fused wins
+// where most updates are uniform-window identities (memory-bound flow), split
+// on dense flow (latency-bound FP64 chains).  The results are bitwise the
+// same either way; the first run of a context is fused.
+constexpr double kAutoFusedShare = 0.6;
+void auto_choose(hydro_gpu_ctx* c) {
+  if (c->schedule != HYDRO_GPU_SCHEDULE_AUTO || c->stat_sweeps <= 0 || !c->stat_host) return;
+  if (cudaStreamQuery(c->stream) != cudaSuccess) {
+    cudaGetLastError();  // runs still in flight: keep the choice
+    return;
+  }
+  const unsigned long long cur = c->stat_host[0] + c->stat_host[1];
+  const unsigned long long seen = cur >= c->stat_seen ? c->stat_seen : 0;
+  c->stat_share = (double)(cur - seen) / c->stat_sweeps;
+  c->auto_fused = c->stat_share >= kAutoFusedShare;
+  c->stat_seen = cur;
+  c->stat_sweeps = 0;
+}
+
 // Whether a run of this context can take fused steps: the whole domain on
 // one device (slabs exchange halos between the sweeps), HLLC.
 bool fused_ok(const hydro_gpu_ctx* c) {
-  return c->schedule == HYDRO_GPU_SCHEDULE_FUSED && c->comm == nullptr && !c->peer_up &&
+  const bool want = c->schedule == HYDRO_GPU_SCHEDULE_FUSED ||
+                    (c->schedule == HYDRO_GPU_SCHEDULE_AUTO && c->auto_fused);
+  return want && c->comm == nullptr && !c->peer_up &&
          !c->peer_dn && c->cfg.wall_lo && c->cfg.wall_hi && c->cfg.flux == HYDRO_GPU_FLUX_HLLC;
 }
 
@@ -517,6 +549,9 @@ int enqueue_run(hydro_gpu_ctx* c, int steps) {
     enqueue_y(c, s, 0, 0.0, s + 1 < steps);
   }
   enqueue_finish(c);
+  if (c->stat_host)  // the uniform-window counters for the AUTO schedule's next choice
+    CUDA_TRY(c, cudaMemcpyAsync(c->stat_host, c->slots + kSlotSkipped, 2 * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, c->stream));
   if (slab) {
     unsigned long long* keys = c->slots + kSlotErr;  // the error and the pending dt error
     NCCL_TRY(c, nccl().all_reduce(keys, keys, 2, ncclUint64, ncclMin, c->comm, c->stream));
@@ -540,8 +575,9 @@ bool launch_graph(hydro_gpu_ctx* c, int steps) {
     harvest(c);
   }
   hydro_gpu_ctx::GraphEntry* entry = nullptr;
+  const bool fused = fused_ok(c);
   for (auto& e : c->graphs)
-    if (e.steps == steps && e.timing == c->timing) entry = &e;
+    if (e.steps == steps && e.timing == c->timing && e.fused == fused) entry = &e;
   if (!entry) {
     std::vector<hydro_gpu_ctx::Pending> saved;
     saved.swap(c->pending);
@@ -578,7 +614,7 @@ bool launch_graph(hydro_gpu_ctx* c, int steps) {
       cudaGraphExecDestroy(c->graphs.front().exec);
       c->graphs.erase(c->graphs.begin());
     }
-    c->graphs.push_back({steps, c->timing, exec, {}});
+    c->graphs.push_back({steps, c->timing, fused, exec, {}});
     entry = &c->graphs.back();
     entry->events.swap(c->pending);
     c->pending.swap(saved);
@@ -644,7 +680,15 @@ int hydro_gpu_create(const hydro_gpu_cfg* cfg, hydro_gpu_ctx** out) {
   }
   ctx->stream = ctx->own_stream;
   if (const char* sch = std::getenv("HYDRO_GPU_SCHEDULE"))  // test / A-B override of the default
-    ctx->schedule = std::strcmp(sch, "split") == 0 ? HYDRO_GPU_SCHEDULE_SPLIT : HYDRO_GPU_SCHEDULE_FUSED;
+    ctx->schedule = std::strcmp(sch, "split") == 0   ? HYDRO_GPU_SCHEDULE_SPLIT
+                    : std::strcmp(sch, "fused") == 0 ? HYDRO_GPU_SCHEDULE_FUSED
+                                                     : HYDRO_GPU_SCHEDULE_AUTO;
+  if (cudaMallocHost(&ctx->stat_host, 2 * sizeof(unsigned long long)) == cudaSuccess) {
+    ctx->stat_host[0] = ctx->stat_host[1] = 0;
+  } else {
+    ctx->stat_host = nullptr;  // AUTO then keeps its first choice
+    cudaGetLastError();
+  }
   if (hb::query_geometry(&ctx->geo) != 0 || hb::query_geometry_tol(&ctx->geo_tol) != 0 ||
       !hb::make_tma_maps(&ctx->maps, ctx->A, ctx->B, ctx->pitch, c.nx, c.ny)) {
     hydro_gpu_destroy(ctx);
@@ -675,6 +719,7 @@ int hydro_gpu_destroy(hydro_gpu_ctx* ctx) {
   if (ctx->A) cudaFree(ctx->A);
   if (ctx->B) cudaFree(ctx->B);
   if (ctx->slots) cudaFree(ctx->slots);
+  if (ctx->stat_host) cudaFreeHost(ctx->stat_host);
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
   if (ctx->inbox) cudaFree(ctx->inbox);
   if (ctx->halo_buf) cudaFree(ctx->halo_buf);
@@ -976,6 +1021,8 @@ int hydro_gpu_run_async(hydro_gpu_ctx* c, int steps) {
   if (steps > HYDRO_GPU_MAX_STEPS)
     return set_err(c, HYDRO_GPU_ERR_CONFIG, "more than %d steps in one call", HYDRO_GPU_MAX_STEPS);
   DeviceGuard g(c->device);
+  auto_choose(c);
+  c->stat_sweeps += 2.0 * steps * (double)c->cfg.nx * (double)c->cfg.ny;
   if (steps >= 2 && launch_graph(c, steps)) {
     CUDA_TRY(c, cudaGetLastError());
     return HYDRO_GPU_OK;
@@ -1301,6 +1348,9 @@ int hydro_gpu_reset_counters(hydro_gpu_ctx* c) {
     c->n[k] = 0;
   }
   CUDA_TRY(c, cudaMemset(c->slots + kSlotSkipped, 0, 2 * sizeof(unsigned long long)));
+  if (c->stat_host) c->stat_host[0] = c->stat_host[1] = 0;
+  c->stat_seen = 0;
+  c->stat_sweeps = 0;
   return HYDRO_GPU_OK;
 }
 
@@ -1325,9 +1375,17 @@ int hydro_gpu_fused_times(hydro_gpu_ctx* c, double* ms, long long* n) {
   return HYDRO_GPU_OK;
 }
 
+int hydro_gpu_schedule_choice(hydro_gpu_ctx* c, int* fused, double* share) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  if (fused) *fused = fused_ok(c) ? 1 : 0;
+  if (share) *share = c->stat_share;
+  return HYDRO_GPU_OK;
+}
+
 int hydro_gpu_set_schedule(hydro_gpu_ctx* c, int schedule, int seg) {
   if (!c) return HYDRO_GPU_ERR_CONFIG;
-  if ((schedule != HYDRO_GPU_SCHEDULE_SPLIT && schedule != HYDRO_GPU_SCHEDULE_FUSED) || seg < 0)
+  if ((schedule != HYDRO_GPU_SCHEDULE_SPLIT && schedule != HYDRO_GPU_SCHEDULE_FUSED &&
+       schedule != HYDRO_GPU_SCHEDULE_AUTO) || seg < 0)
     return set_err(c, HYDRO_GPU_ERR_CONFIG, "unknown schedule");
   if (schedule != c->schedule || seg != c->seg_xy) drop_graphs(c);
   c->schedule = schedule;

@@ -112,7 +112,7 @@ FLUX = {"hllc": 0, "exact10": 1}
 # Sweep arithmetic (include/hydro_gpu.h, enum hydro_gpu_math): "bitwise" is the
 # reference's bits; "tolerance" holds compare_tolerance max_rel <= 1e-12.
 MATH = {"bitwise": 0, "tolerance": 1}
-SCHEDULE = {"split": 0, "fused": 1}
+SCHEDULE = {"split": 0, "fused": 1, "auto": 2}
 CASES = {"uniform": 0, "blast": 1, "sod": 2, "corner_blast": 3, "sod_x": 4, "random": 5}
 RHO, MOM_X, MOM_Y, ENER = 0, 1, 2, 3
 
@@ -447,13 +447,21 @@ class GpuGrid:
         self.math = math
 
     def set_schedule(self, schedule: str, seg: int = 0):
-        """hydro_gpu_set_schedule: "fused" (default: one launch per step before
-        the last, both sweeps) or "split" (a column- and a row-sweep launch per
-        step); seg = rows per fused work item (0 = automatic).  Bitwise the
-        same results."""
+        """hydro_gpu_set_schedule: "fused" (one launch per step before the
+        last, both sweeps), "split" (a column- and a row-sweep launch per
+        step) or "auto" (default: fused where the last runs' updates were
+        mostly uniform-window identities, split on dense flow); seg = rows
+        per fused work item (0 = automatic).  Bitwise the same results."""
         if schedule not in SCHEDULE:
-            raise ConfigError(f"unknown schedule '{schedule}' (expected split or fused)")
+            raise ConfigError(f"unknown schedule '{schedule}' (expected split, fused or auto)")
         self._check(self._lib.hydro_gpu_set_schedule(self._ctx, SCHEDULE[schedule], seg))
+
+    def schedule_choice(self) -> tuple[bool, float]:
+        """hydro_gpu_schedule_choice: (the next run takes fused steps, the
+        uniform-window share behind an automatic choice or -1)."""
+        f, sh = C.c_int(), C.c_double()
+        self._check(self._lib.hydro_gpu_schedule_choice(self._ctx, C.byref(f), C.byref(sh)))
+        return bool(f.value), sh.value
 
     def fused_times(self) -> tuple[float, int]:
         """(device ms, count) of the fused steps timed with set_timing(True)."""
