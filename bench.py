@@ -420,7 +420,7 @@ class Measured:
         self.grid.set_timing(False)
         for _ in range(warmup):
             self.one_step()
-        self.sync()
+            self.sync()  # (the AUTO schedule settles its choice between completed runs)
         env.barrier()
         torch.cuda.synchronize()
         if clocks:

@@ -785,14 +785,26 @@ int ensure_stage(hydro_gpu_ctx* c, bool pinned) {
   return HYDRO_GPU_OK;
 }
 
-// rows [0, n) of `row_bytes` each, src/dst strides in bytes, on up to 8 threads
+// rows [0, n) of `row_bytes` each, src/dst strides in bytes, on up to 16 threads
 void par_copy_rows(char* dst, size_t dst_stride, const char* src, size_t src_stride, size_t n,
                    size_t row_bytes) {
   const size_t total = n * row_bytes;
+  static const unsigned cap = [] {  // HYDRO_GPU_COPY_THREADS overrides the default of 16
+    const char* e = std::getenv("HYDRO_GPU_COPY_THREADS");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? (unsigned)v : 16u;
+  }();
   unsigned nt = std::thread::hardware_concurrency();
-  nt = nt < 1 ? 1 : (nt > 8 ? 8 : nt);
+  nt = nt < 1 ? 1 : (nt > cap ? cap : nt);
   if (total < (4u << 20)) nt = 1;
+  // dense rows on both sides (a Grid2D plane <-> the pinned band): one large
+  // memcpy per thread, which libc streams with non-temporal stores
+  const bool dense = dst_stride == row_bytes && src_stride == row_bytes;
   auto work = [&](size_t a, size_t b) {
+    if (dense) {
+      std::memcpy(dst + a * row_bytes, src + a * row_bytes, (b - a) * row_bytes);
+      return;
+    }
     for (size_t r = a; r < b; ++r) std::memcpy(dst + r * dst_stride, src + r * src_stride, row_bytes);
   };
   if (nt == 1) {

@@ -65,6 +65,7 @@ constexpr int kFNS = HB_FNS;                      // slots (chunks in hand-over)
 // read their slot yet (cp.async.bulk.wait_group.read 1), so a warp never
 // waits for the stores it has just issued.
 constexpr int kFLag = HB_FLAG;
+
 static_assert(kFLag >= 1 && kFLag <= 2 && kFLag < kFNS, "slot release lag");
 constexpr uint32_t kFSlotOff = kFNBA * kFChunkBytes;
 constexpr uint32_t kFBarOff = kFSlotOff + kFNS * kFSlotBytes;
