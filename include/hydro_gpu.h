@@ -79,9 +79,9 @@ enum hydro_gpu_flux { HYDRO_GPU_FLUX_HLLC = 0, HYDRO_GPU_FLUX_EXACT10 = 1 };
 enum hydro_gpu_math { HYDRO_GPU_MATH_BITWISE = 0, HYDRO_GPU_MATH_TOLERANCE = 1 };
 /* Step schedule (hydro_gpu_set_schedule): SPLIT = a column-sweep and a
  * row-sweep launch per step; FUSED = one launch per step doing both sweeps
- * (the column sweep's output stays in shared memory), used for the steps of a
- * run before its last on a whole single-device HLLC domain -- bitwise the
- * same results.  AUTO (the default) picks between them per run from the
+ * (the column sweep's output stays in shared memory), used on a whole
+ * single-device HLLC domain for every step of a run (after one split step
+ * when the step count is odd) -- bitwise the same results.  AUTO (the default) picks between them per run from the
  * share of cell updates the context's last completed runs took by the
  * uniform-window identity (fused above 0.6: memory-bound flow; split below:
  * dense flow); a context's first run is fused. */

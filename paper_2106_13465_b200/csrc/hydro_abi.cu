@@ -283,12 +283,13 @@ void enqueue_y(hydro_gpu_ctx* c, int step, int explicit_dt, double dt, int want_
 
 // One fused step (hydro_fused.cuh): U_a -> U_b in a single launch when
 // `a_to_b`, else U_b -> U_a; never the last step of a run.
-void enqueue_xy(hydro_gpu_ctx* c, int step, bool a_to_b) {
+void enqueue_xy(hydro_gpu_ctx* c, int step, bool a_to_b, bool last) {
   hb::SweepArgs a = sweep_args(c, 0, step);
+  a.last_step = last ? 1 : 0;
   a.src = a_to_b ? c->A : c->B;
   a.dst = a_to_b ? c->B : c->A;
   a.dx2 = c->cfg.dy;
-  a.want_limit = 1;
+  a.want_limit = last ? 0 : 1;  // (the reference computes no dt after its last step)
   a.seg = c->seg_xy;
   a.counter = reinterpret_cast<unsigned*>(c->slots + kSlotFused);
   a.done = a.counter + 1;
@@ -525,20 +526,20 @@ int enqueue_run(hydro_gpu_ctx* c, int steps) {
     if (c->peer_dn) rows_to_block(c, c->cfg.nx - 1, c->peer_dn);  // rows nx-1..nx
     CUDA_TRY(c, cudaGetLastError());
   }
-  // fused schedule: pairs of fused steps (U_a -> U_b -> U_a) between an
-  // optional split first step and the split last step (whose column-sweep
-  // output feeds the final ghost bands)
+  // fused schedule: pairs of fused steps (U_a -> U_b -> U_a) after a split
+  // first step when the count is odd; the last one leaves the final ghost
+  // bands behind (finish_kernel's job after a split last step)
   int f0 = steps, f1 = steps;  // fused steps [f0, f1)
-  if (fused_ok(c) && steps >= 3) {
-    f0 = (steps - 1) % 2;
-    f1 = steps - 1;
+  if (fused_ok(c) && steps >= 2) {
+    f0 = steps % 2;
+    f1 = steps;
   }
   for (int s = 0; s < steps; ++s) {
     if (s >= f0 && s < f1) {
       if (s == f0)  // the dt slot the first fused step writes (a split step leaves it set)
         CUDA_TRY(c, cudaMemsetAsync(c->slots + ((s + 1) & 1), 0xff, sizeof(unsigned long long),
                                     c->stream));
-      enqueue_xy(c, s, ((s - f0) & 1) == 0);
+      enqueue_xy(c, s, ((s - f0) & 1) == 0, s + 1 == steps);
       continue;
     }
     if (slab) {
@@ -548,7 +549,7 @@ int enqueue_run(hydro_gpu_ctx* c, int steps) {
     enqueue_x(c, s, 0, 0.0);
     enqueue_y(c, s, 0, 0.0, s + 1 < steps);
   }
-  enqueue_finish(c);
+  if (f0 == f1) enqueue_finish(c);  // (a fused last step has left the final ghost bands)
   if (c->stat_host)  // the uniform-window counters for the AUTO schedule's next choice
     CUDA_TRY(c, cudaMemcpyAsync(c->stat_host, c->slots + kSlotSkipped, 2 * sizeof(unsigned long long),
                                 cudaMemcpyDeviceToHost, c->stream));

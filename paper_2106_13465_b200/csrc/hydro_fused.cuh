@@ -39,8 +39,15 @@
 // a state whose (uniform-window) update this warp already evaluated to the
 // identity in this launch keeps its input (the same bits as evaluating it).
 //
-// Not fused: the last step of a run (its column-sweep output feeds the final
-// ghost bands, finish_kernel), slabs (multi-GPU halo), the exact-10 flux.
+// The run's last step (last_step) leaves the reference's final ghost bands
+// behind instead of the next step's: its last apply_boundary ran on the
+// column-sweep output, so the x-wall ghost rows come from the row phase's
+// inputs and the y-wall ghost columns from the slot (finish_kernel's job in
+// the split schedule).
+//
+// Not fused: one leading step of a run with an odd step count (the state
+// ping-pongs between the two buffers and must end in the first), slabs
+// (multi-GPU halo), the exact-10 flux.
 
 // ---- layout -------------------------------------------------------------------
 constexpr int kFStrips = kFW + 4;                 // column-phase strips j0-2 .. j0+121
@@ -240,8 +247,7 @@ __device__ __forceinline__ bool row_eval(const Cons (&u)[4], const bool (&outk)[
 // orientation (the row sweep's): mom_a = mom_y (var 2), mom_b = mom_x (var 1).
 __device__ __forceinline__ void fused_row(uint32_t at, int lane, const RowGeo& rg, int ny,
                                           const Gas& g, double dtdx, RowMemo& memo, RowAcc& acc,
-                                          Cons (&out)[4], bool (&outk)[4]) {
-  Cons u[4];
+                                          Cons (&u)[4], Cons (&out)[4], bool (&outk)[4]) {
   {
     const uint8_t* p = hb_smem + at + (12 + 4 * lane) * 8;
     const double2 r01 = *(const double2*)(p), r23 = *(const double2*)(p + 16);
@@ -496,7 +502,7 @@ struct FusedCol {
   }
 };
 
-template <int UNUSED>
+template <int LAST>
 __global__ void __launch_bounds__(256, 1)
     sweep_xy_kernel(SweepArgs a, const __grid_constant__ CUtensorMap load_map,
                     const __grid_constant__ CUtensorMap store_map) {
@@ -747,16 +753,19 @@ __global__ void __launch_bounds__(256, 1)
       rg.ohi = h.j0 + kFW - 1 < ny ? h.j0 + kFW - 1 : ny;
       rg.key_base = error_key(a.step, 2, gi, 0, 0, 0);
       rg.dt_base = error_key(a.step + 1, 0, gi, 0, 0, 0);
-      Cons out[4];
+      Cons uin[4], out[4];
       bool outk[4];
-      fused_row(at, lane, rg, ny, g, dtdx, memo, acc, out, outk);
-      // x-wall ghost rows of the next step (grid.cpp:26-42)
+      fused_row(at, lane, rg, ny, g, dtdx, memo, acc, uin, out, outk);
+      // x-wall ghost rows (grid.cpp:26-42): of the next step, from this row's
+      // update -- or, in the run's last step, the ones the reference leaves
+      // behind: its last apply_boundary ran on the column-sweep output
+      // (schedulers.cpp:103-116), this row's input
       if (lo || hi) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           if (!outk[k]) continue;
           const int jj = rg.jb + k;
-          Cons gh = out[k];
+          Cons gh = LAST ? uin[k] : out[k];
           auto put = [&](int ii) {
             double* q2 = dst + cell_index(pitch, 0, ii, jj);
             q2[0] = gh.r;
@@ -777,6 +786,15 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       }  // !quick
+      if (LAST && (h.j0 == 1 || h.j0 + kFW - 1 >= ny) && lane < 16) {
+        // the run's final y-wall ghost columns: the column-sweep output's
+        // (grid.cpp:44-59), which the row phase left in the slot untouched
+        const int v = lane & 3, cg = lane >> 2;            // cg 0, 1: columns -1, 0; 2, 3: ny+1, ny+2
+        const int jg = cg < 2 ? cg - 1 : ny - 1 + cg;
+        if (cg < 2 ? h.j0 == 1 : h.j0 + kFW - 1 >= ny)
+          dst[cell_index(pitch, v, i, jg)] =
+              *(const double*)(hb_smem + at + v * kFVarBytesS + (uint32_t)(jg - h.j0 + 16) * 8);
+      }
       fence_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -819,7 +837,7 @@ __global__ void __launch_bounds__(256, 1)
     __threadfence();
     const unsigned prev = atomicAdd(a.done, 1u);
     if (prev == gridDim.x - 1) {
-      *a.limit_in = kEmptyLimit;
+      if (!LAST) *a.limit_in = kEmptyLimit;  // (a run's last dt stays readable)
       *a.counter = 0u;
       *a.done = 0u;
       __threadfence();

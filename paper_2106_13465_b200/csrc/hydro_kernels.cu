@@ -1463,6 +1463,7 @@ int HB_SWEEP(query_geometry)(Geometry* g) {
   g->ctas_y_exact = oy1 > 0 ? oy1 : 1;
   int oxy = 0;
   cudaFuncSetAttribute(sweep_xy_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
+  cudaFuncSetAttribute(sweep_xy_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oxy, sweep_xy_kernel<0>, 256, kFSmemBytes);
   g->ctas_xy_per_sm = oxy > 0 ? oxy : 1;
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
@@ -1603,7 +1604,8 @@ void HB_SWEEP(launch_sweep_xy)(const SweepArgs& a0, const CUtensorMap& load, con
   }
   a.seg = (a.seg + 3) / 4 * 4;
   a.nseg = (a.nx + a.seg - 1) / a.seg;
-  launch_sweep_block(sweep_xy_kernel<0>, ctas, 256, kFSmemBytes, s, a, load, store);
+  if (a.last_step) launch_sweep_block(sweep_xy_kernel<1>, ctas, 256, kFSmemBytes, s, a, load, store);
+  else launch_sweep_block(sweep_xy_kernel<0>, ctas, 256, kFSmemBytes, s, a, load, store);
 }
 
 void HB_SWEEP(launch_prologue)(const PrologueArgs& a, cudaStream_t s) {

@@ -127,6 +127,7 @@ struct SweepArgs {
   unsigned long long* skipped;  // cell updates taken by the uniform-window identity (counter)
   double dx2;                 // fused step: the row sweep's spacing (dy)
   unsigned* done;             // fused step: CTAs finished (the last one resets limit_in, counter)
+  int last_step;              // fused step: the run's last -- leaves the final ghost bands behind
 };
 
 // All maps view a tiled buffer as dims {column in block, column block, row in
