@@ -1,6 +1,6 @@
 """profiles/traffic.json from ncu --set full captures: DRAM bytes (read +
 write) per cell of each sweep, keyed like bench.py looks them up
-(<workload>_<flux>_<math>_sweep_<x|y>_dram_bytes_per_cell).
+(<workload>_<flux>_<math>_sweep_<x|y|xy>_dram_bytes_per_cell; xy = the fused step).
     python tools/traffic_json.py cfg3_hllc_tolerance=rep1 cfg3_hllc_bitwise=rep2 ..."""
 import json
 import os
@@ -19,7 +19,7 @@ for arg in sys.argv[1:]:
     for k in kernel_metrics(rep, cells):
         if "sweep" not in k["kernel"] or "dram_bytes" not in k:
             continue
-        which = "x" if "sweep_x" in k["kernel"] else "y"
+        which = "xy" if "sweep_xy" in k["kernel"] else ("x" if "sweep_x" in k["kernel"] else "y")
         out[f"{key}_sweep_{which}_dram_bytes_per_cell"] = round(k["dram_bytes"] / cells, 3)
 json.dump(out, open("profiles/traffic.json", "w"), indent=1)
 print(json.dumps(out, indent=1))
