@@ -611,8 +611,8 @@ def measure_line(env, workload, flux, math, steps, warmup, *, e2e=True, clocks=N
                          "launches": {"sweep_xy": kt["n_xy"], "sweep_x": kt["n_x"],
                                       "sweep_y": kt["n_y"], "other": kt["n_other"]},
                          "note": "event-instrumented pass of the same K bench steps"},
-           "schedule": {"ran": ("fused: one sweep_xy launch per time step between a split first "
-                                "(odd step counts) and last step" if kt["n_xy"] else
+           "schedule": {"ran": ("fused: one sweep_xy launch per time step (after one split step "
+                                "when the step count is odd)" if kt["n_xy"] else
                                 "split: sweep_x + sweep_y per time step"),
                         "how": "auto (hydro_gpu_set_schedule default): fused where the share of "
                                "uniform-window updates of the context's last completed runs is >= "

@@ -403,6 +403,7 @@ struct FusedCol {
   uint32_t memo_at;
   bool memo_valid;
   bool cross;  // steady uniform run: every active lane of the warp holds the same state
+  bool counted;  // an output strip of the band (the halo strips' updates are not counted)
 
   // column orientation: mom_a = mom_x (var 1), mom_b = mom_y (var 2)
   __device__ __forceinline__ static Cons get(uint32_t at) {
@@ -478,7 +479,7 @@ struct FusedCol {
       sink(c + k, o);
       out_at += kFRowBytesS;
     }
-    if (active) nskip += 4;
+    if (counted) nskip += 4;
     const bool last_chunk = out_rest == 0;
     out_at = chunk(q++, last_chunk, cross, o.un) + lane_off;
     out_left = out_rest < 4 ? out_rest : 4;
@@ -486,7 +487,7 @@ struct FusedCol {
   }
   __device__ __forceinline__ Cons reload(int) const { return get(at3); }
   __device__ __forceinline__ Cons prev() const { return before; }
-  __device__ __forceinline__ void count_skip() { ++nskip; }
+  __device__ __forceinline__ void count_skip() { nskip += counted ? 1u : 0u; }
   // after iteration c: cell c-1 was updated (c > ka); a completed 4-row
   // output chunk (or the item's last) is handed over
   __device__ __forceinline__ void boundary(int c) {
@@ -620,6 +621,7 @@ __global__ void __launch_bounds__(256, 1)
         col.bars = bars;
         col.ka = ka;
         col.active = active;
+        col.counted = active && s >= 2 && s < kFW + 2;
         col.begin(q0);
         col.lane_off = (uint32_t)(s + 14) * 8;
         col.out_at = slots0 + (m % kFNS) * kFSlotBytes + col.lane_off;
