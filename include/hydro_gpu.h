@@ -240,6 +240,17 @@ int hydro_gpu_slab_inbox_in(hydro_gpu_ctx* ctx, int step);
 /* Writes the reference's end-of-run ghost state (mirrors of the last
  * column-sweep output, grid.cpp:23-60 as applied before the last row sweep). */
 int hydro_gpu_slab_finish(hydro_gpu_ctx* ctx);
+/* The fused schedule for a caller that drives the slab's steps itself
+ * (hydro_gpu_group): run_begin remakes the AUTO choice, counts the run and
+ * says whether it takes fused steps; step_xy is one fused step (phase 0:
+ * U_a -> U_b, 1: U_b -> U_a; first = the run's first fused step, last = the
+ * run's last step, halo != 0: the inbox of parity step&1 is first copied into
+ * the ghost rows of the step's input buffer); run_end enqueues
+ * hydro_gpu_slab_finish's work unless the last step was fused, and the
+ * counters the next AUTO choice reads. */
+int hydro_gpu_slab_run_begin(hydro_gpu_ctx* ctx, int steps, int* fused);
+int hydro_gpu_slab_step_xy(hydro_gpu_ctx* ctx, int step, int phase, int first, int last, int halo);
+int hydro_gpu_slab_run_end(hydro_gpu_ctx* ctx, int fused_last);
 
 /* ---- multi-rank slabs driven from C++ (one process per GPU) ------------ */
 /* An NCCL unique id (128 bytes) made on one rank and shared with the others

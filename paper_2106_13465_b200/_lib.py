@@ -85,6 +85,9 @@ def lib() -> C.CDLL:
         "hydro_gpu_slab_halo_out": ([_ctx, i], i),
         "hydro_gpu_slab_inbox_in": ([_ctx, i], i),
         "hydro_gpu_slab_finish": ([_ctx], i),
+        "hydro_gpu_slab_run_begin": ([_ctx, i, P(C.c_int)], i),
+        "hydro_gpu_slab_step_xy": ([_ctx, i, i, i, i, i], i),
+        "hydro_gpu_slab_run_end": ([_ctx, i], i),
         "hydro_gpu_decode_error": ([_ctx, u64, P(ErrorInfo)], i),
         "hydro_gpu_set_timing": ([_ctx, i], i),
         "hydro_gpu_kernel_times": ([_ctx, _dp, _dp, _dp, P(C.c_longlong), P(C.c_longlong),

@@ -294,7 +294,11 @@ void enqueue_xy(hydro_gpu_ctx* c, int step, bool a_to_b, bool last) {
   a.counter = reinterpret_cast<unsigned*>(c->slots + kSlotFused);
   a.done = a.counter + 1;
   a.counter_next = nullptr;
-  a.halo_up = a.halo_dn = nullptr;
+  {  // rows produced by this step feed the neighbours' column phase of step+1: inbox parity (step+1)&1
+    const size_t blk = 8 * c->pitch, par = (size_t)((step + 1) & 1);
+    a.halo_up = c->peer_up ? c->peer_up + (par * 2 + 1) * blk : nullptr;
+    a.halo_dn = c->peer_dn ? c->peer_dn + (par * 2 + 0) * blk : nullptr;
+  }
   const CUtensorMap& ld = a_to_b ? c->maps.fa_load : c->maps.fb_load;
   const CUtensorMap& st = a_to_b ? c->maps.fb_store : c->maps.fa_store;
   cudaEvent_t e0{};
@@ -325,13 +329,13 @@ void auto_choose(hydro_gpu_ctx* c) {
   c->stat_sweeps = 0;
 }
 
-// Whether a run of this context can take fused steps: the whole domain on
-// one device (slabs exchange halos between the sweeps), HLLC.
+// Whether a run of this context takes fused steps (HLLC; whole domains and
+// row slabs alike: a slab's fused step stores its halo rows into the
+// neighbours' inboxes like the split row sweep).
 bool fused_ok(const hydro_gpu_ctx* c) {
   const bool want = c->schedule == HYDRO_GPU_SCHEDULE_FUSED ||
                     (c->schedule == HYDRO_GPU_SCHEDULE_AUTO && c->auto_fused);
-  return want && c->comm == nullptr && !c->peer_up &&
-         !c->peer_dn && c->cfg.wall_lo && c->cfg.wall_hi && c->cfg.flux == HYDRO_GPU_FLUX_HLLC;
+  return want && c->cfg.flux == HYDRO_GPU_FLUX_HLLC;
 }
 
 // wall_bc: x-wall ghost rows; full_bc: also the y-wall columns;
@@ -488,8 +492,8 @@ const NcclApi& nccl() {
 void rows_to_block(hydro_gpu_ctx* c, int i0, double* blk) {
   hb::launch_tiles_to_rows(c->A, c->pitch, blk, 0, -1, i0, 2, c->cfg.ny, c->stream);
 }
-void block_to_rows(hydro_gpu_ctx* c, const double* blk, int i0) {
-  hb::launch_rows_to_tiles(blk, 0, c->A, c->pitch, -1, i0, 2, c->cfg.ny, c->stream);
+void block_to_rows(hydro_gpu_ctx* c, const double* blk, int i0, double* state = nullptr) {
+  hb::launch_rows_to_tiles(blk, 0, state ? state : c->A, c->pitch, -1, i0, 2, c->cfg.ny, c->stream);
 }
 
 // The slab's per-step exchange (compute_dt_parallel's min, schedulers.cpp:47-65,
@@ -497,15 +501,16 @@ void block_to_rows(hydro_gpu_ctx* c, const double* blk, int i0) {
 // dt limit min-allreduced over the ranks (u64 min: positive doubles order like
 // their bits; the allreduce also orders every neighbour's peer-memory halo
 // stores of the previous row sweep before this rank reads them), then the
-// inbox copied into the ghost rows.
-int enqueue_exchange(hydro_gpu_ctx* c, int step) {
+// inbox copied into the ghost rows of `state` (the buffer holding the step's
+// input: U_a, or U_b before every second fused step).
+int enqueue_exchange(hydro_gpu_ctx* c, int step, double* state) {
   cudaEvent_t e0{};
   ev_begin(c, &e0);
   unsigned long long* lim = c->slots + (step & 1);
   NCCL_TRY(c, nccl().all_reduce(lim, lim, 1, ncclUint64, ncclMin, c->comm, c->stream));
   const size_t blk = 8 * c->pitch, par = (size_t)(step & 1);
-  if (!c->cfg.wall_lo) block_to_rows(c, c->inbox + (par * 2 + 0) * blk, -1);
-  if (!c->cfg.wall_hi) block_to_rows(c, c->inbox + (par * 2 + 1) * blk, c->cfg.nx + 1);
+  if (!c->cfg.wall_lo) block_to_rows(c, c->inbox + (par * 2 + 0) * blk, -1, state);
+  if (!c->cfg.wall_hi) block_to_rows(c, c->inbox + (par * 2 + 1) * blk, c->cfg.nx + 1, state);
   CUDA_TRY(c, cudaGetLastError());
   ev_end(c, e0, 3);
   return HYDRO_GPU_OK;
@@ -536,14 +541,19 @@ int enqueue_run(hydro_gpu_ctx* c, int steps) {
   }
   for (int s = 0; s < steps; ++s) {
     if (s >= f0 && s < f1) {
+      const bool a_to_b = ((s - f0) & 1) == 0;
+      if (slab) {
+        rc = enqueue_exchange(c, s, a_to_b ? c->A : c->B);
+        if (rc) return rc;
+      }
       if (s == f0)  // the dt slot the first fused step writes (a split step leaves it set)
         CUDA_TRY(c, cudaMemsetAsync(c->slots + ((s + 1) & 1), 0xff, sizeof(unsigned long long),
                                     c->stream));
-      enqueue_xy(c, s, ((s - f0) & 1) == 0, s + 1 == steps);
+      enqueue_xy(c, s, a_to_b, s + 1 == steps);
       continue;
     }
     if (slab) {
-      rc = enqueue_exchange(c, s);
+      rc = enqueue_exchange(c, s, c->A);
       if (rc) return rc;
     }
     enqueue_x(c, s, 0, 0.0);
@@ -1304,6 +1314,52 @@ int hydro_gpu_slab_sweep_y(hydro_gpu_ctx* c, int step) {
   if (!c) return HYDRO_GPU_ERR_CONFIG;
   DeviceGuard g(c->device);
   enqueue_y(c, step, 0, 0.0, 1);
+  CUDA_TRY(c, cudaGetLastError());
+  return HYDRO_GPU_OK;
+}
+
+// Run bookkeeping of a caller that drives the slab's steps itself
+// (hydro_gpu_group): remakes the AUTO schedule's choice, counts the run's
+// sweeps and says whether the run takes fused steps.
+int hydro_gpu_slab_run_begin(hydro_gpu_ctx* c, int steps, int* fused) {
+  if (!c || !fused) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  auto_choose(c);
+  c->stat_sweeps += 2.0 * steps * (double)c->cfg.nx * (double)c->cfg.ny;
+  *fused = fused_ok(c) ? 1 : 0;
+  return HYDRO_GPU_OK;
+}
+
+// One fused step of a slab whose steps are driven from outside: the inbox
+// copied into the ghost rows of the step's input buffer (halo != 0), then the
+// step.  phase 0: U_a -> U_b, 1: U_b -> U_a; first: the run's first fused
+// step; last: the run's last step.
+int hydro_gpu_slab_step_xy(hydro_gpu_ctx* c, int step, int phase, int first, int last, int halo) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  double* state = phase == 0 ? c->A : c->B;
+  if (halo) {
+    const size_t blk = 8 * c->pitch, par = (size_t)(step & 1);
+    if (!c->cfg.wall_lo) block_to_rows(c, c->inbox + (par * 2 + 0) * blk, -1, state);
+    if (!c->cfg.wall_hi) block_to_rows(c, c->inbox + (par * 2 + 1) * blk, c->cfg.nx + 1, state);
+  }
+  if (first)
+    CUDA_TRY(c, cudaMemsetAsync(c->slots + ((step + 1) & 1), 0xff, sizeof(unsigned long long),
+                                c->stream));
+  enqueue_xy(c, step, phase == 0, last != 0);
+  CUDA_TRY(c, cudaGetLastError());
+  return HYDRO_GPU_OK;
+}
+
+// End of such a run: the final ghost bands after a split last step, and the
+// uniform-window counters for the AUTO schedule's next choice.
+int hydro_gpu_slab_run_end(hydro_gpu_ctx* c, int fused_last) {
+  if (!c) return HYDRO_GPU_ERR_CONFIG;
+  DeviceGuard g(c->device);
+  if (!fused_last) enqueue_finish(c);
+  if (c->stat_host)
+    CUDA_TRY(c, cudaMemcpyAsync(c->stat_host, c->slots + kSlotSkipped, 2 * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaGetLastError());
   return HYDRO_GPU_OK;
 }

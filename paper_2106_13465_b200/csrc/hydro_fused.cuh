@@ -45,9 +45,14 @@
 // inputs and the y-wall ghost columns from the slot (finish_kernel's job in
 // the split schedule).
 //
+// Row slabs (PEER): the rows a neighbour's next column sweep needs are also
+// stored into its inbox (peer memory), like the split row sweep does; the
+// per-step exchange copies the own inbox into the ghost rows of whichever
+// buffer holds the state.
+//
 // Not fused: one leading step of a run with an odd step count (the state
-// ping-pongs between the two buffers and must end in the first), slabs
-// (multi-GPU halo), the exact-10 flux.
+// ping-pongs between the two buffers and must end in the first), the
+// exact-10 flux.
 
 // ---- layout -------------------------------------------------------------------
 constexpr int kFStrips = kFW + 4;                 // column-phase strips j0-2 .. j0+121
@@ -503,7 +508,7 @@ struct FusedCol {
   }
 };
 
-template <int LAST>
+template <int LAST, bool PEER>
 __global__ void __launch_bounds__(256, 1)
     sweep_xy_kernel(SweepArgs a, const __grid_constant__ CUtensorMap load_map,
                     const __grid_constant__ CUtensorMap store_map) {
@@ -685,6 +690,7 @@ __global__ void __launch_bounds__(256, 1)
     const size_t pitch = a.pitch;
     RowMemo memo{};
     memo.valid = false;
+    bool wrote_peer = false;
     RowAcc acc, done;
     acc.clear();
     done.clear();
@@ -725,11 +731,14 @@ __global__ void __launch_bounds__(256, 1)
       const int gi = a.row0 + i;
       const uint32_t at = slots0 + sl * kFSlotBytes + wr * kFRowBytesS;
       const bool lo = a.wall_lo && i <= 2, hi = a.wall_hi && i >= nx - 1;
+      // slab borders: the rows the neighbours' next column sweep needs go into
+      // their inboxes over NVLink (InterfaceBuffer, decomposition.hpp:58-79)
+      const bool up = PEER && a.halo_up && i <= 2, dn = PEER && a.halo_dn && i >= nx - 1;
       // a chunk every column warp published as uniform, all in one state this
       // warp has already evaluated to the identity in this launch: the row
       // keeps its input (fused_row would find exactly this by reading it)
       bool quick = false;
-      if (memo.valid && !(lo || hi)) {
+      if (memo.valid && !(lo || hi || up || dn)) {
         const FusedUni& fu = unis[sl];
         const int4 uf = *(const int4*)fu.uni;
         if (uf.x & uf.y & uf.z & uf.w) {
@@ -787,6 +796,24 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
       }
+      if constexpr (PEER) {
+        if (up || dn) {
+          auto put_peer = [&](double* q, const Cons& u) {  // row orientation: mom_b is mom_x
+            q[0] = u.r;
+            q[2 * pitch] = u.ma;
+            q[pitch] = u.mb;
+            q[3 * pitch] = u.e;
+          };
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (!outk[k]) continue;
+            const int jj = rg.jb + k;
+            if (up) put_peer(a.halo_up + (size_t)(i - 1) * 4 * pitch + (jj + kColOff), out[k]);
+            if (dn) put_peer(a.halo_dn + (size_t)(i - (nx - 1)) * 4 * pitch + (jj + kColOff), out[k]);
+          }
+          wrote_peer = true;
+        }
+      }
       }  // !quick
       if (LAST && (h.j0 == 1 || h.j0 + kFW - 1 >= ny) && lane < 16) {
         // the run's final y-wall ghost columns: the column-sweep output's
@@ -811,6 +838,9 @@ __global__ void __launch_bounds__(256, 1)
       redo_wait = false;
     }
     if (cur >= 0) done.add(acc);
+    // peer stores performed system-wide before this kernel completes (the
+    // neighbour reads them after the dt exchange that follows on the stream)
+    if (PEER && wrote_peer) __threadfence_system();
     if (done.ekey != kNoError) record(a.err, done.ekey);
     spd_max = done.spd;
     dt_key = done.dtkey;

@@ -82,8 +82,10 @@ struct hydro_gpu_group {
   std::vector<cudaStream_t> stream;
   std::vector<cudaEvent_t> done;
   cudaEvent_t lead = nullptr;  // the leader's dt-min of the step is done
-  // captured runs, one per step count (bounded cache)
+  // captured runs, one per (step count, schedule) (bounded cache; the key is
+  // 2 * steps + fused)
   std::vector<std::pair<int, cudaGraphExec_t>> graphs;
+  bool fused = false;  // the current run takes fused steps (every slab agrees)
   bool use_graphs = true;
   int math = HYDRO_GPU_MATH_BITWISE;
   hydro_gpu_error last{};
@@ -171,18 +173,25 @@ int enqueue_group_run(hydro_gpu_group* g, int steps) {
     if (!rc && halo) rc = hydro_gpu_slab_halo_out(g->ctx[k], 0);
     if (rc) return slab_rc(g, k, rc);
   }
+  // fused schedule (hydro_fused.cuh): pairs of fused steps after one split
+  // step when the count is odd, like hydro_gpu_run
+  const int f0 = g->fused && steps >= 2 ? steps % 2 : steps;
   for (int s = 0; s < steps; ++s) {
     int rc = enqueue_limit_min(g, s);
     if (rc) return rc;
     for (int k = 0; k < g->n; ++k) {
-      if (halo) rc = hydro_gpu_slab_inbox_in(g->ctx[k], s);
-      if (!rc) rc = hydro_gpu_slab_sweep_x(g->ctx[k], s);
-      if (!rc) rc = hydro_gpu_slab_sweep_y(g->ctx[k], s);
+      if (s >= f0) {
+        rc = hydro_gpu_slab_step_xy(g->ctx[k], s, (s - f0) & 1, s == f0, s + 1 == steps, halo);
+      } else {
+        if (halo) rc = hydro_gpu_slab_inbox_in(g->ctx[k], s);
+        if (!rc) rc = hydro_gpu_slab_sweep_x(g->ctx[k], s);
+        if (!rc) rc = hydro_gpu_slab_sweep_y(g->ctx[k], s);
+      }
       if (rc) return slab_rc(g, k, rc);
     }
   }
   for (int k = 0; k < g->n; ++k) {
-    const int rc = hydro_gpu_slab_finish(g->ctx[k]);
+    const int rc = hydro_gpu_slab_run_end(g->ctx[k], f0 < steps);
     if (rc) return slab_rc(g, k, rc);
   }
   return HYDRO_GPU_OK;
@@ -195,8 +204,9 @@ bool launch_group_graph(hydro_gpu_group* g, int steps) {
   if (!g->use_graphs) return false;
   Guard d0(g->device[0]);
   cudaGraphExec_t exec = nullptr;
+  const int key = 2 * steps + (g->fused ? 1 : 0);
   for (auto& e : g->graphs)
-    if (e.first == steps) exec = e.second;
+    if (e.first == key) exec = e.second;
   if (!exec) {
     if (cudaStreamBeginCapture(g->stream[0], cudaStreamCaptureModeRelaxed) != cudaSuccess) {
       cudaGetLastError();
@@ -230,7 +240,7 @@ bool launch_group_graph(hydro_gpu_group* g, int steps) {
       cudaGraphExecDestroy(g->graphs.front().second);
       g->graphs.erase(g->graphs.begin());
     }
-    g->graphs.push_back({steps, exec});
+    g->graphs.push_back({key, exec});
   }
   if (cudaGraphLaunch(exec, g->stream[0]) != cudaSuccess) {
     cudaGetLastError();
@@ -429,6 +439,13 @@ int hydro_gpu_group_run(hydro_gpu_group* g, int steps, double* last_dt) {
   if (!g || steps < 0 || steps > HYDRO_GPU_MAX_STEPS) return HYDRO_GPU_ERR_CONFIG;
   if (steps == 0) return HYDRO_GPU_OK;
   Guard d0(g->device[0]);
+  g->fused = true;  // fused steps if every slab's schedule takes them
+  for (int k = 0; k < g->n; ++k) {
+    int f = 0;
+    const int rc = hydro_gpu_slab_run_begin(g->ctx[k], steps, &f);
+    if (rc) return slab_rc(g, k, rc);
+    g->fused = g->fused && f != 0;
+  }
   if (!(steps >= 2 && launch_group_graph(g, steps))) {
     const int rc = enqueue_group_run(g, steps);
     if (rc) return rc;

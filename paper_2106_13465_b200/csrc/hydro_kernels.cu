@@ -1462,9 +1462,11 @@ int HB_SWEEP(query_geometry)(Geometry* g) {
   g->ctas_x_exact = ox1 > 0 ? ox1 : 1;
   g->ctas_y_exact = oy1 > 0 ? oy1 : 1;
   int oxy = 0;
-  cudaFuncSetAttribute(sweep_xy_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
-  cudaFuncSetAttribute(sweep_xy_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oxy, sweep_xy_kernel<0>, 256, kFSmemBytes);
+  cudaFuncSetAttribute(sweep_xy_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
+  cudaFuncSetAttribute(sweep_xy_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
+  cudaFuncSetAttribute(sweep_xy_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
+  cudaFuncSetAttribute(sweep_xy_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oxy, sweep_xy_kernel<0, false>, 256, kFSmemBytes);
   g->ctas_xy_per_sm = oxy > 0 ? oxy : 1;
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
@@ -1604,8 +1606,14 @@ void HB_SWEEP(launch_sweep_xy)(const SweepArgs& a0, const CUtensorMap& load, con
   }
   a.seg = (a.seg + 3) / 4 * 4;
   a.nseg = (a.nx + a.seg - 1) / a.seg;
-  if (a.last_step) launch_sweep_block(sweep_xy_kernel<1>, ctas, 256, kFSmemBytes, s, a, load, store);
-  else launch_sweep_block(sweep_xy_kernel<0>, ctas, 256, kFSmemBytes, s, a, load, store);
+  const bool peer = a.halo_up || a.halo_dn;
+  if (a.last_step) {
+    if (peer) launch_sweep_block(sweep_xy_kernel<1, true>, ctas, 256, kFSmemBytes, s, a, load, store);
+    else launch_sweep_block(sweep_xy_kernel<1, false>, ctas, 256, kFSmemBytes, s, a, load, store);
+  } else {
+    if (peer) launch_sweep_block(sweep_xy_kernel<0, true>, ctas, 256, kFSmemBytes, s, a, load, store);
+    else launch_sweep_block(sweep_xy_kernel<0, false>, ctas, 256, kFSmemBytes, s, a, load, store);
+  }
 }
 
 void HB_SWEEP(launch_prologue)(const PrologueArgs& a, cudaStream_t s) {

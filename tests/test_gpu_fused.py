@@ -138,3 +138,33 @@ def test_auto_schedule_follows_the_uniform_window_share(gpu, case, seed, want_fu
         g.run(17)
         g.download(ref.planes)
     assert np.array_equal(grid.planes.view(np.uint64), ref.planes.view(np.uint64))
+
+
+@pytest.mark.parametrize("n,case,bc,nx", [(2, "sod_x", "transmit", 77), (3, "random", "reflect", 77),
+                                          (8, "corner_blast", "reflect", 77), (5, "random", "transmit", 11),
+                                          (4, "corner_blast", "reflect", 300)])
+@pytest.mark.parametrize("schedule", ["fused", "split"])
+def test_group_slabs_take_fused_steps(gpu, monkeypatch, n, case, bc, nx, schedule):
+    """Row slabs on the fused schedule (hydro_gpu_group, all slabs on cuda:0):
+    the fused step's row phase stores the halo rows into the neighbours'
+    inboxes and the exchange fills the ghost rows of whichever buffer holds the
+    state.  Odd and even step counts, two calls; every plane and ghost and the
+    last dt equal one context on the whole grid, in either schedule."""
+    ny = 130
+    one = P.make_case(case, nx, ny, MODEL, seed=19)
+    grp = one.copy()
+    dt_one = None
+    with P.GpuGrid(nx, ny, one.dx, one.dy, MODEL, bc, device=0) as g:
+        g.set_schedule("split")
+        g.upload(one.planes)
+        g.run(13)
+        dt_one = g.run(18)
+        g.download(one.planes)
+    monkeypatch.setenv("HYDRO_GPU_SCHEDULE", schedule)
+    with P.GpuGroup(nx, ny, grp.dx, grp.dy, MODEL, bc, devices=[0] * n) as g:
+        g.upload(grp.planes)
+        g.run(13)
+        dt_grp = g.run(18)
+        g.download(grp.planes)
+    assert dt_grp == dt_one
+    assert np.array_equal(grp.planes.view(np.uint64), one.planes.view(np.uint64))

@@ -99,7 +99,8 @@ def test_native_slab_exchange_is_timed(nccl_world):
     sl.grid.run(8)
     ms, cnt = sl.grid.comm_times()
     kt = sl.grid.kernel_times()
+    _, n_xy = sl.grid.fused_times()
     sl.grid.set_timing(False)
-    assert cnt == 8 and ms > 0.0
-    assert kt["n_x"] == 8 and kt["n_y"] == 8
+    assert cnt == 8 and ms > 0.0  # one exchange per step in either schedule
+    assert n_xy == 8 or (kt["n_x"] == 8 and kt["n_y"] == 8)
     sl.grid.close()
