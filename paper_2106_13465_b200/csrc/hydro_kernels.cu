@@ -1596,11 +1596,12 @@ void HB_SWEEP(launch_sweep_xy)(const SweepArgs& a0, const CUtensorMap& load, con
   SweepArgs a = a0;
   const int ctas = geo.sms * geo.ctas_xy_per_sm;
   const int nbands = (a.ny + kFW - 1) / kFW;
-  // rows per work item: about 8 items per CTA (dynamic balance), 4-row
-  // chunks, 16..256 rows
+  // rows per work item: about 4 items per CTA (dynamic balance against the 6
+  // halo rows and the ring fill every item pays: config 1 -16% vs 8 items),
+  // 4-row chunks, 32..256 rows
   if (a.seg <= 0) {
-    long long seg = (long long)a.nx * nbands / ((long long)ctas * 8);
-    if (seg < 16) seg = 16;
+    long long seg = (long long)a.nx * nbands / ((long long)ctas * 4);
+    if (seg < 32) seg = 32;
     if (seg > 256) seg = 256;
     a.seg = (int)seg;
   }
