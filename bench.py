@@ -614,9 +614,10 @@ def measure_line(env, workload, flux, math, steps, warmup, *, e2e=True, clocks=N
            "schedule": {"ran": ("fused: one sweep_xy launch per time step (after one split step "
                                 "when the step count is odd)" if kt["n_xy"] else
                                 "split: sweep_x + sweep_y per time step"),
-                        "how": "auto (hydro_gpu_set_schedule default): fused where the share of "
-                               "uniform-window updates of the context's last completed runs is >= "
-                               "0.6, else split; bitwise the same results",
+                        "how": "auto (hydro_gpu_set_schedule default): chosen from the context's "
+                               "own completed (warm-up) runs -- the uniform-window share (fused "
+                               ">= 0.6) and the event-timed step time of each schedule; bitwise "
+                               "the same results",
                         "uniform_share_behind_choice": kt["auto_share"]},
            "gpu_launches": kt["n_xy"] + kt["n_x"] + kt["n_y"] + kt["n_other"] + steps,  # + init kernels
            "clocks": clock_info}

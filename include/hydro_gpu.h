@@ -79,12 +79,14 @@ enum hydro_gpu_flux { HYDRO_GPU_FLUX_HLLC = 0, HYDRO_GPU_FLUX_EXACT10 = 1 };
 enum hydro_gpu_math { HYDRO_GPU_MATH_BITWISE = 0, HYDRO_GPU_MATH_TOLERANCE = 1 };
 /* Step schedule (hydro_gpu_set_schedule): SPLIT = a column-sweep and a
  * row-sweep launch per step; FUSED = one launch per step doing both sweeps
- * (the column sweep's output stays in shared memory), used on a whole
- * single-device HLLC domain for every step of a run (after one split step
- * when the step count is odd) -- bitwise the same results.  AUTO (the default) picks between them per run from the
- * share of cell updates the context's last completed runs took by the
- * uniform-window identity (fused above 0.6: memory-bound flow; split below:
- * dense flow); a context's first run is fused. */
+ * (the column sweep's output stays in shared memory), used with the HLLC
+ * flux for every step of a run (after one split step when the step count is
+ * odd), on whole domains and row slabs -- bitwise the same results.  AUTO
+ * (the default) picks between them per run from the context's own completed
+ * runs: the share of cell updates taken by the
+ * uniform-window identity (fused above 0.6: memory-bound flow) and the
+ * event-timed device time per step of each schedule (an untimed schedule is
+ * tried once unless the share is decisive); a context's first run is fused. */
 enum hydro_gpu_schedule {
   HYDRO_GPU_SCHEDULE_SPLIT = 0,
   HYDRO_GPU_SCHEDULE_FUSED = 1,

@@ -64,6 +64,14 @@ struct hydro_gpu_ctx {
   unsigned long long stat_seen = 0;            // their sum when the choice was last made
   double stat_sweeps = 0;                      // cell-sweeps enqueued since then
   double stat_share = -1.0;                    // the share behind the current choice
+  // ... and the device time per step of the last event-bracketed run of each
+  // schedule ([0] split, [1] fused; -1 = not measured at the current share)
+  cudaEvent_t run_ev[2] = {nullptr, nullptr};
+  bool run_pending = false;                    // run_ev bracket a run not yet read
+  int run_steps = 0;
+  bool run_fused = false;
+  double ms_step[2] = {-1.0, -1.0};
+  double ms_share[2] = {-1.0, -1.0};
   // CUDA graphs of whole run_sequential calls, one per (steps, timing):
   // the 2*steps+3 launches replay without per-launch CPU and queue gaps.
   struct GraphEntry {
@@ -309,24 +317,80 @@ void enqueue_xy(hydro_gpu_ctx* c, int step, bool a_to_b, bool last) {
 }
 
 // The AUTO schedule's choice, remade whenever the stream is idle and a run has
-// completed since the last one: fused steps stream the state once per step
-// but run 8 warps per SM, split sweeps stream it twice with 16 -- fused wins
-// where most updates are uniform-window identities (memory-bound flow), split
-// on dense flow (latency-bound FP64 chains).  The results are bitwise the
-// same either way; the first run of a context is fused.
+// completed since the last one.  Fused steps stream the state once per step
+// but run 8 warps per SM and redo a whole 120-column item when a fast pass
+// leaves its range; split sweeps stream it twice with 16 warps and redo
+// 32-strip items.  So fused wins on memory-bound flow (most updates
+// uniform-window identities), split on dense flow and where a strong front
+// keeps forcing redo passes on a small grid.  Two inputs, both from the
+// context's own completed runs: the share of uniform-window updates (the
+// sweeps' counters) and the event-timed device time per step of each
+// schedule.  Untimed schedules are tried once unless the share is decisive
+// (>= 0.98: fused, <= 0.2: split); a timing is forgotten when the share has
+// moved by more than 0.1 since.  The results are bitwise the same either way;
+// the first run of a context is fused.
 constexpr double kAutoFusedShare = 0.6;
 void auto_choose(hydro_gpu_ctx* c) {
-  if (c->schedule != HYDRO_GPU_SCHEDULE_AUTO || c->stat_sweeps <= 0 || !c->stat_host) return;
+  if (c->schedule != HYDRO_GPU_SCHEDULE_AUTO || !c->stat_host) return;
+  if (c->stat_sweeps <= 0 && !c->run_pending) return;
   if (cudaStreamQuery(c->stream) != cudaSuccess) {
     cudaGetLastError();  // runs still in flight: keep the choice
     return;
   }
-  const unsigned long long cur = c->stat_host[0] + c->stat_host[1];
-  const unsigned long long seen = cur >= c->stat_seen ? c->stat_seen : 0;
-  c->stat_share = (double)(cur - seen) / c->stat_sweeps;
-  c->auto_fused = c->stat_share >= kAutoFusedShare;
-  c->stat_seen = cur;
-  c->stat_sweeps = 0;
+  if (c->stat_sweeps > 0) {
+    const unsigned long long cur = c->stat_host[0] + c->stat_host[1];
+    const unsigned long long seen = cur >= c->stat_seen ? c->stat_seen : 0;
+    c->stat_share = (double)(cur - seen) / c->stat_sweeps;
+    c->stat_seen = cur;
+    c->stat_sweeps = 0;
+  }
+  const double share = c->stat_share;
+  if (c->run_pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->run_ev[0], c->run_ev[1]) == cudaSuccess) {
+      c->ms_step[c->run_fused] = (double)ms / c->run_steps;
+      c->ms_share[c->run_fused] = share;
+    } else {
+      cudaGetLastError();
+    }
+    c->run_pending = false;
+  }
+  for (int k = 0; k < 2; ++k)
+    if (c->ms_step[k] >= 0 && share >= 0 && std::fabs(share - c->ms_share[k]) > 0.1) c->ms_step[k] = -1.0;
+  const bool by_share = share < 0 || share >= kAutoFusedShare;
+  if (c->ms_step[0] >= 0 && c->ms_step[1] >= 0) c->auto_fused = c->ms_step[1] <= c->ms_step[0];
+  else if (c->ms_step[1] >= 0 && share >= 0 && share < 0.98) c->auto_fused = false;  // try split once
+  else if (c->ms_step[0] >= 0 && share > 0.2) c->auto_fused = true;                  // try fused once
+  else c->auto_fused = by_share;
+}
+
+// Event bracket around a run for auto_choose (not around event-instrumented
+// runs, whose graphs carry timing nodes).
+void auto_bracket_begin(hydro_gpu_ctx* c, int steps) {
+  c->run_pending = false;
+  if (c->schedule != HYDRO_GPU_SCHEDULE_AUTO || c->timing || steps < 2 ||
+      c->cfg.flux != HYDRO_GPU_FLUX_HLLC)
+    return;
+  for (int k = 0; k < 2; ++k)
+    if (!c->run_ev[k] && cudaEventCreate(&c->run_ev[k]) != cudaSuccess) {
+      cudaGetLastError();
+      c->run_ev[k] = nullptr;
+      return;
+    }
+  if (cudaEventRecord(c->run_ev[0], c->stream) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  c->run_steps = steps;
+  c->run_fused = steps >= 2 && c->auto_fused;
+  c->run_pending = true;
+}
+void auto_bracket_end(hydro_gpu_ctx* c) {
+  if (!c->run_pending) return;
+  if (cudaEventRecord(c->run_ev[1], c->stream) != cudaSuccess) {
+    cudaGetLastError();
+    c->run_pending = false;
+  }
 }
 
 // Whether a run of this context takes fused steps (HLLC; whole domains and
@@ -731,6 +795,8 @@ int hydro_gpu_destroy(hydro_gpu_ctx* ctx) {
   if (ctx->B) cudaFree(ctx->B);
   if (ctx->slots) cudaFree(ctx->slots);
   if (ctx->stat_host) cudaFreeHost(ctx->stat_host);
+  for (int k = 0; k < 2; ++k)
+    if (ctx->run_ev[k]) cudaEventDestroy(ctx->run_ev[k]);
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
   if (ctx->inbox) cudaFree(ctx->inbox);
   if (ctx->halo_buf) cudaFree(ctx->halo_buf);
@@ -1046,12 +1112,15 @@ int hydro_gpu_run_async(hydro_gpu_ctx* c, int steps) {
   DeviceGuard g(c->device);
   auto_choose(c);
   c->stat_sweeps += 2.0 * steps * (double)c->cfg.nx * (double)c->cfg.ny;
+  auto_bracket_begin(c, steps);
   if (steps >= 2 && launch_graph(c, steps)) {
+    auto_bracket_end(c);
     CUDA_TRY(c, cudaGetLastError());
     return HYDRO_GPU_OK;
   }
   int rc = enqueue_run(c, steps);
   if (rc) return rc;
+  auto_bracket_end(c);
   CUDA_TRY(c, cudaGetLastError());
   return HYDRO_GPU_OK;
 }
@@ -1420,6 +1489,7 @@ int hydro_gpu_reset_counters(hydro_gpu_ctx* c) {
   if (c->stat_host) c->stat_host[0] = c->stat_host[1] = 0;
   c->stat_seen = 0;
   c->stat_sweeps = 0;
+  c->run_pending = false;
   return HYDRO_GPU_OK;
 }
 
