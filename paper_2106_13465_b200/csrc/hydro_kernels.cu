@@ -2,7 +2,7 @@
 //
 // One step of the reference (proj/src/schedulers.cpp:103-116) is
 //   apply_boundary -> compute_dt -> column sweep -> apply_boundary -> row sweep.
-// Here it is two launches per step:
+// Split schedule: two launches per step --
 //   sweep_x  (Column axis, strips along i): reads U_a, writes U_b, and writes
 //            the j-ghost columns of U_b (the y-wall half of the second
 //            apply_boundary, grid.cpp:44-59) from its own outputs;
@@ -10,23 +10,27 @@
 //            i-ghost rows of U_a for the next step (the x-wall half of
 //            apply_boundary, grid.cpp:26-42), and folds cell_dt_limit of the
 //            new state into the next step's dt (compute_dt, :233-242).
+// Fused schedule: one launch per step (sweep_xy_kernel, hydro_fused.cuh,
+// included below): the same two phases with U_b kept in shared memory.
 // Every thread owns one strip segment and walks it with a register sliding
 // window: primitive conversion, minmod slopes, Hancock predictor, evolved
 // faces, HLLC flux and the conservative update of the reference's four strip
 // loops (euler_kernel.cpp:111-223) are fused; no per-strip scratch touches
 // HBM.  Segments overlap by the 2-cell stencil halo only.
 //
-// Memory paths: both sweeps stage their strips through per-warp rings in
-// shared memory, filled and drained by TMA (cp.async.bulk.tensor, mbarrier
-// completion) and used in place (Tiles below).  The column sweep's warp holds
-// 32 adjacent columns: each chunk is one box of 4 grid rows x 4 variables x
-// 32 columns (256-byte rows).  The row sweep's warp holds 32 adjacent rows:
-// each chunk is one box per variable of 32 rows x 8 columns (64-byte rows,
-// SWIZZLE_64B), i.e. a transposed tile from the walker's point of view; the
-// exact-10 row sweep keeps 4-column chunks.  Warps claim work items (32
-// strips x one segment) dynamically from a per-sweep counter, in bands of
-// strip groups (item_coords), and redo an item with the exact math policy if
-// the fast pass left its proven range.
+// Memory paths: the state is tiled in HBM (32 rows x 8 columns x 4 variables
+// per 8 KB block, cell_index in hydro_kernels.cuh); both sweeps stage their
+// strips through per-warp rings in shared memory, filled and drained by TMA
+// (cp.async.bulk.tensor.5d over the tiled view, mbarrier completion) and used
+// in place (Tiles below).  The column sweep's warp holds 32 adjacent columns:
+// each chunk is one box of 4 grid rows x 4 variables x 4 column blocks
+// (sixteen 256-byte pieces).  The row sweep's warp holds 32 adjacent rows:
+// each chunk is one box of 32 rows x 8 (bitwise HLLC, SWIZZLE_64B) or 4
+// (tolerance HLLC and exact-10, SWIZZLE_32B) columns x 4 variables, i.e. a
+// contiguous piece of a block and a transposed tile from the walker's point
+// of view.  Warps claim work items (32 strips x one segment) dynamically from
+// a per-sweep counter, in bands of strip groups (item_coords), and redo an
+// item with the exact math policy if the fast pass left its proven range.
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
