@@ -364,13 +364,13 @@ void auto_choose(hydro_gpu_ctx* c) {
   else c->auto_fused = by_share;
 }
 
+bool fused_ok(const hydro_gpu_ctx* c);
+
 // Event bracket around a run for auto_choose (not around event-instrumented
 // runs, whose graphs carry timing nodes).
 void auto_bracket_begin(hydro_gpu_ctx* c, int steps) {
   c->run_pending = false;
-  if (c->schedule != HYDRO_GPU_SCHEDULE_AUTO || c->timing || steps < 2 ||
-      c->cfg.flux != HYDRO_GPU_FLUX_HLLC)
-    return;
+  if (c->schedule != HYDRO_GPU_SCHEDULE_AUTO || c->timing || steps < 2) return;
   for (int k = 0; k < 2; ++k)
     if (!c->run_ev[k] && cudaEventCreate(&c->run_ev[k]) != cudaSuccess) {
       cudaGetLastError();
@@ -382,7 +382,7 @@ void auto_bracket_begin(hydro_gpu_ctx* c, int steps) {
     return;
   }
   c->run_steps = steps;
-  c->run_fused = steps >= 2 && c->auto_fused;
+  c->run_fused = fused_ok(c);
   c->run_pending = true;
 }
 void auto_bracket_end(hydro_gpu_ctx* c) {
@@ -399,7 +399,9 @@ void auto_bracket_end(hydro_gpu_ctx* c) {
 bool fused_ok(const hydro_gpu_ctx* c) {
   const bool want = c->schedule == HYDRO_GPU_SCHEDULE_FUSED ||
                     (c->schedule == HYDRO_GPU_SCHEDULE_AUTO && c->auto_fused);
-  return want && c->cfg.flux == HYDRO_GPU_FLUX_HLLC;
+  // (row slabs with the exact-10 flux stay on the split sweeps)
+  return want && (c->cfg.flux == HYDRO_GPU_FLUX_HLLC ||
+                  (c->comm == nullptr && !c->peer_up && !c->peer_dn && c->cfg.wall_lo && c->cfg.wall_hi));
 }
 
 // wall_bc: x-wall ghost rows; full_bc: also the y-wall columns;

@@ -50,9 +50,12 @@
 // per-step exchange copies the own inbox into the ghost rows of whichever
 // buffer holds the state.
 //
+// Exact-10 flux (FLUX 1): the same kernel with the exact solver at every
+// interface (the column walker with its interface memo, the row phase
+// without); whole domains only (slabs with the exact flux stay split).
+//
 // Not fused: one leading step of a run with an odd step count (the state
-// ping-pongs between the two buffers and must end in the first), the
-// exact-10 flux.
+// ping-pongs between the two buffers and must end in the first).
 
 // ---- layout -------------------------------------------------------------------
 constexpr int kFStrips = kFW + 4;                 // column-phase strips j0-2 .. j0+121
@@ -85,7 +88,9 @@ constexpr uint32_t kFHdrOff = kFBarOff + kFNBA * 8;
 constexpr uint32_t kFFlagOff = kFHdrOff + kFNS * 32;
 constexpr uint32_t kFUniOff = kFFlagOff + 16;       // per slot: FusedUni
 constexpr uint32_t kFUniBytes = 160;
-constexpr int kFSmemBytes = (int)(kFUniOff + kFNS * kFUniBytes) + 128;  // + alignment
+constexpr uint32_t kFMemoOff = kFUniOff + kFNS * kFUniBytes;  // exact-10: the column warps' memos
+constexpr int kFSmemBytes = (int)kFMemoOff + 128;             // + alignment
+constexpr int kFSmemBytesEx = kFSmemBytes + 13 * 1024;
 
 // ---- warp shuffles of the row phase ------------------------------------------
 __device__ __forceinline__ double shfl_up_d(double v) {
@@ -166,7 +171,7 @@ struct RowGeo {
 // face of cell -1 and the flux at the lane's right edge by shuffles.  Results
 // in out[] (outputs only), contributions in acc; returns false if the fast
 // pass left its proven range on an output's stencil.
-template <class M>
+template <class M, int FLUX>
 __device__ __forceinline__ bool row_eval(const Cons (&u)[4], const bool (&outk)[4], int lane,
                                          const RowGeo& rg, const Gas& g, double dtdx, RowAcc& acc,
                                          Cons (&out)[4], bool& ident, double& sp0) {
@@ -185,6 +190,16 @@ __device__ __forceinline__ bool row_eval(const Cons (&u)[4], const bool (&outk)[
   const Prim w4 = shfl_dn(w[0]);   // cell 4 (lane + 1's cell 0)
   Face fl0, frp;
   Flux F1, F2, F3;
+  NoMemo nomemo{};
+  // interface k lies between columns jb+k-1 and jb+k; a Riemann failure
+  // (exact-10: vacuum, exact_riemann.cpp:55-57) counts where the interface
+  // bounds an output cell of the band (strip cell of its left column: jb+k)
+  auto rfail = [&](int k, int f) {
+    const int jl = rg.jb + k - 1, jr = rg.jb + k;
+    if (f >= 0 && ((jr >= rg.j0 && jr <= rg.ohi) || (jl >= rg.j0 && jl <= rg.ohi)))
+      keep_min(acc.ekey, rg.key_base | (1ull << 20) | ((unsigned long long)(rg.jb + k) << 2) | f);
+  };
+  int fr_ = -1;
   {
     Cons el, er;
     predict_evolved(m, wm1, w[0], w[1], half, g, el, er);
@@ -195,28 +210,33 @@ __device__ __forceinline__ bool row_eval(const Cons (&u)[4], const bool (&outk)[
     Cons el, er;
     predict_evolved(m, w[0], w[1], w[2], half, g, el, er);
     const Face fl = face_prim(m, el, w[1], g);
-    F1 = hllc(m, frp, fl, g);
+    F1 = riemann<FLUX>(m, frp, fl, g, fr_, nomemo);
+    rfail(1, fr_);
     frp = face_prim(m, er, w[1], g);
   }
   {
     Cons el, er;
     predict_evolved(m, w[1], w[2], w[3], half, g, el, er);
     const Face fl = face_prim(m, el, w[2], g);
-    F2 = hllc(m, frp, fl, g);
+    F2 = riemann<FLUX>(m, frp, fl, g, fr_, nomemo);
+    rfail(2, fr_);
     frp = face_prim(m, er, w[2], g);
   }
   {
     Cons el, er;
     predict_evolved(m, w[2], w[3], w4, half, g, el, er);
     const Face fl = face_prim(m, el, w[3], g);
-    F3 = hllc(m, frp, fl, g);
+    F3 = riemann<FLUX>(m, frp, fl, g, fr_, nomemo);
+    rfail(3, fr_);
     frp = face_prim(m, er, w[3], g);
   }
   const Face frm1 = shfl_up(frp);  // right face of cell -1
-  const Flux F0 = hllc(m, frm1, fl0, g);
+  const Flux F0 = riemann<FLUX>(m, frm1, fl0, g, fr_, nomemo);
+  rfail(0, fr_);
   const Flux F4 = shfl_dn(F0);     // flux through this lane's right edge
-  // lanes 0 and 31 carry only halo cells: their stencils run off the band
-  if constexpr (M::kFast) m.ok = m.ok | !((lane >= 1) & (lane <= 30));
+  // (lanes 0 and 31 carry only halo cells, but lane 1's first interface and
+  // lane 30's last flux come from them -- clamped copies of valid cells where
+  // their blocks leave the band's halo -- so their range flags count too)
   ident = true;
   sp0 = 0.0;
 #pragma unroll
@@ -250,6 +270,7 @@ __device__ __forceinline__ bool row_eval(const Cons (&u)[4], const bool (&outk)[
 // The row phase of one grid row: slot row at hb_smem offset `at` (U_b of
 // columns j0-2 .. j0+121 at positions 14 .. 137), updated in place.  Row
 // orientation (the row sweep's): mom_a = mom_y (var 2), mom_b = mom_x (var 1).
+template <int FLUX>
 __device__ __forceinline__ void fused_row(uint32_t at, int lane, const RowGeo& rg, int ny,
                                           const Gas& g, double dtdx, RowMemo& memo, RowAcc& acc,
                                           Cons (&u)[4], Cons (&out)[4], bool (&outk)[4]) {
@@ -296,11 +317,11 @@ __device__ __forceinline__ void fused_row(uint32_t at, int lane, const RowGeo& r
   r.clear();
   bool ident;
   double sp0;
-  const bool ok = row_eval<FastMath>(u, outk, lane, rg, g, dtdx, r, out, ident, sp0);
+  const bool ok = row_eval<FastMath, FLUX>(u, outk, lane, rg, g, dtdx, r, out, ident, sp0);
   const bool fast = __all_sync(0xffffffffu, ok);
   if (!fast) {  // an operand left the fast pass's range: the row again, exactly
     r.clear();
-    row_eval<ExactMath>(u, outk, lane, rg, g, dtdx, r, out, ident, sp0);
+    row_eval<ExactMath, FLUX>(u, outk, lane, rg, g, dtdx, r, out, ident, sp0);
   }
   acc.add(r);
   // write the outputs back in place
@@ -508,7 +529,7 @@ struct FusedCol {
   }
 };
 
-template <int LAST, bool PEER>
+template <int LAST, bool PEER, int FLUX>
 __global__ void __launch_bounds__(256, 1)
     sweep_xy_kernel(SweepArgs a, const __grid_constant__ CUtensorMap load_map,
                     const __grid_constant__ CUtensorMap store_map) {
@@ -547,6 +568,7 @@ __global__ void __launch_bounds__(256, 1)
     unsigned m = 0;    // running published-chunk number (slots)
     int seq = 0;       // items taken by this CTA
     int skip_cool = 0;
+    bool memo_keep = false;  // exact-10: this thread's interface memo holds an exact entry
     auto acquire = [&](unsigned mm) {  // slot of chunk mm free (its chunk mm-3 was taken)
       if (mm >= kFNS) bar_sync(kFBarEmpty + (int)(mm % kFNS), 256);
     };
@@ -635,8 +657,8 @@ __global__ void __launch_bounds__(256, 1)
         col.q = 0;
         col.nskip = 0;
         col.skip_cool = skip_cool;
-        col.memo_at = 0;
-        col.memo_valid = false;
+        col.memo_at = pad + kFMemoOff + (uint32_t)tid * 8;  // exact-10 interface memo (13 x 1 KB)
+        col.memo_valid = memo_keep;  // kept across this thread's work items while exact
         auto put_slot = [&](uint32_t at, const Cons& u) {
           double* q = (double*)(hb_smem + at);
           q[0] = u.r;
@@ -663,8 +685,9 @@ __global__ void __launch_bounds__(256, 1)
           }
         };
         ek = kNoError;
-        const bool ok = walk_strip<M, false, 0>(ka, kb, col, sink, g, dtdx, 0.0, base_x, a.row0, ek);
+        const bool ok = walk_strip<M, false, FLUX>(ka, kb, col, sink, g, dtdx, 0.0, base_x, a.row0, ek);
         q0 += (unsigned)nq;
+        memo_keep = col.memo_valid;
         skip_cool = col.skip_cool;
         nskip += col.nskip;
         return ok || !active;
@@ -766,7 +789,7 @@ __global__ void __launch_bounds__(256, 1)
       rg.dt_base = error_key(a.step + 1, 0, gi, 0, 0, 0);
       Cons uin[4], out[4];
       bool outk[4];
-      fused_row(at, lane, rg, ny, g, dtdx, memo, acc, uin, out, outk);
+      fused_row<FLUX>(at, lane, rg, ny, g, dtdx, memo, acc, uin, out, outk);
       // x-wall ghost rows (grid.cpp:26-42): of the next step, from this row's
       // update -- or, in the run's last step, the ones the reference leaves
       // behind: its last apply_boundary ran on the column-sweep output

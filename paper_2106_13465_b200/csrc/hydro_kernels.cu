@@ -139,7 +139,9 @@ __device__ __forceinline__ Flux riemann(M& m, const Face& L, const Face& R, cons
   } else {
     bool vacuum;
     Flux f;
-    if (memo.match(L.w, R.w)) {
+    if constexpr (std::is_same_v<Mem, NoMemo>) {  // (the fused step's row phase)
+      f = exact10_flux(m, L, R, g, vacuum);
+    } else if (memo.match(L.w, R.w)) {
       f = {memo.f(8), memo.f(9), memo.f(10), memo.f(11)};
       vacuum = memo.f(12) != 0.0;
     } else {
@@ -1466,11 +1468,13 @@ int HB_SWEEP(query_geometry)(Geometry* g) {
   g->ctas_x_exact = ox1 > 0 ? ox1 : 1;
   g->ctas_y_exact = oy1 > 0 ? oy1 : 1;
   int oxy = 0;
-  cudaFuncSetAttribute(sweep_xy_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
-  cudaFuncSetAttribute(sweep_xy_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
-  cudaFuncSetAttribute(sweep_xy_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
-  cudaFuncSetAttribute(sweep_xy_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oxy, sweep_xy_kernel<0, false>, 256, kFSmemBytes);
+  cudaFuncSetAttribute(sweep_xy_kernel<0, false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
+  cudaFuncSetAttribute(sweep_xy_kernel<1, false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
+  cudaFuncSetAttribute(sweep_xy_kernel<0, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
+  cudaFuncSetAttribute(sweep_xy_kernel<1, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytes);
+  cudaFuncSetAttribute(sweep_xy_kernel<0, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytesEx);
+  cudaFuncSetAttribute(sweep_xy_kernel<1, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmemBytesEx);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oxy, sweep_xy_kernel<0, false, 0>, 256, kFSmemBytes);
   g->ctas_xy_per_sm = oxy > 0 ? oxy : 1;
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
@@ -1612,12 +1616,15 @@ void HB_SWEEP(launch_sweep_xy)(const SweepArgs& a0, const CUtensorMap& load, con
   a.seg = (a.seg + 3) / 4 * 4;
   a.nseg = (a.nx + a.seg - 1) / a.seg;
   const bool peer = a.halo_up || a.halo_dn;
-  if (a.last_step) {
-    if (peer) launch_sweep_block(sweep_xy_kernel<1, true>, ctas, 256, kFSmemBytes, s, a, load, store);
-    else launch_sweep_block(sweep_xy_kernel<1, false>, ctas, 256, kFSmemBytes, s, a, load, store);
+  if (a.flux == 1) {  // exact-10 (whole domains: the caller keeps slabs on the split sweeps)
+    if (a.last_step) launch_sweep_block(sweep_xy_kernel<1, false, 1>, ctas, 256, kFSmemBytesEx, s, a, load, store);
+    else launch_sweep_block(sweep_xy_kernel<0, false, 1>, ctas, 256, kFSmemBytesEx, s, a, load, store);
+  } else if (a.last_step) {
+    if (peer) launch_sweep_block(sweep_xy_kernel<1, true, 0>, ctas, 256, kFSmemBytes, s, a, load, store);
+    else launch_sweep_block(sweep_xy_kernel<1, false, 0>, ctas, 256, kFSmemBytes, s, a, load, store);
   } else {
-    if (peer) launch_sweep_block(sweep_xy_kernel<0, true>, ctas, 256, kFSmemBytes, s, a, load, store);
-    else launch_sweep_block(sweep_xy_kernel<0, false>, ctas, 256, kFSmemBytes, s, a, load, store);
+    if (peer) launch_sweep_block(sweep_xy_kernel<0, true, 0>, ctas, 256, kFSmemBytes, s, a, load, store);
+    else launch_sweep_block(sweep_xy_kernel<0, false, 0>, ctas, 256, kFSmemBytes, s, a, load, store);
   }
 }
 

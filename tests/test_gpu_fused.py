@@ -173,3 +173,70 @@ def test_group_slabs_take_fused_steps(gpu, monkeypatch, n, case, bc, nx, schedul
         g.download(grp.planes)
     assert dt_grp == dt_one
     assert np.array_equal(grp.planes.view(np.uint64), one.planes.view(np.uint64))
+
+
+# ---- exact-10 flux on the fused schedule ---------------------------------------
+
+def exact_run(case, nx, ny, steps, bc, seed, schedule, math="bitwise"):
+    grid = P.make_case(case, nx, ny, MODEL, seed=seed)
+    with P.GpuGrid(nx, ny, grid.dx, grid.dy, MODEL, bc, device=0, flux="exact10", math=math) as g:
+        g.set_schedule(schedule)
+        g.upload(grid.planes)
+        dt = g.run(steps)
+        g.download(grid.planes)
+        g.set_timing(True)
+        g.reset_counters()
+        g.run(2)
+        n_xy = g.fused_times()[1]
+    return grid.planes, dt, n_xy
+
+
+@pytest.mark.parametrize("case,nx,ny,steps,bc,seed", [
+    ("corner_blast", 64, 130, 10, "reflect", 0), ("random", 40, 121, 6, "transmit", 31),
+    ("random", 96, 250, 8, "reflect", 32), ("sod_x", 33, 241, 12, "transmit", 0),
+    ("blast", 150, 150, 9, "reflect", 0),
+])
+def test_fused_exact10_matches_the_oracle_bitwise(gpu, case, nx, ny, steps, bc, seed):
+    planes, dt, n_xy = exact_run(case, nx, ny, steps, bc, seed, "fused")
+    assert n_xy == 2, "the fused kernel did not run with the exact-10 flux"
+    ref = O.make_case(case, nx, ny, seed=seed)
+    with O.flux_mode("exact10"):
+        dt_ref = O.run_sequential(ref, steps, bc)
+    if not np.array_equal(planes, ref.u):
+        bad = np.argwhere(planes != ref.u)
+        pytest.fail(f"{len(bad)} values differ from the oracle, first {bad[:4].tolist()}")
+    assert dt == dt_ref
+
+
+def test_fused_exact10_equals_split_in_tolerance_mode(gpu):
+    ps, ds, _ = exact_run("random", 200, 363, 8, "reflect", 12, "split", "tolerance")
+    pf, df, n_xy = exact_run("random", 200, 363, 8, "reflect", 12, "fused", "tolerance")
+    assert n_xy == 2
+    assert np.array_equal(ps.view(np.uint64), pf.view(np.uint64)) and ds == df
+
+
+@pytest.mark.parametrize("axis", ["column", "row"])
+def test_fused_exact10_reports_vacuum_like_the_oracle(gpu, axis):
+    """Two cold halves rushing apart generate vacuum at the centre interface
+    (exact_riemann.cpp:55-57), along i (the column phase finds it) or along j
+    (the row phase does): the reference's validation error, word for word."""
+    nx, ny = (32, 130) if axis == "column" else (40, 128)
+    g = O.make_case("uniform", nx, ny)
+    u = g.u
+    rho, p = 1.0, 0.01
+    ii, jj = np.meshgrid(np.arange(1, nx + 1), np.arange(1, ny + 1), indexing="ij")
+    vel = np.where((ii <= nx // 2) if axis == "column" else (jj <= ny // 2), -3.0, 3.0)
+    u[0, 2:nx + 2, 2:ny + 2] = rho
+    u[1 if axis == "column" else 2, 2:nx + 2, 2:ny + 2] = rho * vel
+    u[2 if axis == "column" else 1, 2:nx + 2, 2:ny + 2] = 0.0
+    u[3, 2:nx + 2, 2:ny + 2] = p / 0.3999999999999999 + 0.5 * rho * vel * vel
+    grid = P.Grid2D(g.nx, g.ny, g.dx, g.dy, g.u.copy())
+    with O.flux_mode("exact10"), pytest.raises(O.CheckerError) as e_ref:
+        O.run_sequential(g, 4, "transmit")
+    assert axis in str(e_ref.value)
+    with P.GpuGrid(nx, ny, grid.dx, grid.dy, MODEL, "transmit", device=0, flux="exact10") as gg:
+        gg.set_schedule("fused")
+        gg.upload(grid.planes)
+        with pytest.raises(P.ValidationError) as e_gpu:
+            gg.run(4)
+    assert str(e_gpu.value) == str(e_ref.value)
