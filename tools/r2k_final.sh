@@ -2,7 +2,7 @@
 # Final measurement pass of round 2 (run under gpurun from the repo root): GPU tests, the
 # default bench line + the reference arm, config 4, ncu captures (fused step on config 3,
 # split sweeps on config 2), the launch list of the bench command.
-O=gpurun_out/r2j
+O=gpurun_out/r2k
 mkdir -p $O
 nvidia-smi > $O/nvidia_smi.txt 2>&1
 timeout 1800 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 $O/pytest_gpu.log

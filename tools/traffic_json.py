@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from ncu_summary import kernel_metrics  # noqa: E402
 
 CELLS = {"cfg0": 256 ** 2, "cfg1": 2048 ** 2, "cfg2": 8192 ** 2, "cfg3": 16384 ** 2, "cfg4": 16384 ** 2}
-out = {"source": "ncu --set full --clock-control none (tools/r2j_final.sh captures: the fused step on config 3, "
+out = {"source": "ncu --set full --clock-control none (tools/r2k_final.sh captures: the fused step on config 3, "
                  "one column and one row sweep on config 2): (dram__bytes_read.sum + dram__bytes_write.sum) / cells",
        "alg_bytes_per_cell": 64}
 for arg in sys.argv[1:]:
