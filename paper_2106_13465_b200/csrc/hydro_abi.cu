@@ -695,11 +695,16 @@ bool launch_graph(hydro_gpu_ctx* c, int steps) {
     entry = &c->graphs.back();
     entry->events.swap(c->pending);
     c->pending.swap(saved);
+    // (the first launch would upload the graph: not inside AUTO's event bracket)
+    if (cudaGraphUpload(entry->exec, c->stream) != cudaSuccess) cudaGetLastError();
   }
+  auto_bracket_begin(c, steps);  // after the capture: device time of the run alone
   if (cudaGraphLaunch(entry->exec, c->stream) != cudaSuccess) {
     cudaGetLastError();
+    c->run_pending = false;
     return false;
   }
+  auto_bracket_end(c);
   if (c->timing) c->pending.insert(c->pending.end(), entry->events.begin(), entry->events.end());
   return true;
 }
@@ -1114,12 +1119,11 @@ int hydro_gpu_run_async(hydro_gpu_ctx* c, int steps) {
   DeviceGuard g(c->device);
   auto_choose(c);
   c->stat_sweeps += 2.0 * steps * (double)c->cfg.nx * (double)c->cfg.ny;
-  auto_bracket_begin(c, steps);
   if (steps >= 2 && launch_graph(c, steps)) {
-    auto_bracket_end(c);
     CUDA_TRY(c, cudaGetLastError());
     return HYDRO_GPU_OK;
   }
+  auto_bracket_begin(c, steps);
   int rc = enqueue_run(c, steps);
   if (rc) return rc;
   auto_bracket_end(c);
