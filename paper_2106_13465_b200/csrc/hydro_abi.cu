@@ -13,8 +13,13 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#if defined(__x86_64__) || defined(_M_X64)
+#include <emmintrin.h>
+#endif
+
 #include <cmath>
 #include <cstdarg>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -869,6 +874,47 @@ int ensure_stage(hydro_gpu_ctx* c, bool pinned) {
   return HYDRO_GPU_OK;
 }
 
+// memcpy with non-temporal stores (x86-64: SSE2 is baseline): the staging
+// copies stream gigabytes once through the host, and regular stores would
+// first read every destination line for ownership -- a third of the copy's
+// memory traffic.  Unaligned heads and tails go through memcpy.
+void stream_copy(char* dst, const char* src, size_t n) {
+#if defined(__x86_64__) || defined(_M_X64)
+  static const bool nt = [] {  // HYDRO_GPU_COPY_NT=0: plain memcpy (A/B)
+    const char* e = std::getenv("HYDRO_GPU_COPY_NT");
+    return !(e && e[0] == '0');
+  }();
+  if (n < 4096 || !nt) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  const size_t head = (16 - ((uintptr_t)dst & 15)) & 15;
+  if (head) {
+    std::memcpy(dst, src, head);
+    dst += head;
+    src += head;
+    n -= head;
+  }
+  const size_t blocks = n / 64;
+  for (size_t b = 0; b < blocks; ++b) {
+    const __m128i x0 = _mm_loadu_si128((const __m128i*)(src) + 0);
+    const __m128i x1 = _mm_loadu_si128((const __m128i*)(src) + 1);
+    const __m128i x2 = _mm_loadu_si128((const __m128i*)(src) + 2);
+    const __m128i x3 = _mm_loadu_si128((const __m128i*)(src) + 3);
+    _mm_stream_si128((__m128i*)(dst) + 0, x0);
+    _mm_stream_si128((__m128i*)(dst) + 1, x1);
+    _mm_stream_si128((__m128i*)(dst) + 2, x2);
+    _mm_stream_si128((__m128i*)(dst) + 3, x3);
+    src += 64;
+    dst += 64;
+  }
+  _mm_sfence();
+  if (n & 63) std::memcpy(dst, src, n & 63);
+#else
+  std::memcpy(dst, src, n);
+#endif
+}
+
 // rows [0, n) of `row_bytes` each, src/dst strides in bytes, on up to 16 threads
 void par_copy_rows(char* dst, size_t dst_stride, const char* src, size_t src_stride, size_t n,
                    size_t row_bytes) {
@@ -881,15 +927,15 @@ void par_copy_rows(char* dst, size_t dst_stride, const char* src, size_t src_str
   unsigned nt = std::thread::hardware_concurrency();
   nt = nt < 1 ? 1 : (nt > cap ? cap : nt);
   if (total < (4u << 20)) nt = 1;
-  // dense rows on both sides (a Grid2D plane <-> the pinned band): one large
-  // memcpy per thread, which libc streams with non-temporal stores
+  // dense rows on both sides (a Grid2D plane <-> the pinned band): one copy
+  // per thread
   const bool dense = dst_stride == row_bytes && src_stride == row_bytes;
   auto work = [&](size_t a, size_t b) {
     if (dense) {
-      std::memcpy(dst + a * row_bytes, src + a * row_bytes, (b - a) * row_bytes);
+      stream_copy(dst + a * row_bytes, src + a * row_bytes, (b - a) * row_bytes);
       return;
     }
-    for (size_t r = a; r < b; ++r) std::memcpy(dst + r * dst_stride, src + r * src_stride, row_bytes);
+    for (size_t r = a; r < b; ++r) stream_copy(dst + r * dst_stride, src + r * src_stride, row_bytes);
   };
   if (nt == 1) {
     work(0, n);
