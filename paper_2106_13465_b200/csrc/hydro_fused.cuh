@@ -80,6 +80,9 @@ constexpr int kFNS = HB_FNS;                      // slots (chunks in hand-over)
 // read their slot yet (cp.async.bulk.wait_group.read 1), so a warp never
 // waits for the stores it has just issued.
 constexpr int kFLag = HB_FLAG;
+#ifndef HB_FONEBAR
+#define HB_FONEBAR 1
+#endif
 
 static_assert(kFLag >= 1 && kFLag <= 2 && kFLag < kFNS, "slot release lag");
 constexpr uint32_t kFSlotOff = kFNBA * kFChunkBytes;
@@ -635,12 +638,22 @@ __global__ void __launch_bounds__(256, 1)
           fence_async_smem();  // slot writes -> the row warps' TMA stores (skipped rows)
           bar_arrive(kFBarFull + (int)sl, 256);
           ++m;
-          bar_sync(kFBarCol, 128);  // input chunk q is free in every lane
+          // input chunk q is free once every column warp is here: the next
+          // slot's barrier (all 128 column threads sync on it) says so, else
+          // the column warps' own
+#if HB_FONEBAR
+          const bool joined = !last && m >= (unsigned)kFNS;
+          if (joined) acquire(m);
+          else bar_sync(kFBarCol, 128);
+#else
+          const bool joined = false;
+          bar_sync(kFBarCol, 128);
+#endif
           if (tid == 0 && q + kFNBA < nq) {
             fence_async_smem();
             issue(q + kFNBA);
           }
-          if (!last) acquire(m);
+          if (!last && !joined) acquire(m);
           return slots0 + (m % kFNS) * kFSlotBytes;
         };
         FusedCol<decltype(chunk)> col{chunk};
