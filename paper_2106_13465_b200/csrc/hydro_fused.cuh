@@ -91,7 +91,9 @@ constexpr uint32_t kFHdrOff = kFBarOff + kFNBA * 8;
 constexpr uint32_t kFFlagOff = kFHdrOff + kFNS * 32;
 constexpr uint32_t kFUniOff = kFFlagOff + 16;       // per slot: FusedUni
 constexpr uint32_t kFUniBytes = 160;
-constexpr uint32_t kFMemoOff = kFUniOff + kFNS * kFUniBytes;  // exact-10: the column warps' memos
+constexpr uint32_t kFEdgeOff = kFUniOff + kFNS * kFUniBytes;  // row warps' wall-band memos (EdgeMemo)
+constexpr uint32_t kFEdgeBytes = 80;
+constexpr uint32_t kFMemoOff = kFEdgeOff + 4 * 2 * kFEdgeBytes;  // exact-10: the column warps' memos
 constexpr int kFSmemBytes = (int)kFMemoOff + 128;             // + alignment
 constexpr int kFSmemBytesEx = kFSmemBytes + 13 * 1024;
 
@@ -140,6 +142,19 @@ struct RowMemo {
   Cons u;      // a state whose uniform-window row update was the identity
   double spd;  // its dt signal speed
 };
+
+// The same memo for the rows of a band at a y-wall, whose ghost columns hold
+// the wall's image G of the interior state U (reflecting walls: the normal
+// momentum negated, which differs from U even at rest: -0 against +0): a row
+// with U in every interior column and G in every ghost column whose update
+// this warp has already evaluated to the identity in this launch.  One per
+// row warp and wall side, in shared memory.
+struct EdgeMemo {
+  double u[4], g[4];  // r, mom_y, mom_x, E (row orientation)
+  double spd;
+  double valid;
+};
+static_assert(sizeof(EdgeMemo) == kFEdgeBytes, "EdgeMemo layout");
 
 // What a row contributes: the largest dt signal speed, the first errors (this
 // step's, and the dt of the next step's), uniform-window updates taken.
@@ -275,8 +290,9 @@ __device__ __forceinline__ bool row_eval(const Cons (&u)[4], const bool (&outk)[
 // orientation (the row sweep's): mom_a = mom_y (var 2), mom_b = mom_x (var 1).
 template <int FLUX>
 __device__ __forceinline__ void fused_row(uint32_t at, int lane, const RowGeo& rg, int ny,
-                                          const Gas& g, double dtdx, RowMemo& memo, RowAcc& acc,
-                                          Cons (&u)[4], Cons (&out)[4], bool (&outk)[4]) {
+                                          const Gas& g, double dtdx, RowMemo& memo, EdgeMemo* edge,
+                                          RowAcc& acc, Cons (&u)[4], Cons (&out)[4],
+                                          bool (&outk)[4]) {
   {
     const uint8_t* p = hb_smem + at + (12 + 4 * lane) * 8;
     const double2 r01 = *(const double2*)(p), r23 = *(const double2*)(p + 16);
@@ -316,6 +332,36 @@ __device__ __forceinline__ void fused_row(uint32_t at, int lane, const RowGeo& r
     acc.spd = smax(acc.spd, memo.spd);
     return;
   }
+  // a band at a y-wall: U in the interior columns, the wall's image G in the
+  // ghost columns (see EdgeMemo)
+  const bool wall_l = rg.jlo < 1, wall_r = rg.jhi > ny;
+  bool pat = false;
+  Cons G = ref;
+  EdgeMemo* const em = edge + (wall_l ? 0 : 1);
+  if (!uni && (wall_l | wall_r)) {
+    const uint8_t* pg = hb_smem + at + ((wall_l ? 0 : ny + 1) - rg.j0 + 16) * 8;
+    G = {*(const double*)pg, *(const double*)(pg + 2 * kFVarBytesS), *(const double*)(pg + kFVarBytesS),
+         *(const double*)(pg + 3 * kFVarBytesS)};
+    bool okc = true;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int j = rg.jb + k;
+      j = j < rg.jlo ? rg.jlo : (j > rg.jhi ? rg.jhi : j);
+      okc &= same_bits(u[k], (j < 1 || j > ny) ? G : ref);
+    }
+    pat = __all_sync(0xffffffffu, okc);
+    if (pat && em->valid != 0.0 &&
+        same_bits(Cons{em->u[0], em->u[1], em->u[2], em->u[3]}, ref) &&
+        same_bits(Cons{em->g[0], em->g[1], em->g[2], em->g[3]}, G)) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        out[k] = u[k];
+        if (outk[k]) ++acc.nskip;
+      }
+      acc.spd = smax(acc.spd, em->spd);
+      return;
+    }
+  }
   RowAcc r;
   r.clear();
   bool ident;
@@ -351,10 +397,22 @@ __device__ __forceinline__ void fused_row(uint32_t at, int lane, const RowGeo& r
   }
   // a uniform row whose update was the identity on every output: remember
   // the state for this launch
-  if (uni && __all_sync(0xffffffffu, ident)) {
+  const bool all_ident = __all_sync(0xffffffffu, ident);
+  const double sp_ref = shfl_d(sp0, 1);
+  if (uni && all_ident) {
     memo.valid = true;
     memo.u = ref;
-    memo.spd = shfl_d(sp0, 1);
+    memo.spd = sp_ref;
+  }
+  if (pat && all_ident) {
+    __syncwarp();
+    if (lane == 0) {
+      em->u[0] = ref.r; em->u[1] = ref.ma; em->u[2] = ref.mb; em->u[3] = ref.e;
+      em->g[0] = G.r; em->g[1] = G.ma; em->g[2] = G.mb; em->g[3] = G.e;
+      em->spd = sp_ref;
+      em->valid = 1.0;
+    }
+    __syncwarp();
   }
 }
 
@@ -726,6 +784,9 @@ __global__ void __launch_bounds__(256, 1)
     const size_t pitch = a.pitch;
     RowMemo memo{};
     memo.valid = false;
+    EdgeMemo* const edge = (EdgeMemo*)(hb_smem + pad + kFEdgeOff) + 2 * wr;
+    if (lane < 2) edge[lane].valid = 0.0;
+    __syncwarp();
     bool wrote_peer = false;
     RowAcc acc, done;
     acc.clear();
@@ -802,7 +863,7 @@ __global__ void __launch_bounds__(256, 1)
       rg.dt_base = error_key(a.step + 1, 0, gi, 0, 0, 0);
       Cons uin[4], out[4];
       bool outk[4];
-      fused_row<FLUX>(at, lane, rg, ny, g, dtdx, memo, acc, uin, out, outk);
+      fused_row<FLUX>(at, lane, rg, ny, g, dtdx, memo, edge, acc, uin, out, outk);
       // x-wall ghost rows (grid.cpp:26-42): of the next step, from this row's
       // update -- or, in the run's last step, the ones the reference leaves
       // behind: its last apply_boundary ran on the column-sweep output
