@@ -86,7 +86,7 @@ enum hydro_gpu_math { HYDRO_GPU_MATH_BITWISE = 0, HYDRO_GPU_MATH_TOLERANCE = 1 }
  * runs: the share of cell updates taken by the
  * uniform-window identity (fused above 0.6: memory-bound flow) and the
  * event-timed device time per step of each schedule (an untimed schedule is
- * tried once unless the share is decisive); a context's first run is fused. */
+ * tried once); a context's first run is fused. */
 enum hydro_gpu_schedule {
   HYDRO_GPU_SCHEDULE_SPLIT = 0,
   HYDRO_GPU_SCHEDULE_FUSED = 1,

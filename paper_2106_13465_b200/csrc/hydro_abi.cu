@@ -330,9 +330,10 @@ void enqueue_xy(hydro_gpu_ctx* c, int step, bool a_to_b, bool last) {
 // keeps forcing redo passes on a small grid.  Two inputs, both from the
 // context's own completed runs: the share of uniform-window updates (the
 // sweeps' counters) and the event-timed device time per step of each
-// schedule.  Untimed schedules are tried once unless the share is decisive
-// (>= 0.98: fused, <= 0.2: split); a timing is forgotten when the share has
-// moved by more than 0.1 since.  The results are bitwise the same either way;
+// schedule.  An untimed schedule is tried once (fused not on dense flow, share
+// <= 0.2); a timing is forgotten when the share the other schedule measures
+// has moved by more than 0.1 between two of its runs.  (The share alone does not decide for fused: a 256^2 blast is 99%
+// uniform windows and 4x slower fused in the bitwise arithmetic.)  The results are bitwise the same either way;
 // the first run of a context is fused.
 constexpr double kAutoFusedShare = 0.6;
 void auto_choose(hydro_gpu_ctx* c) {
@@ -353,18 +354,23 @@ void auto_choose(hydro_gpu_ctx* c) {
   if (c->run_pending) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, c->run_ev[0], c->run_ev[1]) == cudaSuccess) {
-      c->ms_step[c->run_fused] = (double)ms / c->run_steps;
-      c->ms_share[c->run_fused] = share;
+      const int r = c->run_fused ? 1 : 0;
+      // the flow has changed since this schedule was last timed (shares are
+      // compared per schedule: the two count uniform windows differently):
+      // the other schedule's timing is stale
+      if (c->ms_step[r] >= 0 && share >= 0 && c->ms_share[r] >= 0 &&
+          std::fabs(share - c->ms_share[r]) > 0.1)
+        c->ms_step[1 - r] = -1.0;
+      c->ms_step[r] = (double)ms / c->run_steps;
+      c->ms_share[r] = share;
     } else {
       cudaGetLastError();
     }
     c->run_pending = false;
   }
-  for (int k = 0; k < 2; ++k)
-    if (c->ms_step[k] >= 0 && share >= 0 && std::fabs(share - c->ms_share[k]) > 0.1) c->ms_step[k] = -1.0;
   const bool by_share = share < 0 || share >= kAutoFusedShare;
   if (c->ms_step[0] >= 0 && c->ms_step[1] >= 0) c->auto_fused = c->ms_step[1] <= c->ms_step[0];
-  else if (c->ms_step[1] >= 0 && share >= 0 && share < 0.98) c->auto_fused = false;  // try split once
+  else if (c->ms_step[1] >= 0) c->auto_fused = false;                                // try split once
   else if (c->ms_step[0] >= 0 && share > 0.2) c->auto_fused = true;                  // try fused once
   else c->auto_fused = by_share;
 }
