@@ -406,7 +406,10 @@ __device__ __forceinline__ bool walk_strip_impl(int ka, int kb, Src& src, Sink& 
   }
   if (kSkip) {
     if (!probe) --src.skip_cool;
-    else if (!__any_sync(0xffffffffu, saw && src.active)) src.skip_cool = kSkipCool;
+    // (a warp without an active lane -- the fused step's last band -- has seen
+    // nothing either way and keeps probing)
+    else if (__any_sync(0xffffffffu, src.active) && !__any_sync(0xffffffffu, saw && src.active))
+      src.skip_cool = kSkipCool;
   }
   // the memo carries over to this thread's next work item only if its
   // entries are exact: written by an exact pass, or by a fast pass that kept
