@@ -495,6 +495,9 @@ class Measured:
                "frac": achieved / peak, "traffic": traffic,
                "traffic_source": f"profiles/traffic.json {tkey}" if traffic else None,
                "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms,
+               "peak_note": "the peak is a measured copy rate (torch b.copy_(a), MEASURED_PEAKS.json), "
+                            "not the DRAM's nominal 8 TB/s: a streaming kernel can reach or slightly "
+                            "exceed it (frac ~1.0)",
                "alg_bytes_note": "64 B per cell per launch: one read + one write of the 4 fp64 "
                                  "fields (a fused launch completes a whole cell-step with them)",
                "step": {"sweeps_ms_per_time_step": step_ms,
